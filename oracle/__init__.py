@@ -1,0 +1,26 @@
+"""CPU oracle for the SFSeg / SFSeg++ power-iteration hot path (TEST INFRASTRUCTURE).
+
+This package is test infrastructure only.  It may be imported, called or
+executed ONLY by ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs.  The product path
+(``paper_2212_08058_b200``) never imports it and shares no code with it.
+
+It is a plain, slow, float64 numpy transcription of the paper's definitions
+(arxiv 2212.08058, /root/reference/PAPER.md) -- see ``sfseg_oracle.py`` for the
+per-function citations and ``dense.py`` for the explicit adjacency matrix used
+to pin it.  Pins live in ``tests/test_oracle_pins.py``.
+
+Parity status per function:
+  gaussian_taps          pinned (SPEC worked value S:118, closed-form sums)
+  combine                pinned (SPEC worked values S:187-189)
+  gaussian_filter        pinned (direct triple loop, impulse response, dense M)
+  power_iterate          pinned (dense M brute force, eigh closed form, PF invariants)
+  normalize_l2           pinned
+  threshold              parity unpinned beyond its definition (SURVEY A12 reading)
+  power_iterate_backward pinned (central finite differences, Euler identity)
+"""
+from .sfseg_oracle import (  # noqa: F401
+    ACT_IDENTITY, ACT_SIGMOID, THR_PER_FRAME_MAX, THR_GLOBAL_MAX, THR_ABSOLUTE,
+    DegenerateError, gaussian_taps, combine, correlate_axis, gaussian_filter,
+    apply_M, normalize_l2, power_iterate, threshold, power_iterate_backward,
+)
