@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark of the SFSeg power-iteration hot path on B200 (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path over one synthetic volume:
+fused channel combine + K_iter power iterations (temporal pass, fused spatial
+pass with F multiplies and norm) + final normalisation + per-frame threshold
+(SURVEY.md §8(a) rows a1-a9).  At N=1 the workload is BASELINE.json configs[1]
+("c2": 1x70x480x854, C=1, sigma_t=2, sigma_s=8, 15 iterations, tau=0.5).
+For N>1 (torchrun, one rank per GPU) every rank solves its own c2 volume
+(data-parallel over independent volumes, weak scaling, no data-path collective).
+
+metric: voxel-iterations/s = B*T*H*W*K_iter per step, whole job.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "voxel-iterations/sec (T*H*W*iters/s)"
+UNIT = "voxel-iterations/s"
+ALU_PEAK_FMA_PER_CLK_PER_SM = 128     # FP32 lanes per SM (B200_PROFILING.md / blackwell guide)
+SM_COUNT = 148
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        def num(s):
+            try:
+                return float(s)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in self.rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in self.rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_sample(cfg_name: str, t_crop: int = 0):
+    """Time the oracle (as it stands) on a bounded sample: one power iteration of
+    the workload (optionally on the first t_crop frames).  Returns (vox_iter_per_s, secs, sample)."""
+    import numpy as np
+    import oracle as O
+    import workloads as WL
+    cfg = WL.get_config(cfg_name)
+    if t_crop:
+        wl = WL.generate(cfg_name, t_range=(0, min(t_crop, cfg.T)))
+    else:
+        wl = WL.generate(cfg_name)
+    F, _ = O.combine(wl.ch, wl.w, wl.b, cfg.act)
+    gt, gs = O.gaussian_taps(cfg.sigma_t, cfg.radius_t), O.gaussian_taps(cfg.sigma_s, cfg.radius_s)
+    t0 = time.perf_counter()
+    O.power_iterate(F, gt, gs, 1)
+    dt = time.perf_counter() - t0
+    nvox = F.size
+    sample = (f"1 of {cfg.K} power iterations (combine excluded) of {cfg_name} "
+              f"{'x'.join(str(s) for s in F.shape)} in numpy float64, single thread")
+    return nvox / dt, dt, sample
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import workloads as WL
+    cfg = WL.get_config(args.config)
+    t_crop = 16 if args.config in ("c2", "c3", "probe") else 8
+    for _ in range(args.warmup):
+        cpu_oracle_sample(args.config, t_crop)
+    total_t, total_units = 0.0, 0
+    sample = ""
+    for _ in range(args.steps):
+        v, dt, sample = cpu_oracle_sample(args.config, t_crop)
+        total_t += dt
+        total_units += v * dt
+    value = total_units / total_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (workloads/ generator; DAVIS-2016-shaped blobs)",
+        "config": {"workload": f"{args.config}: {cfg.note}", "shape": [cfg.B, cfg.T, cfg.H, cfg.W], "C": cfg.C,
+                   "sigma_t": cfg.sigma_t, "sigma_s": cfg.sigma_s, "radius_t": cfg.radius_t,
+                   "radius_s": cfg.radius_s, "iters": cfg.K},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2212_08058_b200 as sf
+    import workloads as WL
+
+    world, rank, local = _dist()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    sf.lib()
+
+    cfg = WL.get_config(args.config)
+    wl = WL.generate(args.config, with_mask=False)
+    B, Cn, T, H, W = wl.ch.shape
+    K = cfg.K
+    gauss = sf.Gauss(cfg.sigma_t, cfg.sigma_s, cfg.radius_t, cfg.radius_s)
+    ch_host = torch.from_numpy(wl.ch).pin_memory()
+    ch = ch_host.to(dev)
+    solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev)
+    x = torch.empty((B, T, H, W), dtype=torch.float32, device=dev)
+    mask = torch.empty((B, T, H, W), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        solver.forward(ch, wl.w, wl.b, cfg.act, x_out=x, check=False)
+        solver.threshold(x, cfg.tau, sf.THR_PER_FRAME_MAX, mask=mask)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    solver.sync()   # raises on a device-detected error
+
+    clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
+                          if os.environ.get("CUDA_VISIBLE_DEVICES", "").isdigit() else local)
+    clocks.start()
+    time.sleep(0.2)
+    # inputs (ch 115 MB + F/p/v 344 MB at c2) exceed the 126 MB L2: no flush needed
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sf.profile_enable(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    sf.profile_enable(False)
+    prof = sf.profile_read()
+    solver.sync()
+    if world > 1:
+        dist.barrier()
+    time.sleep(0.1)
+    clocks.stop()
+    ms = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    vox = B * T * H * W
+    units_per_step = vox * K
+    value = world * units_per_step * args.steps / (ms_max / 1e3)
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    peaks, peaks_src = _peaks()
+    sp_ms, sp_n = prof["spass"]
+    tp_ms, tp_n = prof["tpass"]
+    sp_avg_s = sp_ms / max(sp_n, 1) / 1e3
+    tp_avg_s = tp_ms / max(tp_n, 1) / 1e3
+    r_s, r_t = cfg.radius_s, cfg.radius_t
+    fma_per_vox = 2 * (2 * r_s + 1) + 3            # x taps + y taps + F*u, F*y, y*y
+    flops_per_launch = 2.0 * fma_per_vox * vox
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    alu_peak_tflops = SM_COUNT * ALU_PEAK_FMA_PER_CLK_PER_SM * 2 * sm_max * 1e6 / 1e12
+    achieved = flops_per_launch / sp_avg_s / 1e12 if sp_n else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(args.config, {}).get("spass_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    tp_bytes = 8.0 * B * T * H * W
+    roofline = {
+        "kernel": f"spass_kernel<R={r_s}> (fused x/y Gaussian + F multiplies + norm)",
+        "bound": "alu", "achieved": achieved, "peak": alu_peak_tflops, "unit": "TFLOP/s",
+        "frac": (achieved / alu_peak_tflops) if achieved else None, "traffic": traffic,
+        "peak_source": f"derived: {SM_COUNT} SM x {ALU_PEAK_FMA_PER_CLK_PER_SM} FP32 FMA/clk x 2 x "
+                       f"{sm_max:.0f} MHz ({peaks_src} sm_max_mhz)",
+        "algorithmic_flops_per_launch": flops_per_launch,
+        "launch_ms": sp_avg_s * 1e3, "launches": sp_n,
+        "share_of_step": sp_ms / ms if ms > 0 else None,
+        "tpass": {"launch_ms": tp_avg_s * 1e3, "launches": tp_n,
+                  "achieved_GBps": tp_bytes / tp_avg_s / 1e9 if tp_n else None, "peak_GBps": hbm_peak,
+                  "bound": "hbm"},
+        "path_hbm_frac_algorithmic_12B": 12.0 * value / world / 1e9 / hbm_peak,
+    }
+
+    # ---------------------------------------------------------------- e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        d_ch = torch.empty_like(ch)
+        x_host = torch.empty((B, T, H, W), dtype=torch.float32).pin_memory()
+        m_host = torch.empty((B, T, H, W), dtype=torch.uint8).pin_memory()
+        e2e_steps = max(1, min(args.steps, 10))
+        sf.solve_host(ch_host, wl.w, gauss, K, cfg.tau, solver, d_ch, x, mask, x_host, m_host)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            sf.solve_host(ch_host, wl.w, gauss, K, cfg.tau, solver, d_ch, x, mask, x_host, m_host)
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * units_per_step * e2e_steps / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(ch_host.numel() * 4),
+               "d2h_bytes_per_step": int(x_host.numel() * 4 + m_host.numel()),
+               "steps": e2e_steps, "api": "sfseg_solve_host (pinned host in/out)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, sample = cpu_oracle_sample(args.config)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, "seconds": dt}
+
+    if rank == 0:
+        ck = clocks.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (workloads/ generator; DAVIS-2016-shaped blobs, seed 0)",
+            "config": {"workload": f"{args.config}: {cfg.note}", "shape": [B, T, H, W], "C": Cn,
+                       "sigma_t": cfg.sigma_t, "sigma_s": cfg.sigma_s, "radius_t": r_t, "radius_s": r_s,
+                       "iters": K, "tau": cfg.tau, "parallelism": f"dp{world} (one volume per GPU)",
+                       "l2": "inputs > L2 (ch 115 MB + F/p/v 344 MB vs 126 MB L2); no flush"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": (2 * K + 4) * args.steps,
+            "clocks": {k: ck[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+            "clock_samples": ck["samples"],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "probe"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,182 @@
+/*
+ * sfseg.h -- C ABI of the B200-native SFSeg / SFSeg++ power-iteration hot path.
+ *
+ * The method (arxiv 2212.08058, /root/reference/PAPER.md, "P:<lines>"):
+ *   principal eigenvector of the implicit space-time pixel graph
+ *   M_ij = F_i F_j G(i - j)        (Eq.1/2, unary-only case p = 1,
+ *                                   constant pairwise map -- SURVEY.md §8(c) A3)
+ *   by power iteration in 3D-filtering form (Eq.4/7/8):
+ *   y_k = F . (G_3D * (F . x_{k-1})),   x_k = y_k / ||y_k||_2,
+ *   with F the learned channel combine of Eq.9 and G_3D the
+ *   separable Gaussian of P:319 (normalised 1D taps, radius ceil(3 sigma),
+ *   zero padding -- readings A5, A6, A8).
+ *
+ * Conventions (all entry points):
+ *   - Every pointer is a DEVICE pointer unless its name ends in _host.
+ *   - Dense layouts: channels [B][C][T][H][W] fp32, volumes [B][T][H][W] fp32,
+ *     masks [B][T][H][W] uint8; W fastest, no padding, C order.
+ *   - The caller owns all memory (PyTorch allocates); the library never
+ *     allocates or frees device memory and keeps no hidden global state other
+ *     than a per-process cache of TMA descriptors' driver entry point.
+ *   - `stream` is a cudaStream_t passed as void*; all work is enqueued on it.
+ *     Entry points do NOT synchronise unless stated ("syncs").
+ *   - Validation first: every argument is checked before any launch; on a
+ *     validation error nothing is written and nothing is launched.
+ *   - Device-detected errors (zero norm, non-finite norm) are recorded in the
+ *     workspace's error word and reported by sfseg_sync_status().
+ *   - No C++ exception crosses the ABI.
+ *   - Results are bitwise reproducible for a fixed (shape, build, GPU model):
+ *     all reductions are fixed-order (fp32 within a CTA, fp64 across CTAs).
+ */
+#ifndef SFSEG_H_
+#define SFSEG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFSEG_ABI_VERSION 1
+
+typedef enum {
+  SFSEG_OK = 0,
+  SFSEG_ERR_INVALID_ARGUMENT = 1, /* null pointer, C<1, K<1, sigma<=0, tau non-finite, bad enum */
+  SFSEG_ERR_SHAPE = 2,            /* B,T,H,W < 1; radius above the compiled maximum */
+  SFSEG_ERR_WORKSPACE = 3,        /* workspace too small or not 256-byte aligned */
+  SFSEG_ERR_DEGENERATE = 4,       /* some ||y_k|| == 0 (e.g. F == 0); device-detected */
+  SFSEG_ERR_NONFINITE = 5,        /* NaN/Inf reached a norm; device-detected */
+  SFSEG_ERR_CUDA = 6,             /* a CUDA runtime / driver call failed */
+  SFSEG_ERR_NCCL = 7,             /* a NCCL call failed (multi-GPU) */
+  SFSEG_ERR_UNSUPPORTED = 8       /* feature not available in this build */
+} sfseg_status;
+
+/* Dense volume shape.  When time-sharded, T is the LOCAL slab length. */
+typedef struct { int64_t B, T, H, W; } sfseg_shape;
+
+/* Separable Gaussian G_3D.  radius < 0 => ceil(3 sigma) (reading A5).
+ * 1D taps g[k] = exp(-k^2/(2 sigma^2)) / sum_{|j|<=r} exp(-j^2/(2 sigma^2))
+ * (reading A6); the same sigma_s / radius_s is used for the y and x axes. */
+typedef struct { double sigma_t, sigma_s; int32_t radius_t, radius_s; } sfseg_gauss;
+
+typedef enum { SFSEG_ACT_IDENTITY = 0, SFSEG_ACT_SIGMOID = 1 } sfseg_act;
+typedef enum {
+  SFSEG_THR_PER_FRAME_MAX = 0,  /* mask = x > tau * max_frame(x)   (reading A12, default) */
+  SFSEG_THR_GLOBAL_MAX = 1,     /* mask = x > tau * max_volume(x) */
+  SFSEG_THR_ABSOLUTE = 2        /* mask = x > tau */
+} sfseg_thr_mode;
+
+/* Multi-GPU time-slab sharding.  NULL => single GPU. */
+typedef struct sfseg_comm sfseg_comm;
+typedef struct {
+  sfseg_comm* comm;   /* from sfseg_comm_create */
+  int64_t T_global;   /* frames of the whole volume */
+  int64_t t_offset;   /* first global frame of this rank's slab */
+} sfseg_dist;
+
+/* Per-iteration statistics written by sfseg_power_iterate (DEVICE memory,
+ * double [B][K][3]):  [..][k][0] = nu_k  = ||y_k||_2 (normaliser of Eq.8)
+ *                      [..][k][1] = gain n_k = nu_k / ||x_{k-1}||_2 (x_0 not unit; A10)
+ *                      [..][k][2] = Rayleigh quotient x_{k-1}^T M x_{k-1} / ||x_{k-1}||^2
+ *                                   (Eq.3; only when want_rayleigh != 0, else 0). */
+#define SFSEG_STATS_PER_ITER 3
+
+const char* sfseg_status_string(sfseg_status s);
+int32_t sfseg_abi_version(void);
+/* Text of the last CUDA error seen by this thread inside the library (for SFSEG_ERR_CUDA). */
+const char* sfseg_last_cuda_error(void);
+
+/* Largest radii compiled into this build (spatial, temporal). */
+void sfseg_max_radii(int32_t* radius_s_max_host, int32_t* radius_t_max_host);
+
+/* Workspace needed by sfseg_power_iterate / sfseg_power_iterate_backward for
+ * this problem (want_tape != 0: also the bytes of the tape buffer that a
+ * forward must record for a later backward).  Host outputs; no GPU work. */
+sfseg_status sfseg_workspace_bytes(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K,
+                                   int32_t want_tape, const sfseg_dist* dist_or_null,
+                                   size_t* ws_bytes_host, size_t* tape_bytes_host);
+
+/* Eq.9 / Alg.1 lines 1-2:
+ *   F = act(sum_c w_c ch_c + b), act = identity (single channel "without the
+ *   sigmoid") or sigmoid 1/(1+e^{-z}) (the printed e^{x} is a typo, A1).
+ * ch [B][C][T][H][W] -> F [B][T][H][W].  w_host: C floats in host memory. */
+sfseg_status sfseg_combine_channels(const float* ch, int32_t C, sfseg_shape shape,
+                                    const float* w_host, float b, int32_t act,
+                                    float* F, void* stream);
+
+/* K power iterations (Eq.4/7/8, Alg.1 Step 2 + normalise)
+ * from x_0 = F (Alg.1 line 3) or from x0_or_null ([B][T][H][W]).
+ *   ch/C/w_host/b/act: as sfseg_combine_channels (combine fused into the solve).
+ *   x_out  [B][T][H][W]: x_K, unit L2 norm per volume (reading A9).
+ *   F_out_or_null [B][T][H][W]: the combined F (needed by a later backward).
+ *   stats_or_null: DEVICE double [B][K][3] (see SFSEG_STATS_PER_ITER).
+ *   want_rayleigh: also compute the Rayleigh quotient (+4 B/voxel/iteration).
+ *   tape_or_null: if non-NULL (size from sfseg_workspace_bytes with want_tape),
+ *     records what sfseg_power_iterate_backward needs.
+ *   ws / ws_bytes: device workspace, 256-byte aligned, >= sfseg_workspace_bytes.
+ *   dist_or_null: time-slab sharding; NULL => whole volume on this GPU.
+ * Asynchronous; call sfseg_sync_status(ws, stream) to learn device errors. */
+sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host, float b,
+                                 int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
+                                 const float* x0_or_null, float* x_out, float* F_out_or_null,
+                                 double* stats_or_null, int32_t want_rayleigh, void* tape_or_null,
+                                 void* ws, size_t ws_bytes, const sfseg_dist* dist_or_null,
+                                 void* stream);
+
+/* Gradient of L(x_K) w.r.t. the channel weights and bias through the K
+ * unrolled iterations ("through the full spectral algorithm", P:42, P:212-213,
+ * P:232); recursion of SURVEY.md Appendix A.  Inputs are those of the forward
+ * call that wrote `tape` (same ch, w, b, act, shape, gauss, K, x0).
+ *   dL_dx [B][T][H][W]: dL/dx_K supplied by the caller (the loss is not in the ABI).
+ *   dL_dw_host: C doubles; dL_db_host: 1 double (host memory).
+ * Syncs `stream` once at the end (host outputs); returns device errors too. */
+sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const float* w_host,
+                                          float b, int32_t act, sfseg_shape shape,
+                                          sfseg_gauss gauss, int32_t K,
+                                          const float* x0_or_null, const void* tape,
+                                          const float* dL_dx, double* dL_dw_host,
+                                          double* dL_db_host, void* ws, size_t ws_bytes,
+                                          const sfseg_dist* dist_or_null, void* stream);
+
+/* Hard threshold ("simply obtained by thresholding"): uint8 mask.
+ * Mode per sfseg_thr_mode; strict '>' in fp32 against tau*max; a frame (or
+ * volume) whose max is <= 0 yields zeros.  ws: >= sfseg_threshold_ws_bytes. */
+size_t sfseg_threshold_ws_bytes(sfseg_shape shape);
+sfseg_status sfseg_threshold(const float* x, sfseg_shape shape, float tau, int32_t mode,
+                             uint8_t* mask, void* ws, size_t ws_bytes, void* stream);
+
+/* Synchronise `stream`, then read and clear the device error word in `ws`.
+ * Returns SFSEG_OK, SFSEG_ERR_DEGENERATE, SFSEG_ERR_NONFINITE or SFSEG_ERR_CUDA. */
+sfseg_status sfseg_sync_status(void* ws, void* stream);
+
+/* End-to-end convenience over HOST buffers (used for the e2e measurement):
+ * H2D of ch_host (pinned or pageable) into d_ch, sfseg_power_iterate, then
+ * sfseg_threshold, then D2H of x and mask into x_out_host / mask_out_host
+ * (either may be NULL), then sync.  Device buffers d_ch ([B][C][T][H][W]),
+ * d_x ([B][T][H][W]) and d_mask are caller-owned scratch.  Syncs. */
+sfseg_status sfseg_solve_host(const float* ch_host, int32_t C, const float* w_host, float b,
+                              int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
+                              float tau, int32_t thr_mode, float* d_ch, float* d_x,
+                              uint8_t* d_mask, float* x_out_host, uint8_t* mask_out_host,
+                              void* ws, size_t ws_bytes, void* stream);
+
+/* ---- optional per-kernel timing (benchmark instrumentation) ----
+ * When enabled, every pass launch is bracketed by CUDA events recorded on the
+ * launching stream.  sfseg_profile_read syncs those events and returns, per
+ * category [0]=temporal pass, [1]=spatial pass, [2]=once-per-solve kernels,
+ * [3]=backward passes, the summed milliseconds and launch counts, then resets. */
+sfseg_status sfseg_profile_enable(int32_t on);
+sfseg_status sfseg_profile_read(double* ms_host /*[4]*/, int64_t* count_host /*[4]*/);
+
+/* ---- multi-GPU communicator (NCCL, loaded at run time with dlopen) ---- */
+/* 128-byte NCCL unique id into id_host (call on rank 0, broadcast it). */
+sfseg_status sfseg_get_unique_id(uint8_t id_host[128]);
+sfseg_status sfseg_comm_create(const uint8_t id_host[128], int32_t nranks, int32_t rank,
+                               int32_t device, sfseg_comm** out);
+sfseg_status sfseg_comm_destroy(sfseg_comm* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFSEG_H_ */

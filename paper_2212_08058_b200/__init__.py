@@ -1,0 +1,290 @@
+"""B200-native SFSeg / SFSeg++ power-iteration hot path (arxiv 2212.08058).
+
+Thin Python binding over the C ABI of ``libsfseg.so`` (include/sfseg.h):
+argument marshalling only -- every step of the path runs in the library's
+sm_100a kernels.  PyTorch provides device memory and the current CUDA stream.
+There is no CPU fallback: if the in-tree ``libsfseg.so`` is missing or fails
+to load, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+__all__ = [
+    "SfsegError", "Gauss", "lib", "workspace_bytes", "combine_channels", "power_iterate",
+    "power_iterate_backward", "threshold", "solve_host", "Solver",
+    "ACT_IDENTITY", "ACT_SIGMOID", "THR_PER_FRAME_MAX", "THR_GLOBAL_MAX", "THR_ABSOLUTE",
+]
+
+ACT_IDENTITY, ACT_SIGMOID = 0, 1
+THR_PER_FRAME_MAX, THR_GLOBAL_MAX, THR_ABSOLUTE = 0, 1, 2
+STATUS = {0: "ok", 1: "invalid argument", 2: "shape", 3: "workspace", 4: "degenerate",
+          5: "non-finite", 6: "cuda", 7: "nccl", 8: "unsupported"}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsfseg.so")
+
+
+class SfsegError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = f"{where}: sfseg status {status} ({STATUS.get(status, '?')})"
+        if status == 6 and _lib is not None:
+            try:
+                msg += ": " + _lib.sfseg_last_cuda_error().decode()
+            except Exception:  # pragma: no cover
+                pass
+        super().__init__(msg)
+        self.status = status
+
+
+class Shape(C.Structure):
+    _fields_ = [("B", C.c_int64), ("T", C.c_int64), ("H", C.c_int64), ("W", C.c_int64)]
+
+
+class GaussC(C.Structure):
+    _fields_ = [("sigma_t", C.c_double), ("sigma_s", C.c_double),
+                ("radius_t", C.c_int32), ("radius_s", C.c_int32)]
+
+
+class DistC(C.Structure):
+    _fields_ = [("comm", C.c_void_p), ("T_global", C.c_int64), ("t_offset", C.c_int64)]
+
+
+@dataclass(frozen=True)
+class Gauss:
+    sigma_t: float
+    sigma_s: float
+    radius_t: int = -1     # < 0 => ceil(3 sigma)
+    radius_s: int = -1
+
+    def c(self) -> GaussC:
+        return GaussC(self.sigma_t, self.sigma_s, self.radius_t, self.radius_s)
+
+
+_lib: Optional[C.CDLL] = None
+
+_P = C.c_void_p
+_SIGS = {
+    "sfseg_status_string": (C.c_char_p, [C.c_int]),
+    "sfseg_abi_version": (C.c_int32, []),
+    "sfseg_last_cuda_error": (C.c_char_p, []),
+    "sfseg_max_radii": (None, [_P, _P]),
+    "sfseg_workspace_bytes": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P, _P, _P]),
+    "sfseg_combine_channels": (C.c_int, [_P, C.c_int32, Shape, _P, C.c_float, C.c_int32, _P, _P]),
+    "sfseg_power_iterate": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
+                                      _P, _P, _P, _P, C.c_int32, _P, _P, C.c_size_t, _P, _P]),
+    "sfseg_power_iterate_backward": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC,
+                                               C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t, _P, _P]),
+    "sfseg_threshold_ws_bytes": (C.c_size_t, [Shape]),
+    "sfseg_threshold": (C.c_int, [_P, Shape, C.c_float, C.c_int32, _P, _P, C.c_size_t, _P]),
+    "sfseg_sync_status": (C.c_int, [_P, _P]),
+    "sfseg_solve_host": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
+                                   C.c_float, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "sfseg_profile_enable": (C.c_int, [C.c_int32]),
+    "sfseg_profile_read": (C.c_int, [_P, _P]),
+    "sfseg_get_unique_id": (C.c_int, [_P]),
+    "sfseg_comm_create": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P]),
+    "sfseg_comm_destroy": (C.c_int, [_P]),
+}
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree libsfseg.so (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built; run `python -m paper_2212_08058_b200.build` "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, where: str) -> None:
+    if status != 0:
+        raise SfsegError(status, where)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _shape(x: torch.Tensor) -> Shape:
+    B, T, H, W = x.shape
+    return Shape(B, T, H, W)
+
+
+def _require(t: torch.Tensor, name: str, ndim: int, dtype=torch.float32):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype or t.dim() != ndim or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor with {ndim} dims")
+
+
+def _weights(w, Cn: int):
+    w = [float(v) for v in (w.tolist() if hasattr(w, "tolist") else w)]
+    if len(w) != Cn:
+        raise ValueError("len(w) must equal the channel count")
+    return (C.c_float * Cn)(*w)
+
+
+def profile_enable(on: bool = True) -> None:
+    """Bracket every pass launch with CUDA events (bench instrumentation)."""
+    _check(lib().sfseg_profile_enable(int(on)), "sfseg_profile_enable")
+
+
+def profile_read():
+    """Sync the recorded events; returns {category: (total_ms, launches)} and resets."""
+    ms = (C.c_double * 4)()
+    n = (C.c_int64 * 4)()
+    _check(lib().sfseg_profile_read(ms, n), "sfseg_profile_read")
+    names = ("tpass", "spass", "once", "backward")
+    return {names[i]: (ms[i], n[i]) for i in range(4)}
+
+
+def workspace_bytes(shape, C_: int, gauss: Gauss, K: int, want_tape: bool = False):
+    ws, tape = C.c_size_t(0), C.c_size_t(0)
+    _check(lib().sfseg_workspace_bytes(Shape(*shape), C_, gauss.c(), K, int(want_tape), None,
+                                       C.byref(ws), C.byref(tape)), "sfseg_workspace_bytes")
+    return ws.value, tape.value
+
+
+def _alloc_bytes(n: int, device) -> torch.Tensor:
+    # torch's caching allocator returns >= 512-byte aligned blocks
+    return torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+
+
+def combine_channels(ch: torch.Tensor, w, b: float = 0.0, act: int = ACT_IDENTITY, stream=None) -> torch.Tensor:
+    """Eq.9: F = act(sum_c w_c ch_c + b).  ch [B][C][T][H][W]."""
+    _require(ch, "ch", 5)
+    B, Cn, T, H, W = ch.shape
+    F = torch.empty((B, T, H, W), dtype=torch.float32, device=ch.device)
+    _check(lib().sfseg_combine_channels(_ptr(ch), Cn, Shape(B, T, H, W), _weights(w, Cn), float(b), int(act),
+                                        _ptr(F), _stream(stream)), "sfseg_combine_channels")
+    return F
+
+
+class Solver:
+    """Holds the workspace (and optional tape) for one problem shape.
+
+    ``forward`` runs sfseg_power_iterate; ``backward`` runs
+    sfseg_power_iterate_backward on the tape of the last forward.
+    """
+
+    def __init__(self, shape, C_: int, gauss: Gauss, K: int, device="cuda", want_tape: bool = False):
+        self.shape = tuple(int(v) for v in shape)
+        self.C, self.gauss, self.K = int(C_), gauss, int(K)
+        self.device = torch.device(device)
+        self.want_tape = bool(want_tape)
+        ws, tape = workspace_bytes(self.shape, self.C, gauss, self.K, want_tape)
+        thr = lib().sfseg_threshold_ws_bytes(Shape(*self.shape))
+        self.ws_bytes = ws
+        self.ws = _alloc_bytes(ws + thr, self.device)
+        self.thr_ws_bytes = thr
+        self.tape = _alloc_bytes(tape, self.device) if want_tape else None
+        self.stats = torch.zeros((self.shape[0], self.K, 3), dtype=torch.float64, device=self.device)
+
+    def forward(self, ch: torch.Tensor, w, b: float = 0.0, act: int = ACT_IDENTITY, x0=None,
+                x_out: Optional[torch.Tensor] = None, want_rayleigh: bool = False, F_out=None,
+                stream=None, check: bool = True) -> torch.Tensor:
+        _require(ch, "ch", 5)
+        B, Cn, T, H, W = ch.shape
+        if (B, T, H, W) != self.shape or Cn != self.C:
+            raise ValueError("ch shape does not match the solver")
+        if x0 is not None:
+            _require(x0, "x0", 4)
+        if x_out is None:
+            x_out = torch.empty(self.shape, dtype=torch.float32, device=ch.device)
+        st = lib().sfseg_power_iterate(
+            _ptr(ch), Cn, _weights(w, Cn), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
+            _ptr(x0), _ptr(x_out), _ptr(F_out), _ptr(self.stats), int(want_rayleigh), _ptr(self.tape),
+            _ptr(self.ws), self.ws_bytes, None, _stream(stream))
+        _check(st, "sfseg_power_iterate")
+        if check:
+            self.sync(stream)
+        return x_out
+
+    def sync(self, stream=None) -> None:
+        _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate (device)")
+
+    def backward(self, ch: torch.Tensor, w, dL_dx: torch.Tensor, b: float = 0.0, act: int = ACT_IDENTITY,
+                 x0=None, stream=None):
+        if self.tape is None:
+            raise RuntimeError("Solver was built without want_tape")
+        _require(ch, "ch", 5)
+        _require(dL_dx, "dL_dx", 4)
+        Cn = ch.shape[1]
+        dw = (C.c_double * Cn)()
+        db = C.c_double(0.0)
+        st = lib().sfseg_power_iterate_backward(
+            _ptr(ch), Cn, _weights(w, Cn), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
+            _ptr(x0), _ptr(self.tape), _ptr(dL_dx), dw, C.byref(db), _ptr(self.ws), self.ws_bytes, None,
+            _stream(stream))
+        _check(st, "sfseg_power_iterate_backward")
+        return [dw[i] for i in range(Cn)], db.value
+
+    def threshold(self, x: torch.Tensor, tau: float, mode: int = THR_PER_FRAME_MAX,
+                  mask: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        if mask is None:
+            mask = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+        thr_ws = self.ws.narrow(0, self.ws_bytes + (-self.ws_bytes) % 256, self.thr_ws_bytes) \
+            if self.thr_ws_bytes else None
+        _check(lib().sfseg_threshold(_ptr(x), _shape(x), float(tau), int(mode), _ptr(mask), _ptr(thr_ws),
+                                     self.thr_ws_bytes, _stream(stream)), "sfseg_threshold")
+        return mask
+
+
+def power_iterate(ch: torch.Tensor, w, gauss: Gauss, K: int, b: float = 0.0, act: int = ACT_IDENTITY,
+                  x0=None, want_rayleigh: bool = False):
+    """One-shot solve; returns (x_K [B][T][H][W], stats float64 [B][K][3])."""
+    B, Cn, T, H, W = ch.shape
+    s = Solver((B, T, H, W), Cn, gauss, K, device=ch.device)
+    x = s.forward(ch, w, b, act, x0=x0, want_rayleigh=want_rayleigh)
+    return x, s.stats.clone()
+
+
+def power_iterate_backward(ch, w, gauss: Gauss, K: int, dL_dx, b: float = 0.0, act: int = ACT_IDENTITY, x0=None):
+    B, Cn, T, H, W = ch.shape
+    s = Solver((B, T, H, W), Cn, gauss, K, device=ch.device, want_tape=True)
+    x = s.forward(ch, w, b, act, x0=x0)
+    dw, db = s.backward(ch, w, dL_dx, b, act, x0=x0)
+    return x, dw, db
+
+
+def threshold(x: torch.Tensor, tau: float, mode: int = THR_PER_FRAME_MAX) -> torch.Tensor:
+    _require(x, "x", 4)
+    n = lib().sfseg_threshold_ws_bytes(_shape(x))
+    ws = _alloc_bytes(n, x.device)
+    mask = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    _check(lib().sfseg_threshold(_ptr(x), _shape(x), float(tau), int(mode), _ptr(mask), _ptr(ws), n,
+                                 _stream()), "sfseg_threshold")
+    return mask
+
+
+def solve_host(ch_host: torch.Tensor, w, gauss: Gauss, K: int, tau: float, solver: Solver,
+               d_ch: torch.Tensor, d_x: torch.Tensor, d_mask: torch.Tensor,
+               x_out_host: Optional[torch.Tensor], mask_out_host: Optional[torch.Tensor],
+               b: float = 0.0, act: int = ACT_IDENTITY, thr_mode: int = THR_PER_FRAME_MAX, stream=None):
+    """End-to-end call over HOST buffers (H2D, solve, threshold, D2H, sync) via sfseg_solve_host."""
+    B, Cn, T, H, W = ch_host.shape
+    _check(lib().sfseg_solve_host(
+        C.c_void_p(ch_host.data_ptr()), Cn, _weights(w, Cn), float(b), int(act), Shape(B, T, H, W), gauss.c(),
+        int(K), float(tau), int(thr_mode), _ptr(d_ch), _ptr(d_x), _ptr(d_mask),
+        None if x_out_host is None else C.c_void_p(x_out_host.data_ptr()),
+        None if mask_out_host is None else C.c_void_p(mask_out_host.data_ptr()),
+        _ptr(solver.ws), solver.ws.numel(), _stream(stream)), "sfseg_solve_host")

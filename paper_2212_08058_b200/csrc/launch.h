@@ -1,0 +1,14 @@
+// Host-side launchers of the radius-templated pass kernels (one translation
+// unit per mode so the heavy instantiations compile in parallel).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "spass.cuh"
+#include "tpass.cuh"
+
+namespace sfseg {
+cudaError_t launch_spass_fwd(int R, const SpassParams& P, int grid, cudaStream_t st);
+cudaError_t launch_spass_bwd(int R, const SpassParams& P, int grid, cudaStream_t st);
+cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t st);
+cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st);
+}  // namespace sfseg

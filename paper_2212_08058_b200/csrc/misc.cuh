@@ -1,0 +1,239 @@
+// Once-per-solve kernels: channel combine (Eq.9), final normalisation (Eq.8),
+// hard threshold (reading A12), and the backward's set-up and
+// final contraction (Appendix A).  All are HBM-streaming elementwise kernels
+// over the pitched volume; reductions use per-block partials and a fixed-order
+// fp64 finalize in the last block (deterministic).
+#pragma once
+#include "common.cuh"
+
+namespace sfseg {
+
+constexpr int kEwThreads = 256;
+
+// ------------------------------------------------------------------ combine (+ x_0, p_0, ||x_0||)
+struct CombineParams {
+  const float* ch;      // dense [B][C][T][H][W]
+  const float* x0;      // dense [B][T][H][W] or null (x_0 = F)
+  float* F;             // pitched [B*T][H][Wp]
+  float* p0;            // pitched: p_0 = F * x_0 (null: skip)
+  float* F_out;         // dense or null
+  float* x0p;           // pitched copy of x0 (null: skip)
+  double* sc;
+  double* partials;     // [B][T*gx]
+  unsigned* counter;
+  unsigned* err;
+  int B, C, T, H, W, Wp, act, gx;
+  float bias;
+  float w[kMaxC];
+};
+
+__global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_constant__ CombineParams P) {
+  __shared__ double red[kEwThreads / 32];
+  __shared__ int flag;
+  const int bt = blockIdx.y;
+  const int b = bt / P.T, t = bt - b * P.T;
+  const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
+  const long vol_dense = (long)P.T * HW;
+  double acc = 0.0;
+  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HWp; e += (long)P.gx * kEwThreads) {
+    const int y = (int)(e / P.Wp), x = (int)(e - (long)y * P.Wp);
+    const long po = (long)bt * HWp + e;
+    float f = 0.f, pv = 0.f, xv = 0.f;
+    if (x < P.W) {
+      const long d = (long)t * HW + (long)y * P.W + x;
+      const float* chb = P.ch + (long)b * P.C * vol_dense + d;
+      float z = P.bias;
+      for (int c = 0; c < P.C; ++c) z = fmaf(P.w[c], __ldg(chb + (long)c * vol_dense), z);
+      f = (P.act == 1) ? 1.f / (1.f + expf(-z)) : z;
+      xv = P.x0 ? __ldg(P.x0 + (long)b * vol_dense + d) : f;
+      pv = f * xv;
+      if (P.F_out) P.F_out[(long)b * vol_dense + d] = f;
+      acc += (double)xv * (double)xv;
+    }
+    P.F[po] = f;
+    if (P.p0) P.p0[po] = pv;
+    if (P.x0p) P.x0p[po] = xv;
+  }
+  if (P.partials == nullptr) return;  // plain combine (sfseg_combine_channels): no reduction
+  const double s = block_sum<kEwThreads>(acc, red);
+  const long nper = (long)P.T * P.gx;
+  if (threadIdx.x == 0) P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = s;
+  if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
+  for (int bb = 0; bb < P.B; ++bb) {
+    const double tot = block_sum_array<kEwThreads>(P.partials + (long)bb * nper, nper, 1, red);
+    if (threadIdx.x == 0) {
+      const double xn = sqrt(tot);
+      P.sc[bb * kScal + SC_XNORM] = xn;
+      P.sc[bb * kScal + SC_S] = 1.0;
+      flag_norm(P.err, xn);
+    }
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+// ------------------------------------------------------------------ final normalisation x_K = y_K / nu_K
+__global__ void __launch_bounds__(kEwThreads) final_scale_kernel(const float* __restrict__ y, float* __restrict__ x,
+                                                                 const double* sc, int T, int H, int W, int Wp) {
+  const int bt = blockIdx.y, b = bt / T;
+  const float s = (float)sc[b * kScal + SC_S];
+  const long HW = (long)H * W;
+  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HW; e += (long)gridDim.x * kEwThreads) {
+    const int yy = (int)(e / W), xx = (int)(e - (long)yy * W);
+    x[(long)bt * HW + e] = __ldcs(y + ((long)bt * H + yy) * Wp + xx) * s;
+  }
+}
+
+// ------------------------------------------------------------------ threshold
+__global__ void __launch_bounds__(kEwThreads) frame_max_kernel(const float* __restrict__ x, float* fmax, long HW) {
+  __shared__ float red[kEwThreads / 32];
+  const long base = (long)blockIdx.x * HW;
+  float m = -INFINITY;
+  for (long e = threadIdx.x; e < HW; e += kEwThreads) m = fmaxf(m, x[base + e]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r = red[0];
+    for (int i = 1; i < kEwThreads / 32; ++i) r = fmaxf(r, red[i]);
+    fmax[blockIdx.x] = r;
+  }
+}
+
+__global__ void __launch_bounds__(kEwThreads) threshold_kernel(const float* __restrict__ x, uint8_t* __restrict__ mask,
+                                                               const float* fmax, int T, long HW, float tau,
+                                                               int mode) {
+  const int bt = blockIdx.y, b = bt / T;
+  float thr;
+  bool none = false;
+  if (mode == 2) {
+    thr = tau;
+  } else {
+    float m;
+    if (mode == 0) {
+      m = fmax[bt];
+    } else {
+      m = fmax[b * T];
+      for (int t = 1; t < T; ++t) m = fmaxf(m, fmax[b * T + t]);
+    }
+    none = !(m > 0.f);
+    thr = tau * m;
+  }
+  const long base = (long)bt * HW;
+  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HW; e += (long)gridDim.x * kEwThreads)
+    mask[base + e] = (!none && x[base + e] > thr) ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ backward set-up: x_bar_K, F_bar = 0, c_K
+struct BwdInitParams {
+  const float* g;       // dense dL/dx_K [B][T][H][W]
+  const float* F;       // pitched
+  const float* uK1;     // tape u_{K-1} pitched
+  float* xbar;          // pitched
+  float* Fbar;          // pitched (zeroed)
+  const double* tape_nu;
+  double* sc;
+  double* partials;
+  unsigned* counter;
+  int B, T, H, W, Wp, K, gx;
+};
+
+__global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_constant__ BwdInitParams P) {
+  __shared__ double red[kEwThreads / 32];
+  __shared__ int flag;
+  const int bt = blockIdx.y;
+  const int b = bt / P.T, t = bt - b * P.T;
+  const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
+  double acc = 0.0;
+  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HWp; e += (long)P.gx * kEwThreads) {
+    const int y = (int)(e / P.Wp), x = (int)(e - (long)y * P.Wp);
+    const long po = (long)bt * HWp + e;
+    float gv = 0.f;
+    if (x < P.W) {
+      gv = P.g[((long)b * P.T + t) * HW + (long)y * P.W + x];
+      acc += (double)gv * (double)P.F[po] * (double)P.uK1[po];
+    }
+    P.xbar[po] = gv;
+    P.Fbar[po] = 0.f;
+  }
+  const double s = block_sum<kEwThreads>(acc, red);
+  const long nper = (long)P.T * P.gx;
+  if (threadIdx.x == 0) P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = s;
+  if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
+  for (int bb = 0; bb < P.B; ++bb) {
+    const double tot = block_sum_array<kEwThreads>(P.partials + (long)bb * nper, nper, 1, red);
+    if (threadIdx.x == 0) {
+      const double nuK = P.tape_nu[(long)bb * P.K + (P.K - 1)];
+      // c_K = <x_K, x_bar_K> = sum(g F u_{K-1}) / nu_K ; cn = c_K / nu_K
+      P.sc[bb * kScal + SC_CN] = tot / (nuK * nuK);
+      P.sc[bb * kScal + SC_INV_NU] = 1.0 / nuK;
+      P.sc[bb * kScal + SC_INV_NU_PREV] = (P.K >= 2) ? 1.0 / P.tape_nu[(long)bb * P.K + (P.K - 2)] : 0.0;
+    }
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+// ------------------------------------------------------------------ backward contraction dw, db
+struct ContractParams {
+  const float* ch;      // dense [B][C][T][H][W]
+  const float* Fbar;    // pitched
+  const float* xbar0;   // pitched x_bar_0 (added when x_0 = F) or null
+  double* partials;     // [G][C+1]
+  double* out;          // [C+1] : dw_0..dw_{C-1}, db
+  unsigned* counter;
+  int B, C, T, H, W, Wp, act;
+  float bias;
+  float w[kMaxC];
+};
+
+template <int CMAX>
+__global__ void __launch_bounds__(kEwThreads) contract_kernel(const __grid_constant__ ContractParams P) {
+  __shared__ double red[kEwThreads / 32];
+  __shared__ int flag;
+  double acc[CMAX + 1];
+#pragma unroll
+  for (int c = 0; c <= CMAX; ++c) acc[c] = 0.0;
+  const long HW = (long)P.H * P.W, vol = (long)P.T * HW;
+  const long N = (long)P.B * vol;
+  for (long i = (long)blockIdx.x * kEwThreads + threadIdx.x; i < N; i += (long)gridDim.x * kEwThreads) {
+    const long b = i / vol, r = i - b * vol;
+    const long t = r / HW, rr = r - t * HW;
+    const long y = rr / P.W, x = rr - y * P.W;
+    const long po = ((b * P.T + t) * P.H + y) * P.Wp + x;
+    float fb = P.Fbar[po];
+    if (P.xbar0) fb += P.xbar0[po];
+    const float* chb = P.ch + b * P.C * vol + r;
+    float cv[CMAX];
+    float z = P.bias;
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) {
+      cv[c] = (c < P.C) ? __ldg(chb + (long)c * vol) : 0.f;
+      z = fmaf(P.w[c], cv[c], z);  // w[c] == 0 for c >= C (host zero-fills)
+    }
+    float dphi = 1.f;
+    if (P.act == 1) {
+      const float s = 1.f / (1.f + expf(-z));
+      dphi = s * (1.f - s);
+    }
+    const double zb = (double)fb * (double)dphi;
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) acc[c] += zb * (double)cv[c];
+    acc[CMAX] += zb;
+  }
+#pragma unroll
+  for (int c = 0; c <= CMAX; ++c) {
+    const double s = block_sum<kEwThreads>(acc[c], red);
+    if (threadIdx.x == 0) P.partials[(long)blockIdx.x * (CMAX + 1) + c] = s;
+  }
+  if (!last_block_arrive(P.counter, gridDim.x, &flag)) return;
+  for (int c = 0; c <= CMAX; ++c) {
+    const double tot = block_sum_array<kEwThreads>(P.partials + c, gridDim.x, CMAX + 1, red);
+    if (threadIdx.x == 0) {
+      if (c < P.C) P.out[c] = tot;
+      if (c == CMAX) P.out[P.C] = tot;
+    }
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+}  // namespace sfseg

@@ -1,0 +1,732 @@
+// Host side of libsfseg.so: argument validation, workspace carve-up, radius
+// dispatch, TMA descriptor construction and launch sequencing of the
+// sm_100a kernels.  C ABI declared in include/sfseg.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/sfseg.h"
+#include "common.cuh"
+#include "misc.cuh"
+#include "spass.cuh"
+#include "tpass.cuh"
+#include "comm.cuh"
+#include "launch.h"
+
+using namespace sfseg;
+
+namespace {
+
+#define SF_CUDA(call)                                                   \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) {                                            \
+      last_cuda_error() = e_;                                           \
+      return SFSEG_ERR_CUDA;                                            \
+    }                                                                   \
+  } while (0)
+
+cudaError_t& last_cuda_error() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------------ radius dispatch tables
+constexpr int kSpatialRadii[] = {1, 2, 3, 4, 5, 6, 8, 9, 12, 16, 18, 24, 32, 36, 48};
+constexpr int kTemporalRadii[] = {0, 1, 2, 3, 4, 5, 6, 8, 9, 12, 16};
+
+int pick_spatial(int r) {
+  for (int R : kSpatialRadii)
+    if (R >= r) return R;
+  return -1;
+}
+int pick_temporal(int r) {
+  for (int R : kTemporalRadii)
+    if (R >= r) return R;
+  return -1;
+}
+
+int resolve_radius(double sigma, int32_t r) { return r >= 0 ? r : (int)std::ceil(3.0 * sigma - 1e-12); }
+
+void gauss_taps(double sigma, int r, int Rpad, float* out /* 2*Rpad+1 */) {
+  std::vector<double> g(2 * r + 1);
+  double s = 0.0;
+  for (int k = -r; k <= r; ++k) {
+    g[k + r] = std::exp(-(double)k * k / (2.0 * sigma * sigma));
+    s += g[k + r];
+  }
+  for (int i = 0; i < 2 * Rpad + 1; ++i) {
+    const int k = i - Rpad;
+    out[i] = (std::abs(k) <= r) ? (float)(g[k + r] / s) : 0.f;
+  }
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ TMA descriptor encode (driver entry point)
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+bool make_volume_tmap(CUtensorMap* map, const float* base, int64_t W, int64_t H, int64_t BT, int64_t Wp, int boxw) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)BT};
+  cuuint64_t strides[2] = {(cuuint64_t)(Wp * 4), (cuuint64_t)(H * Wp * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)kM, 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int spass_occupancy(int R) {
+  static int occ[64] = {0};
+  if (R < 0 || R >= 64) return 1;
+  if (occ[R] == 0) {
+    occ[R] = (spass_smem_bytes(R) * 2 + 2048 <= 227 * 1024) ? 2 : 1;
+  }
+  return occ[R];
+}
+
+// ------------------------------------------------------------------ optional per-kernel event timing
+// (bench instrumentation: sfseg_profile_enable / sfseg_profile_read)
+struct ProfRec {
+  int cat;
+  cudaEvent_t a, b;
+};
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Profiler& prof() {
+  static Profiler p;
+  return p;
+}
+enum ProfCat { PC_TPASS = 0, PC_SPASS = 1, PC_ONCE = 2, PC_BWD = 3, PC_N = 4 };
+
+// RAII scope that brackets a launch with events when profiling is on.
+struct ProfScope {
+  cudaStream_t st;
+  int cat;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(cudaStream_t s, int c) : st(s), cat(c) {
+    Profiler& p = prof();
+    if (!p.on) return;
+    std::lock_guard<std::mutex> g(p.mu);
+    a = p.get();
+    b = p.get();
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    Profiler& p = prof();
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> g(p.mu);
+    p.recs.push_back({cat, a, b});
+  }
+};
+
+// ------------------------------------------------------------------ problem plan
+struct Plan {
+  int64_t B, T, H, W, Wp, BT;
+  int C, K;
+  int rt, rs;      // requested radii
+  int RT, RS;      // compiled radii (>= requested; extra taps are zero)
+  float gt[2 * kMaxRT + 1];
+  float gs[2 * kMaxRS + 1];
+  int64_t vol_elems;  // B*T*H*Wp
+  int S;              // strips
+  int64_t U;          // spass row units
+  int G;              // spass grid
+  int gx;             // elementwise grid.x per frame
+  // workspace offsets
+  size_t off_sc, off_part, off_out, off_F, off_p, off_v, off_xbar, off_Fbar, off_x0p, ws_fwd, ws_bwd;
+  size_t n_part;
+  size_t tape_nu_bytes, tape_bytes;
+};
+
+sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan* P) {
+  if (C < 1 || C > kMaxC) return C < 1 ? SFSEG_ERR_INVALID_ARGUMENT : SFSEG_ERR_UNSUPPORTED;
+  if (K < 1) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (!(g.sigma_t > 0.0) || !(g.sigma_s > 0.0) || !std::isfinite(g.sigma_t) || !std::isfinite(g.sigma_s))
+    return SFSEG_ERR_INVALID_ARGUMENT;
+  if (sh.B < 1 || sh.T < 1 || sh.H < 1 || sh.W < 1) return SFSEG_ERR_SHAPE;
+  if (sh.H > (1 << 24) || sh.W > (1 << 24) || sh.B * sh.T > (1 << 30)) return SFSEG_ERR_SHAPE;
+  P->B = sh.B;
+  P->T = sh.T;
+  P->H = sh.H;
+  P->W = sh.W;
+  P->BT = sh.B * sh.T;
+  P->Wp = round_up(sh.W, 8);
+  P->C = C;
+  P->K = K;
+  P->rt = resolve_radius(g.sigma_t, g.radius_t);
+  P->rs = resolve_radius(g.sigma_s, g.radius_s);
+  P->RT = pick_temporal(P->rt);
+  P->RS = pick_spatial(std::max(P->rs, 1));
+  if (P->RT < 0 || P->RS < 0) return SFSEG_ERR_SHAPE;
+  gauss_taps(g.sigma_t, P->rt, P->RT, P->gt);
+  gauss_taps(g.sigma_s, P->rs, P->RS, P->gs);
+  P->vol_elems = P->BT * P->H * P->Wp;
+  P->S = (int)((sh.W + kTW - 1) / kTW);
+  P->U = P->BT * P->S * P->H;
+  const int64_t cap = (int64_t)num_sms() * spass_occupancy(P->RS);
+  P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 64));
+  const int64_t per_frame = (P->H * P->Wp + 256 * 4 - 1) / (256 * 4);
+  P->gx = (int)std::max<int64_t>(1, std::min<int64_t>(per_frame, 16));
+  // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
+  size_t n_part = std::max<size_t>(2 * (size_t)P->B * P->G, (size_t)P->BT * P->gx);
+  n_part = std::max<size_t>(n_part, (size_t)4 * num_sms() * (kMaxC + 1));
+  P->n_part = n_part;
+  size_t off = align_up(sizeof(WsHeader));
+  P->off_sc = off;
+  off += align_up(sizeof(double) * kScal * P->B);
+  P->off_part = off;
+  off += align_up(sizeof(double) * n_part);
+  P->off_out = off;
+  off += align_up(sizeof(double) * (kMaxC + 1));
+  const size_t vb = align_up(sizeof(float) * (size_t)P->vol_elems);
+  P->off_F = off;
+  off += vb;
+  P->off_p = off;
+  off += vb;
+  P->off_v = off;
+  off += vb;
+  P->ws_fwd = off;
+  P->off_xbar = off;
+  off += vb;
+  P->off_Fbar = off;
+  off += vb;
+  P->off_x0p = off;
+  off += vb;
+  P->ws_bwd = off;
+  P->tape_nu_bytes = align_up(sizeof(double) * P->B * K);
+  P->tape_bytes = P->tape_nu_bytes + (size_t)K * vb;
+  return SFSEG_OK;
+}
+
+template <class T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+sfseg_status check_ws(const void* ws, size_t ws_bytes, size_t need) {
+  if (!ws) return SFSEG_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(ws) % kAlign) != 0 || ws_bytes < need) return SFSEG_ERR_WORKSPACE;
+  return SFSEG_OK;
+}
+
+sfseg_status map_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return SFSEG_OK;
+  last_cuda_error() = e;
+  return SFSEG_ERR_CUDA;
+}
+
+void fill_combine(CombineParams& cp, const Plan& P, const float* ch, const float* w_host, float b, int act, void* ws) {
+  std::memset(&cp, 0, sizeof(cp));
+  cp.ch = ch;
+  cp.sc = at<double>(ws, P.off_sc);
+  cp.partials = at<double>(ws, P.off_part);
+  cp.counter = &at<WsHeader>(ws, 0)->counter[1];
+  cp.err = &at<WsHeader>(ws, 0)->err;
+  cp.B = (int)P.B;
+  cp.C = P.C;
+  cp.T = (int)P.T;
+  cp.H = (int)P.H;
+  cp.W = (int)P.W;
+  cp.Wp = (int)P.Wp;
+  cp.act = act;
+  cp.gx = P.gx;
+  cp.bias = b;
+  for (int c = 0; c < P.C; ++c) cp.w[c] = w_host[c];
+}
+
+void fill_spass_common(SpassParams& sp, const Plan& P, void* ws) {
+  sp.F = at<float>(ws, P.off_F);
+  sp.sc = at<double>(ws, P.off_sc);
+  sp.partials = at<double>(ws, P.off_part);
+  sp.counter = &at<WsHeader>(ws, 0)->counter[0];
+  sp.err = &at<WsHeader>(ws, 0)->err;
+  sp.U = P.U;
+  sp.B = (int)P.B;
+  sp.T = (int)P.T;
+  sp.H = (int)P.H;
+  sp.W = (int)P.W;
+  sp.Wp = (int)P.Wp;
+  sp.S = P.S;
+  sp.G = P.G;
+  sp.K = P.K;
+  for (int i = 0; i < 2 * P.RS + 1; ++i) sp.g[i] = P.gs[i];
+}
+
+void fill_tpass_common(TpassParams& tp, const Plan& P, void* ws) {
+  tp.sc = at<double>(ws, P.off_sc);
+  tp.frame4 = P.H * P.Wp / 4;
+  tp.T = (int)P.T;
+  for (int i = 0; i < 2 * P.RT + 1; ++i) tp.g[i] = P.gt[i];
+}
+
+bool validate_act(int act) { return act == SFSEG_ACT_IDENTITY || act == SFSEG_ACT_SIGMOID; }
+
+bool finite_weights(const float* w, int C, float b) {
+  if (!std::isfinite(b)) return false;
+  for (int c = 0; c < C; ++c)
+    if (!std::isfinite(w[c])) return false;
+  return true;
+}
+
+// Time-slab sharded solve; filled in by the multi-GPU milestone.
+sfseg_status dist_power_iterate(const Plan& P, const float* ch, const float* w_host, float b, int act,
+                                const float* x0, float* x_out, float* F_out, double* stats, int want_rayleigh,
+                                void* tape, void* ws, size_t ws_bytes, const sfseg_dist* dist, void* stream) {
+  (void)P; (void)ch; (void)w_host; (void)b; (void)act; (void)x0; (void)x_out; (void)F_out; (void)stats;
+  (void)want_rayleigh; (void)tape; (void)ws; (void)ws_bytes; (void)dist; (void)stream;
+  return SFSEG_ERR_UNSUPPORTED;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* sfseg_status_string(sfseg_status s) {
+  switch (s) {
+    case SFSEG_OK: return "ok";
+    case SFSEG_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case SFSEG_ERR_SHAPE: return "invalid shape or radius";
+    case SFSEG_ERR_WORKSPACE: return "workspace too small or misaligned";
+    case SFSEG_ERR_DEGENERATE: return "degenerate iterate (zero norm)";
+    case SFSEG_ERR_NONFINITE: return "non-finite value reached a norm";
+    case SFSEG_ERR_CUDA: return "CUDA error";
+    case SFSEG_ERR_NCCL: return "NCCL error";
+    case SFSEG_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+int32_t sfseg_abi_version(void) { return SFSEG_ABI_VERSION; }
+
+const char* sfseg_last_cuda_error(void) { return cudaGetErrorString(last_cuda_error()); }
+
+void sfseg_max_radii(int32_t* rs, int32_t* rt) {
+  if (rs) *rs = kMaxRS;
+  if (rt) *rt = kMaxRT;
+}
+
+sfseg_status sfseg_workspace_bytes(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K, int32_t want_tape,
+                                   const sfseg_dist* dist, size_t* ws_bytes, size_t* tape_bytes) {
+  if (!ws_bytes) return SFSEG_ERR_INVALID_ARGUMENT;
+  Plan P;
+  sfseg_status st = make_plan(shape, C, gauss, K, &P);
+  if (st != SFSEG_OK) return st;
+  size_t extra = dist ? sfseg::comm_ws_bytes(P.B, P.RT, P.H, P.Wp) : 0;
+  *ws_bytes = (want_tape ? P.ws_bwd : P.ws_fwd) + extra;
+  if (tape_bytes) *tape_bytes = want_tape ? P.tape_bytes : 0;
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_combine_channels(const float* ch, int32_t C, sfseg_shape sh, const float* w_host, float b,
+                                    int32_t act, float* F, void* stream) {
+  if (!ch || !w_host || !F || C < 1 || !validate_act(act)) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (C > kMaxC) return SFSEG_ERR_UNSUPPORTED;
+  if (sh.B < 1 || sh.T < 1 || sh.H < 1 || sh.W < 1) return SFSEG_ERR_SHAPE;
+  if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
+  // Dense-to-dense combine: reuse the combine kernel with Wp = W and no side outputs.
+  CombineParams cp;
+  std::memset(&cp, 0, sizeof(cp));
+  cp.ch = ch;
+  cp.F = F;
+  cp.B = (int)sh.B;
+  cp.C = C;
+  cp.T = (int)sh.T;
+  cp.H = (int)sh.H;
+  cp.W = (int)sh.W;
+  cp.Wp = (int)sh.W;
+  cp.act = act;
+  cp.bias = b;
+  for (int c = 0; c < C; ++c) cp.w[c] = w_host[c];
+  const int64_t per_frame = (sh.H * sh.W + 1023) / 1024;
+  cp.gx = (int)std::max<int64_t>(1, std::min<int64_t>(per_frame, 16));
+  cp.partials = nullptr;  // no ||x_0|| reduction for the standalone combine
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  combine_kernel<<<dim3(cp.gx, (unsigned)(sh.B * sh.T)), kEwThreads, 0, st>>>(cp);
+  return map_cuda(cudaGetLastError());
+}
+
+sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
+                                 sfseg_shape sh, sfseg_gauss gauss, int32_t K, const float* x0, float* x_out,
+                                 float* F_out, double* stats, int32_t want_rayleigh, void* tape, void* ws,
+                                 size_t ws_bytes, const sfseg_dist* dist, void* stream) {
+  if (!ch || !w_host || !x_out || !validate_act(act)) return SFSEG_ERR_INVALID_ARGUMENT;
+  Plan P;
+  sfseg_status s = make_plan(sh, C, gauss, K, &P);
+  if (s != SFSEG_OK) return s;
+  if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (dist) return dist_power_iterate(P, ch, w_host, b, act, x0, x_out, F_out, stats, want_rayleigh, tape,
+                                             ws, ws_bytes, dist, stream);
+  if ((s = check_ws(ws, ws_bytes, P.ws_fwd)) != SFSEG_OK) return s;
+  if (tape && (reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) return SFSEG_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  // header + per-volume scalars start from zero
+  SF_CUDA(cudaMemsetAsync(ws, 0, P.off_part, st));
+
+  float* F = at<float>(ws, P.off_F);
+  float* p = at<float>(ws, P.off_p);
+  float* v = at<float>(ws, P.off_v);
+  double* tape_nu = tape ? static_cast<double*>(tape) : nullptr;
+  auto tape_u = [&](int i) -> float* {
+    return reinterpret_cast<float*>(static_cast<char*>(tape) + P.tape_nu_bytes +
+                                    (size_t)i * align_up(sizeof(float) * (size_t)P.vol_elems));
+  };
+
+  // (a1) combine -> F, p_0 = F * x_0, ||x_0||
+  CombineParams cp;
+  fill_combine(cp, P, ch, w_host, b, act, ws);
+  cp.x0 = x0;
+  cp.F = F;
+  cp.p0 = p;
+  cp.F_out = F_out;
+  combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
+  SF_CUDA(cudaGetLastError());
+
+  SpassParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  if (!make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+  fill_spass_common(sp, P, ws);
+  sp.stats = stats;
+  sp.tape_nu = tape_nu;
+  TpassParams tp;
+  std::memset(&tp, 0, sizeof(tp));
+  fill_tpass_common(tp, P, ws);
+  tp.src = p;
+  tp.out = v;
+
+  for (int k = 1; k <= K; ++k) {
+    // (a2)+(a3) v = s_{k-1} * G_t * p_{k-1}
+    {
+      ProfScope ps(st, PC_TPASS);
+      SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
+    }
+    // (a4)-(a7) u = G_y G_x v ; y_k = F u ; p_k = F y_k ; ||y_k||, <p_{k-1}, u>
+    sp.out = p;
+    sp.pprev = want_rayleigh ? p : nullptr;
+    sp.tape_u = tape ? tape_u(k - 1) : nullptr;
+    sp.k = k;
+    sp.last = (k == K) ? 1 : 0;
+    {
+      ProfScope ps(st, PC_SPASS);
+      SF_CUDA(launch_spass_fwd(P.RS, sp, P.G, st));
+    }
+  }
+  // (a8) x_K = y_K / nu_K (dense output)
+  {
+    const int64_t per = (P.H * P.W + 1023) / 1024;
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(per, 64)), (unsigned)P.BT);
+    final_scale_kernel<<<grid, kEwThreads, 0, st>>>(p, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H, (int)P.W,
+                                                    (int)P.Wp);
+    SF_CUDA(cudaGetLastError());
+  }
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
+                                          sfseg_shape sh, sfseg_gauss gauss, int32_t K, const float* x0,
+                                          const void* tape, const float* dL_dx, double* dL_dw_host,
+                                          double* dL_db_host, void* ws, size_t ws_bytes, const sfseg_dist* dist,
+                                          void* stream) {
+  if (!ch || !w_host || !tape || !dL_dx || !dL_dw_host || !validate_act(act)) return SFSEG_ERR_INVALID_ARGUMENT;
+  Plan P;
+  sfseg_status s = make_plan(sh, C, gauss, K, &P);
+  if (s != SFSEG_OK) return s;
+  if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (dist) return SFSEG_ERR_UNSUPPORTED;
+  if ((s = check_ws(ws, ws_bytes, P.ws_bwd)) != SFSEG_OK) return s;
+  if ((reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) return SFSEG_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SF_CUDA(cudaMemsetAsync(ws, 0, P.off_part, st));
+
+  float* F = at<float>(ws, P.off_F);
+  float* v = at<float>(ws, P.off_v);
+  float* xbar = at<float>(ws, P.off_xbar);
+  float* Fbar = at<float>(ws, P.off_Fbar);
+  float* x0p = x0 ? at<float>(ws, P.off_x0p) : nullptr;
+  const double* tape_nu = static_cast<const double*>(tape);
+  auto tape_u = [&](int i) -> const float* {
+    return reinterpret_cast<const float*>(static_cast<const char*>(tape) + P.tape_nu_bytes +
+                                          (size_t)i * align_up(sizeof(float) * (size_t)P.vol_elems));
+  };
+
+  CombineParams cp;
+  fill_combine(cp, P, ch, w_host, b, act, ws);
+  cp.x0 = x0;
+  cp.F = F;
+  cp.x0p = x0p;
+  combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
+  SF_CUDA(cudaGetLastError());
+
+  BwdInitParams ip;
+  std::memset(&ip, 0, sizeof(ip));
+  ip.g = dL_dx;
+  ip.F = F;
+  ip.uK1 = tape_u(K - 1);
+  ip.xbar = xbar;
+  ip.Fbar = Fbar;
+  ip.tape_nu = tape_nu;
+  ip.sc = at<double>(ws, P.off_sc);
+  ip.partials = at<double>(ws, P.off_part);
+  ip.counter = &at<WsHeader>(ws, 0)->counter[2];
+  ip.B = (int)P.B;
+  ip.T = (int)P.T;
+  ip.H = (int)P.H;
+  ip.W = (int)P.W;
+  ip.Wp = (int)P.Wp;
+  ip.K = K;
+  ip.gx = P.gx;
+  bwd_init_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ip);
+  SF_CUDA(cudaGetLastError());
+
+  SpassParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  if (!make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+  fill_spass_common(sp, P, ws);
+  sp.tape_nu = const_cast<double*>(tape_nu);
+  sp.out = xbar;
+  sp.Fbar = Fbar;
+  sp.x0p = x0p;
+  TpassParams tp;
+  std::memset(&tp, 0, sizeof(tp));
+  fill_tpass_common(tp, P, ws);
+  tp.src = xbar;
+  tp.F = F;
+  tp.out = v;
+  for (int k = K; k >= 1; --k) {
+    tp.u1 = tape_u(k - 1);
+    {
+      ProfScope ps(st, PC_BWD);
+      SF_CUDA(launch_tpass_bwd(P.RT, tp, (int)P.B, st));
+    }
+    sp.u1 = tape_u(k - 1);
+    sp.u2 = (k >= 2) ? tape_u(k - 2) : nullptr;
+    sp.k = k;
+    {
+      ProfScope ps(st, PC_BWD);
+      SF_CUDA(launch_spass_bwd(P.RS, sp, P.G, st));
+    }
+  }
+
+  ContractParams cc;
+  std::memset(&cc, 0, sizeof(cc));
+  cc.ch = ch;
+  cc.Fbar = Fbar;
+  cc.xbar0 = x0 ? nullptr : xbar;
+  cc.partials = at<double>(ws, P.off_part);
+  cc.out = at<double>(ws, P.off_out);
+  cc.counter = &at<WsHeader>(ws, 0)->counter[3];
+  cc.B = (int)P.B;
+  cc.C = C;
+  cc.T = (int)P.T;
+  cc.H = (int)P.H;
+  cc.W = (int)P.W;
+  cc.Wp = (int)P.Wp;
+  cc.act = act;
+  cc.bias = b;
+  for (int c = 0; c < C; ++c) cc.w[c] = w_host[c];
+  const int G2 = 4 * num_sms();
+  if (C <= 1) contract_kernel<1><<<G2, kEwThreads, 0, st>>>(cc);
+  else if (C <= 2) contract_kernel<2><<<G2, kEwThreads, 0, st>>>(cc);
+  else if (C <= 4) contract_kernel<4><<<G2, kEwThreads, 0, st>>>(cc);
+  else if (C <= 8) contract_kernel<8><<<G2, kEwThreads, 0, st>>>(cc);
+  else if (C <= 16) contract_kernel<16><<<G2, kEwThreads, 0, st>>>(cc);
+  else contract_kernel<kMaxC><<<G2, kEwThreads, 0, st>>>(cc);
+  SF_CUDA(cudaGetLastError());
+  std::vector<double> out(C + 1);
+  SF_CUDA(cudaMemcpyAsync(out.data(), cc.out, sizeof(double) * (C + 1), cudaMemcpyDeviceToHost, st));
+  s = sfseg_sync_status(ws, stream);
+  for (int c = 0; c < C; ++c) dL_dw_host[c] = out[c];
+  if (dL_db_host) *dL_db_host = out[C];
+  return s;
+}
+
+size_t sfseg_threshold_ws_bytes(sfseg_shape sh) {
+  if (sh.B < 1 || sh.T < 1) return 0;
+  return align_up(sizeof(float) * (size_t)(sh.B * sh.T));
+}
+
+sfseg_status sfseg_threshold(const float* x, sfseg_shape sh, float tau, int32_t mode, uint8_t* mask, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (!x || !mask || !std::isfinite(tau)) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (mode < 0 || mode > 2) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (sh.B < 1 || sh.T < 1 || sh.H < 1 || sh.W < 1) return SFSEG_ERR_SHAPE;
+  sfseg_status s = check_ws(ws, ws_bytes, sfseg_threshold_ws_bytes(sh));
+  if (s != SFSEG_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long HW = (long)(sh.H * sh.W);
+  float* fmax = static_cast<float*>(ws);
+  if (mode != SFSEG_THR_ABSOLUTE) {
+    frame_max_kernel<<<(unsigned)(sh.B * sh.T), kEwThreads, 0, st>>>(x, fmax, HW);
+    SF_CUDA(cudaGetLastError());
+  }
+  const int64_t per = (HW + 1023) / 1024;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(per, 64)), (unsigned)(sh.B * sh.T));
+  threshold_kernel<<<grid, kEwThreads, 0, st>>>(x, mask, fmax, (int)sh.T, HW, tau, mode);
+  return map_cuda(cudaGetLastError());
+}
+
+sfseg_status sfseg_sync_status(void* ws, void* stream) {
+  if (!ws) return SFSEG_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned err = 0;
+  SF_CUDA(cudaMemcpyAsync(&err, &at<WsHeader>(ws, 0)->err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  if (err) {
+    unsigned zero = 0;
+    SF_CUDA(cudaMemcpyAsync(&at<WsHeader>(ws, 0)->err, &zero, sizeof(unsigned), cudaMemcpyHostToDevice, st));
+    SF_CUDA(cudaStreamSynchronize(st));
+  }
+  if (err & ERR_NONFINITE) return SFSEG_ERR_NONFINITE;
+  if (err & ERR_DEGENERATE) return SFSEG_ERR_DEGENERATE;
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_solve_host(const float* ch_host, int32_t C, const float* w_host, float b, int32_t act,
+                              sfseg_shape sh, sfseg_gauss gauss, int32_t K, float tau, int32_t thr_mode, float* d_ch,
+                              float* d_x, uint8_t* d_mask, float* x_out_host, uint8_t* mask_out_host, void* ws,
+                              size_t ws_bytes, void* stream) {
+  if (!ch_host || !d_ch || !d_x || !d_mask) return SFSEG_ERR_INVALID_ARGUMENT;
+  Plan P;
+  sfseg_status s = make_plan(sh, C, gauss, K, &P);
+  if (s != SFSEG_OK) return s;
+  const size_t thr_ws = sfseg_threshold_ws_bytes(sh);
+  if ((s = check_ws(ws, ws_bytes, P.ws_fwd + thr_ws)) != SFSEG_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t nvox = (size_t)(sh.B * sh.T * sh.H * sh.W);
+  SF_CUDA(cudaMemcpyAsync(d_ch, ch_host, sizeof(float) * nvox * C, cudaMemcpyHostToDevice, st));
+  s = sfseg_power_iterate(d_ch, C, w_host, b, act, sh, gauss, K, nullptr, d_x, nullptr, nullptr, 0, nullptr, ws,
+                          P.ws_fwd, nullptr, stream);
+  if (s != SFSEG_OK) return s;
+  s = sfseg_threshold(d_x, sh, tau, thr_mode, d_mask, static_cast<char*>(ws) + P.ws_fwd, thr_ws, stream);
+  if (s != SFSEG_OK) return s;
+  if (x_out_host) SF_CUDA(cudaMemcpyAsync(x_out_host, d_x, sizeof(float) * nvox, cudaMemcpyDeviceToHost, st));
+  if (mask_out_host) SF_CUDA(cudaMemcpyAsync(mask_out_host, d_mask, nvox, cudaMemcpyDeviceToHost, st));
+  return sfseg_sync_status(ws, stream);
+}
+
+sfseg_status sfseg_get_unique_id(uint8_t id_host[128]) {
+  if (!id_host) return SFSEG_ERR_INVALID_ARGUMENT;
+  NcclApi& api = nccl();
+  if (!api.ok) return SFSEG_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != ncclSuccess) return SFSEG_ERR_NCCL;
+  static_assert(sizeof(id.internal) == 128, "NCCL unique id size");
+  std::memcpy(id_host, id.internal, 128);
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_comm_create(const uint8_t id_host[128], int32_t nranks, int32_t rank, int32_t device,
+                               sfseg_comm** out) {
+  if (!id_host || !out || nranks < 1 || rank < 0 || rank >= nranks || device < 0) return SFSEG_ERR_INVALID_ARGUMENT;
+  NcclApi& api = nccl();
+  if (!api.ok) return SFSEG_ERR_UNSUPPORTED;
+  SF_CUDA(cudaSetDevice(device));
+  ncclUniqueId id;
+  std::memcpy(id.internal, id_host, 128);
+  sfseg_comm* c = new (std::nothrow) sfseg_comm;
+  if (!c) return SFSEG_ERR_CUDA;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  if (api.CommInitRank(&c->comm, nranks, id, rank) != ncclSuccess) {
+    delete c;
+    return SFSEG_ERR_NCCL;
+  }
+  *out = c;
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_comm_destroy(sfseg_comm* c) {
+  if (!c) return SFSEG_ERR_INVALID_ARGUMENT;
+  NcclApi& api = nccl();
+  sfseg_status s = SFSEG_OK;
+  if (c->comm && api.ok && api.CommDestroy(c->comm) != ncclSuccess) s = SFSEG_ERR_NCCL;
+  delete c;
+  return s;
+}
+
+sfseg_status sfseg_profile_enable(int32_t on) {
+  Profiler& p = prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  p.on = on != 0;
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_profile_read(double* ms_host, int64_t* count_host) {
+  if (!ms_host || !count_host) return SFSEG_ERR_INVALID_ARGUMENT;
+  Profiler& p = prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  for (int i = 0; i < PC_N; ++i) {
+    ms_host[i] = 0.0;
+    count_host[i] = 0;
+  }
+  sfseg_status s = SFSEG_OK;
+  for (ProfRec& r : p.recs) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess)
+      s = SFSEG_ERR_CUDA;
+    ms_host[r.cat] += ms;
+    count_host[r.cat] += 1;
+    p.pool.push_back(r.a);
+    p.pool.push_back(r.b);
+  }
+  p.recs.clear();
+  return s;
+}
+
+}  // extern "C"

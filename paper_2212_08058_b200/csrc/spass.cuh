@@ -1,0 +1,336 @@
+// Fused spatial pass of G_3D (x then y) + elementwise F multiplies
+// + per-iteration norm partials (Eq.8) -- the FP32-FMA-bound kernel of the path.
+//
+// Persistent, statically balanced: the work is the list of "row units"
+// (bt, strip, y) ordered bt-major, split into G equal contiguous ranges, one
+// per CTA.  A range decomposes into column segments (bt, strip, ya..yb); each
+// segment streams rows through:
+//   TMA (cp.async.bulk.tensor.3d, OOB zero fill = zero padding in x and y)
+//     -> stage[2][32 rows][BOXW] (double-buffered, mbarrier complete_tx)
+//   x-pass: lane = row, 8 consecutive outputs per thread, (2R+1) taps from the
+//     kernel-parameter constant bank -> q rows written twice into a ring
+//     (duplicated so every y window is contiguous: immediate-offset LDS.128)
+//   y-pass: lane = column quad, warp = row quad, 4x4 outputs per thread
+//   epilogue: forward  y = F u ; store p = F y (or y on the last iteration);
+//             tape u; partials of ||y||^2 and <p_{k-1}, u> (Rayleigh)
+//             backward (Appendix A): x_bar_{k-1} = F v, F_bar += y_bar u_{k-1} + x_{k-1} v,
+//             partials of <x_{k-1}, x_bar_{k-1}>
+// No x- or y-pass FMA is repeated except the 2R-row warm-up per segment
+// (about 1-3 % at the configs' sizes).  The last CTA to finish reduces the
+// per-CTA partials in fixed order in fp64 (deterministic) and writes the
+// per-volume norm / scale for the next launch.
+#pragma once
+#include "common.cuh"
+
+namespace sfseg {
+
+constexpr int kMaxRS = 48;
+
+__host__ __device__ constexpr int spass_boxw(int R) {
+  // smallest width >= kTW + 2R with width == 4 (mod 32): the TMA box row stride then
+  // makes the x-pass LDS.128 (lane = row) bank-conflict free.
+  return ((kTW + 2 * R - 4 + 31) / 32) * 32 + 4;
+}
+__host__ __device__ constexpr int spass_nslot(int R) { return (2 * R + kM - 1) / kM + 1; }
+__host__ __device__ constexpr size_t spass_smem_bytes(int R) {
+  return sizeof(float) * (2ull * kM * spass_boxw(R) + 2ull * spass_nslot(R) * kM * kRingStride) + 2 * 8 + 8 * 8 + 16;
+}
+
+enum SpassMode : int { SP_FWD = 0, SP_BWD = 1 };
+
+struct SpassParams {
+  CUtensorMap tmap;        // input volume (v): dims {W, H, B*T}, box {BOXW, kM, 1}, fp32
+  const float* F;          // pitched [B*T][H][Wp]
+  float* out;              // FWD: p (or y when last) ; BWD: x_bar (in place)
+  float* tape_u;           // FWD: record u (nullable)
+  const float* pprev;      // FWD: p_{k-1} for the Rayleigh quotient (nullable; may alias out)
+  const float* u1;         // BWD: tape u_{k-1}
+  const float* u2;         // BWD: tape u_{k-2} (k >= 2) or null
+  const float* x0p;        // BWD: pitched x_0 when the user gave one (k == 1), else null (x_0 = F)
+  float* Fbar;             // BWD: accumulated dL/dF
+  double* sc;              // per-volume scalars [B][kScal]
+  double* partials;        // [2][B][G]
+  unsigned* counter;
+  unsigned* err;
+  double* stats;           // FWD: [B][K][3] (nullable)
+  double* tape_nu;         // FWD writes nu_k; BWD reads nu
+  long U;                  // total row units = B*T*S*H
+  int B, T, H, W, Wp, S, G;
+  int K, k;                // iteration (FWD) or backward step (BWD), 1-based
+  int last;                // FWD: write y instead of p
+  float g[2 * kMaxRS + 1]; // g[i] = weight of spatial offset i - R (same taps for y and x)
+};
+
+template <int R>
+struct SpassGeom {
+  static constexpr int BOXW = spass_boxw(R);
+  static constexpr int NSLOT = spass_nslot(R);
+  static constexpr int RING_ROWS = NSLOT * kM;
+  static constexpr int XIN = ((8 + 2 * R) + 3) / 4 * 4;  // x-pass inputs per thread (float4 multiple)
+  static_assert(BOXW <= 256, "TMA box width limit");
+};
+
+struct Seg {
+  int bt, s, ya, yb;
+};
+
+__device__ __forceinline__ Seg seg_decode(long u, long u_end, int H, int S) {
+  Seg g;
+  const long col = u / H;
+  g.ya = (int)(u - col * H);
+  g.s = (int)(col % S);
+  g.bt = (int)(col / S);
+  const long rem = u_end - u;
+  g.yb = (int)min((long)H, (long)g.ya + rem);
+  return g;
+}
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_constant__ SpassParams P) {
+  using Geo = SpassGeom<R>;
+  constexpr int BOXW = Geo::BOXW;
+  constexpr int NSLOT = Geo::NSLOT;
+  constexpr int RING_ROWS = Geo::RING_ROWS;
+  constexpr int PRO = NSLOT - 1;  // x-blocks needed before the first y-block
+  constexpr unsigned STAGE_BYTES = kM * BOXW * sizeof(float);
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* stage = reinterpret_cast<float*>(smem);
+  float* ring = stage + 2 * kM * BOXW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * RING_ROWS * kRingStride);
+  double* red = reinterpret_cast<double*>(bars + 2);
+  int* flag = reinterpret_cast<int*>(red + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int H = P.H, W = P.W, Wp = P.Wp, S = P.S, T = P.T;
+  const long u_begin = (long)blockIdx.x * P.U / P.G;
+  const long u_end = (long)(blockIdx.x + 1) * P.U / P.G;
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+    prefetch_tmap(&P.tmap);
+  }
+  __syncthreads();
+
+  // ---- producer (thread 0): flat sequence of x-blocks over this CTA's segments
+  long pu = u_begin;
+  Seg pseg{};
+  int pn = 0, pnx = 0;
+  auto producer_issue = [&](int flat) {
+    if (pu >= u_end) return;
+    if (pn == 0) {
+      pseg = seg_decode(pu, u_end, H, S);
+      pnx = (pseg.yb - pseg.ya + 2 * R + kM - 1) / kM;
+    }
+    const int st = flat & 1;
+    mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
+    tma_load_3d(stage + st * kM * BOXW, &P.tmap, &bars[st], pseg.s * kTW - R, pseg.ya - R + pn * kM, pseg.bt);
+    if (++pn == pnx) {
+      pn = 0;
+      pu += pseg.yb - pseg.ya;
+    }
+  };
+  if (tid == 0) {
+    producer_issue(0);
+    producer_issue(1);
+  }
+
+  double acc0 = 0.0, acc1 = 0.0;  // per-thread partial sums of the current volume
+  int cur_vol = -1;
+  auto flush = [&](int vol) {
+    const double s0 = block_sum<kSpassThreads>(acc0, red);
+    const double s1 = block_sum<kSpassThreads>(acc1, red);
+    if (tid == 0) {
+      P.partials[(long)vol * P.G + blockIdx.x] = s0;
+      P.partials[(long)(P.B + vol) * P.G + blockIdx.x] = s1;
+    }
+    acc0 = acc1 = 0.0;
+  };
+
+  // per-volume scalars for the backward epilogue (refreshed per segment)
+  float cn = 0.f, inv_nu = 0.f, inv_nu_prev = 0.f;
+
+  int flat = 0;
+  long u = u_begin;
+  while (u < u_end) {
+    const Seg sg = seg_decode(u, u_end, H, S);
+    const int L = sg.yb - sg.ya;
+    const int nxb = (L + 2 * R + kM - 1) / kM;
+    const int nyb = (L + kM - 1) / kM;
+    const int vol = sg.bt / T;
+    if (vol != cur_vol) {
+      if (cur_vol >= 0) flush(cur_vol);
+      cur_vol = vol;
+      if (MODE == SP_BWD) {
+        cn = (float)P.sc[vol * kScal + SC_CN];
+        inv_nu = (float)P.sc[vol * kScal + SC_INV_NU];
+        inv_nu_prev = (float)P.sc[vol * kScal + SC_INV_NU_PREV];
+      }
+    }
+
+    // ---------------------------------------------------------------- y-pass + epilogue
+    auto ypass = [&](int m) {
+      const float* wb = ring + ((m % NSLOT) * kM + 4 * warp) * kRingStride + 4 * lane;
+      float4 a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 4 + 2 * R; ++j) {
+        const float4 q = *reinterpret_cast<const float4*>(wb + j * kRingStride);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int kk = j - i;
+          if (kk >= 0 && kk <= 2 * R) {
+            const float gk = P.g[kk];
+            a[i].x = fmaf(gk, q.x, a[i].x);
+            a[i].y = fmaf(gk, q.y, a[i].y);
+            a[i].z = fmaf(gk, q.z, a[i].z);
+            a[i].w = fmaf(gk, q.w, a[i].w);
+          }
+        }
+      }
+      const int x = sg.s * kTW + 4 * lane;
+      if (x >= W) return;
+      const float m1 = (x + 1 < W) ? 1.f : 0.f, m2 = (x + 2 < W) ? 1.f : 0.f, m3 = (x + 3 < W) ? 1.f : 0.f;
+      const float4 msk = make_float4(1.f, m1, m2, m3);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int y = sg.ya + m * kM + 4 * warp + i;
+        if (y >= sg.yb) break;
+        const long off = ((long)sg.bt * H + y) * Wp + x;
+        const float4 f = f4_mul(*reinterpret_cast<const float4*>(P.F + off), msk);
+        const float4 uu = f4_mul(a[i], msk);
+        if (MODE == SP_FWD) {
+          const float4 yv = f4_mul(f, uu);
+          acc0 += (double)f4_dot(yv, yv);
+          if (P.pprev) acc1 += (double)f4_dot(*reinterpret_cast<const float4*>(P.pprev + off), uu);
+          if (P.tape_u) *reinterpret_cast<float4*>(P.tape_u + off) = uu;
+          *reinterpret_cast<float4*>(P.out + off) = P.last ? yv : f4_mul(f, yv);
+        } else {
+          const float4 xb = *reinterpret_cast<const float4*>(P.out + off);
+          const float4 u1 = *reinterpret_cast<const float4*>(P.u1 + off);
+          float4 xp;
+          if (P.u2) xp = f4_scale(f4_mul(f, *reinterpret_cast<const float4*>(P.u2 + off)), inv_nu_prev);
+          else if (P.x0p) xp = f4_mul(*reinterpret_cast<const float4*>(P.x0p + off), msk);
+          else xp = f;
+          float4 yb;
+          yb.x = (xb.x - f.x * u1.x * cn) * inv_nu;
+          yb.y = (xb.y - f.y * u1.y * cn) * inv_nu;
+          yb.z = (xb.z - f.z * u1.z * cn) * inv_nu;
+          yb.w = (xb.w - f.w * u1.w * cn) * inv_nu;
+          float4 fb = *reinterpret_cast<const float4*>(P.Fbar + off);
+          fb.x += yb.x * u1.x + xp.x * uu.x;
+          fb.y += yb.y * u1.y + xp.y * uu.y;
+          fb.z += yb.z * u1.z + xp.z * uu.z;
+          fb.w += yb.w * u1.w + xp.w * uu.w;
+          *reinterpret_cast<float4*>(P.Fbar + off) = fb;
+          const float4 xn = f4_mul(f, uu);
+          *reinterpret_cast<float4*>(P.out + off) = xn;
+          acc0 += (double)f4_dot(xp, xn);
+        }
+      }
+    };
+
+    for (int n = 0; n < nxb; ++n, ++flat) {
+      const int st = flat & 1;
+      mbar_wait(&bars[st], (flat >> 1) & 1);
+      // ------------------------------------------------------------ x-pass of block n
+      {
+        const float* srow = stage + st * kM * BOXW + lane * BOXW;
+        const int sl = n % NSLOT;
+        float* r0 = ring + (sl * kM + lane) * kRingStride;
+        float* r1 = r0 + RING_ROWS * kRingStride;
+#pragma unroll 1
+        for (int oi = 0; oi < 2; ++oi) {
+          const int o = warp + 8 * oi;
+          float in[Geo::XIN];
+#pragma unroll
+          for (int i = 0; i < Geo::XIN / 4; ++i) {
+            const float4 v4 = *reinterpret_cast<const float4*>(srow + 8 * o + 4 * i);
+            in[4 * i + 0] = v4.x;
+            in[4 * i + 1] = v4.y;
+            in[4 * i + 2] = v4.z;
+            in[4 * i + 3] = v4.w;
+          }
+          float a[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) a[j] = 0.f;
+#pragma unroll
+          for (int kk = 0; kk <= 2 * R; ++kk) {
+            const float gk = P.g[kk];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = fmaf(gk, in[j + kk], a[j]);
+          }
+          const float4 lo = make_float4(a[0], a[1], a[2], a[3]);
+          const float4 hi = make_float4(a[4], a[5], a[6], a[7]);
+          *reinterpret_cast<float4*>(r0 + 8 * o) = lo;
+          *reinterpret_cast<float4*>(r0 + 8 * o + 4) = hi;
+          *reinterpret_cast<float4*>(r1 + 8 * o) = lo;
+          *reinterpret_cast<float4*>(r1 + 8 * o + 4) = hi;
+        }
+      }
+      __syncthreads();  // stage st consumed; ring slot visible
+      if (tid == 0) {
+        fence_proxy_async();
+        producer_issue(flat + 2);
+      }
+      if (n >= PRO && n - PRO < nyb) ypass(n - PRO);
+      __syncthreads();  // ring slot (n+1) % NSLOT may be overwritten next
+    }
+    for (int m = max(0, nxb - PRO); m < nyb; ++m) ypass(m);
+    __syncthreads();
+    u += L;
+  }
+  if (cur_vol >= 0) flush(cur_vol);
+
+  // ---------------------------------------------------------------- last CTA: fixed-order fp64 finalize
+  if (!last_block_arrive(P.counter, (unsigned)P.G, flag)) return;
+  const long per_vol = P.U / P.B;  // units per volume
+  for (int b = warp; b < P.B; b += kSpassThreads / 32) {
+    const long vs = (long)b * per_vol, ve = vs + per_vol;
+    double s0 = 0.0, s1 = 0.0;
+    for (int c = lane; c < P.G; c += 32) {
+      const long cs = (long)c * P.U / P.G, ce = (long)(c + 1) * P.U / P.G;
+      if (cs < ve && ce > vs) {
+        s0 += P.partials[(long)b * P.G + c];
+        s1 += P.partials[(long)(P.B + b) * P.G + c];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (lane == 0) {
+      double* sc = P.sc + b * kScal;
+      if (MODE == SP_FWD) {
+        const double nu = sqrt(s0);
+        const double xn = sc[SC_XNORM];
+        if (P.stats) {
+          double* st = P.stats + ((long)b * P.K + (P.k - 1)) * 3;
+          st[0] = nu;
+          st[1] = nu / xn;
+          st[2] = P.pprev ? sc[SC_S] * s1 / (xn * xn) : 0.0;
+        }
+        if (P.tape_nu) P.tape_nu[(long)b * P.K + (P.k - 1)] = nu;
+        flag_norm(P.err, nu);
+        sc[SC_S] = 1.0 / nu;
+        sc[SC_XNORM] = 1.0;
+        sc[SC_NU] = nu;
+      } else {
+        // step k produced x_bar_{k-1}; s0 = c_{k-1} = <x_{k-1}, x_bar_{k-1}>
+        if (P.k >= 2) {
+          const double nu1 = P.tape_nu[(long)b * P.K + (P.k - 2)];
+          sc[SC_CN] = s0 / nu1;
+          sc[SC_INV_NU] = 1.0 / nu1;
+          sc[SC_INV_NU_PREV] = (P.k >= 3) ? 1.0 / P.tape_nu[(long)b * P.K + (P.k - 3)] : 0.0;
+        }
+      }
+    }
+  }
+  if (tid == 0) *P.counter = 0u;
+}
+
+}  // namespace sfseg

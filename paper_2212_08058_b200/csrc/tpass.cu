@@ -1,0 +1,26 @@
+// Temporal-pass instantiations (all compiled temporal radii, forward + adjoint).
+#include "launch.h"
+
+namespace sfseg {
+template <int MODE>
+static cudaError_t launch_tpass_t(int RT, const TpassParams& P, int B, cudaStream_t st) {
+  dim3 grid((unsigned)((P.frame4 + 255) / 256), (unsigned)B);
+  switch (RT) {
+#define TP_CASE(r)                                  \
+  case r:                                           \
+    tpass_kernel<r, MODE><<<grid, 256, 0, st>>>(P); \
+    return cudaGetLastError();
+    TP_CASE(0) TP_CASE(1) TP_CASE(2) TP_CASE(3) TP_CASE(4) TP_CASE(5) TP_CASE(6) TP_CASE(8) TP_CASE(9)
+    TP_CASE(12) TP_CASE(16)
+#undef TP_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t st) {
+  return launch_tpass_t<TP_FWD>(RT, P, B, st);
+}
+cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st) {
+  return launch_tpass_t<TP_BWD>(RT, P, B, st);
+}
+}  // namespace sfseg

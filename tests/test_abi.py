@@ -1,0 +1,86 @@
+"""C-ABI contract checks that need no GPU: the in-tree libsfseg.so loads,
+exports every function include/sfseg.h declares, and host-only entry points
+validate arguments before touching the device."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_2212_08058_b200 as sf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sfseg.h")
+
+
+def _declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sfseg_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2212_08058_b200 import build
+    build.build()
+    return sf.lib()
+
+
+def test_header_declares_the_north_star_calls():
+    names = _declared_functions()
+    for n in ("sfseg_combine_channels", "sfseg_power_iterate", "sfseg_power_iterate_backward",
+              "sfseg_threshold"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    names = _declared_functions()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in sfseg.h but not exported"
+
+
+def test_status_strings_and_version(lib):
+    assert lib.sfseg_abi_version() == 1
+    for s in range(9):
+        assert lib.sfseg_status_string(s)
+    rs, rt = C.c_int32(), C.c_int32()
+    lib.sfseg_max_radii(C.byref(rs), C.byref(rt))
+    assert rs.value >= 36 and rt.value >= 9
+
+
+def test_workspace_query_and_validation(lib):
+    g = sf.Gauss(2.0, 8.0)
+    ws, tape = sf.workspace_bytes((1, 70, 480, 854), 1, g, 15, want_tape=True)
+    vol = 70 * 480 * 856 * 4
+    assert ws >= 6 * vol and tape >= 15 * vol
+    ws2, tape2 = sf.workspace_bytes((1, 70, 480, 854), 1, g, 15, want_tape=False)
+    assert ws2 < ws and tape2 == 0
+    with pytest.raises(sf.SfsegError) as e:
+        sf.workspace_bytes((1, 0, 4, 4), 1, g, 3)
+    assert e.value.status == 2
+    with pytest.raises(sf.SfsegError) as e:
+        sf.workspace_bytes((1, 4, 4, 4), 1, sf.Gauss(-1.0, 1.0), 3)
+    assert e.value.status == 1
+    with pytest.raises(sf.SfsegError) as e:
+        sf.workspace_bytes((1, 4, 4, 4), 0, g, 3)
+    assert e.value.status == 1
+    with pytest.raises(sf.SfsegError) as e:
+        sf.workspace_bytes((1, 4, 4, 4), 1, g, 0)
+    assert e.value.status == 1
+    with pytest.raises(sf.SfsegError) as e:   # radius above the compiled maximum
+        sf.workspace_bytes((1, 4, 4, 4), 1, sf.Gauss(2.0, 30.0), 3)
+    assert e.value.status == 2
+
+
+def test_null_pointers_rejected_before_launch(lib):
+    shp = sf.Shape(1, 2, 3, 4)
+    g = sf.Gauss(1.0, 1.0).c()
+    w = (C.c_float * 1)(1.0)
+    assert lib.sfseg_power_iterate(None, 1, w, 0.0, 0, shp, g, 2, None, None, None, None, 0, None,
+                                   None, 0, None, None) == 1
+    assert lib.sfseg_threshold(None, shp, 0.5, 0, None, None, 0, None) == 1
+    assert lib.sfseg_combine_channels(None, 1, shp, w, 0.0, 0, None, None) == 1
+    assert lib.sfseg_power_iterate_backward(None, 1, w, 0.0, 0, shp, g, 2, None, None, None, None, None,
+                                            None, 0, None, None) == 1
+    assert lib.sfseg_sync_status(None, None) == 1
