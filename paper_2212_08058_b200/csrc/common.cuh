@@ -15,10 +15,11 @@
 
 namespace sfseg {
 
-constexpr int kTW = 128;        // output columns per spatial-pass strip
+constexpr int kTW = 64;         // output columns per spatial-pass strip
 constexpr int kM = 32;          // rows per spatial-pass block
-constexpr int kSpassThreads = 256;
-constexpr int kRingStride = 132;  // ring row stride in floats (== 4 mod 32: conflict-free)
+constexpr int kSpassThreads = 128;
+constexpr int kSpassWarps = kSpassThreads / 32;
+constexpr int kRingStride = kTW + 4;  // ring row stride in floats (== 4 mod 32: conflict-free)
 constexpr int kMaxC = 64;       // channels passed by value in kernel parameters
 constexpr int kScal = 8;        // doubles of per-volume scalars
 
@@ -99,9 +100,10 @@ __device__ __forceinline__ bool last_block_arrive(unsigned* counter, unsigned to
   return last;
 }
 
+// First device-detected error wins (a zero norm at k makes every later norm NaN).
 __device__ __forceinline__ void flag_norm(unsigned* err, double nu) {
-  if (!isfinite(nu)) atomicOr(err, ERR_NONFINITE);
-  else if (!(nu > 0.0)) atomicOr(err, ERR_DEGENERATE);
+  if (!isfinite(nu)) atomicCAS(err, 0u, (unsigned)ERR_NONFINITE);
+  else if (!(nu > 0.0)) atomicCAS(err, 0u, (unsigned)ERR_DEGENERATE);
 }
 
 // ---------------------------------------------------------------- mbarrier / TMA (sm_90+ PTX)

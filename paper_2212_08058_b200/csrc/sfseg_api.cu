@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -36,6 +37,22 @@ namespace {
 
 cudaError_t& last_cuda_error() {
   static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+
+// SFSEG_DEBUG_SYNC=1: synchronise after every launch and name the failing kernel.
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFSEG_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+cudaError_t after_launch(const char* name, cudaStream_t st) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && debug_sync()) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess && debug_sync()) fprintf(stderr, "[sfseg] kernel %s failed: %s\n", name, cudaGetErrorString(e));
   return e;
 }
 
@@ -435,7 +452,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
   cp.p0 = p;
   cp.F_out = F_out;
   combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
-  SF_CUDA(cudaGetLastError());
+  SF_CUDA(after_launch("combine", st));
 
   SpassParams sp;
   std::memset(&sp, 0, sizeof(sp));
@@ -454,6 +471,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     {
       ProfScope ps(st, PC_TPASS);
       SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
+      SF_CUDA(after_launch("tpass_fwd", st));
     }
     // (a4)-(a7) u = G_y G_x v ; y_k = F u ; p_k = F y_k ; ||y_k||, <p_{k-1}, u>
     sp.out = p;
@@ -464,6 +482,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     {
       ProfScope ps(st, PC_SPASS);
       SF_CUDA(launch_spass_fwd(P.RS, sp, P.G, st));
+      SF_CUDA(after_launch("spass_fwd", st));
     }
   }
   // (a8) x_K = y_K / nu_K (dense output)
@@ -472,7 +491,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(per, 64)), (unsigned)P.BT);
     final_scale_kernel<<<grid, kEwThreads, 0, st>>>(p, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H, (int)P.W,
                                                     (int)P.Wp);
-    SF_CUDA(cudaGetLastError());
+    SF_CUDA(after_launch("final_scale", st));
   }
   return SFSEG_OK;
 }
@@ -510,7 +529,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
   cp.F = F;
   cp.x0p = x0p;
   combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
-  SF_CUDA(cudaGetLastError());
+  SF_CUDA(after_launch("combine", st));
 
   BwdInitParams ip;
   std::memset(&ip, 0, sizeof(ip));
@@ -531,7 +550,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
   ip.K = K;
   ip.gx = P.gx;
   bwd_init_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ip);
-  SF_CUDA(cudaGetLastError());
+  SF_CUDA(after_launch("bwd_init", st));
 
   SpassParams sp;
   std::memset(&sp, 0, sizeof(sp));
@@ -552,6 +571,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
     {
       ProfScope ps(st, PC_BWD);
       SF_CUDA(launch_tpass_bwd(P.RT, tp, (int)P.B, st));
+      SF_CUDA(after_launch("tpass_bwd", st));
     }
     sp.u1 = tape_u(k - 1);
     sp.u2 = (k >= 2) ? tape_u(k - 2) : nullptr;
@@ -559,6 +579,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
     {
       ProfScope ps(st, PC_BWD);
       SF_CUDA(launch_spass_bwd(P.RS, sp, P.G, st));
+      SF_CUDA(after_launch("spass_bwd", st));
     }
   }
 
@@ -586,7 +607,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
   else if (C <= 8) contract_kernel<8><<<G2, kEwThreads, 0, st>>>(cc);
   else if (C <= 16) contract_kernel<16><<<G2, kEwThreads, 0, st>>>(cc);
   else contract_kernel<kMaxC><<<G2, kEwThreads, 0, st>>>(cc);
-  SF_CUDA(cudaGetLastError());
+  SF_CUDA(after_launch("contract", st));
   std::vector<double> out(C + 1);
   SF_CUDA(cudaMemcpyAsync(out.data(), cc.out, sizeof(double) * (C + 1), cudaMemcpyDeviceToHost, st));
   s = sfseg_sync_status(ws, stream);

@@ -26,10 +26,14 @@ namespace sfseg {
 
 constexpr int kMaxRS = 48;
 
+// The TMA box starts at column x0 - RA with RA = round_up(R, 4): a box whose start
+// is not 16-byte aligned faults on sm_100a (measured: R % 4 != 0 gave
+// "illegal instruction"), so the x-pass reads its taps at offset D = RA - R.
+__host__ __device__ constexpr int spass_ra(int R) { return (R + 3) / 4 * 4; }
 __host__ __device__ constexpr int spass_boxw(int R) {
-  // smallest width >= kTW + 2R with width == 4 (mod 32): the TMA box row stride then
+  // smallest width >= kTW + 2 RA with width == 4 (mod 32): the TMA box row stride then
   // makes the x-pass LDS.128 (lane = row) bank-conflict free.
-  return ((kTW + 2 * R - 4 + 31) / 32) * 32 + 4;
+  return ((kTW + 2 * spass_ra(R) - 4 + 31) / 32) * 32 + 4;
 }
 __host__ __device__ constexpr int spass_nslot(int R) { return (2 * R + kM - 1) / kM + 1; }
 __host__ __device__ constexpr size_t spass_smem_bytes(int R) {
@@ -66,7 +70,9 @@ struct SpassGeom {
   static constexpr int BOXW = spass_boxw(R);
   static constexpr int NSLOT = spass_nslot(R);
   static constexpr int RING_ROWS = NSLOT * kM;
-  static constexpr int XIN = ((8 + 2 * R) + 3) / 4 * 4;  // x-pass inputs per thread (float4 multiple)
+  static constexpr int RA = spass_ra(R);
+  static constexpr int D = RA - R;                           // tap offset inside the aligned box
+  static constexpr int XIN = ((8 + 2 * R + D) + 3) / 4 * 4;  // x-pass inputs per thread (float4 multiple)
   static_assert(BOXW <= 256, "TMA box width limit");
 };
 
@@ -86,7 +92,7 @@ __device__ __forceinline__ Seg seg_decode(long u, long u_end, int H, int S) {
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_constant__ SpassParams P) {
+__global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_constant__ SpassParams P) {
   using Geo = SpassGeom<R>;
   constexpr int BOXW = Geo::BOXW;
   constexpr int NSLOT = Geo::NSLOT;
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_co
     }
     const int st = flat & 1;
     mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
-    tma_load_3d(stage + st * kM * BOXW, &P.tmap, &bars[st], pseg.s * kTW - R, pseg.ya - R + pn * kM, pseg.bt);
+    tma_load_3d(stage + st * kM * BOXW, &P.tmap, &bars[st], pseg.s * kTW - Geo::RA, pseg.ya - R + pn * kM, pseg.bt);
     if (++pn == pnx) {
       pn = 0;
       pu += pseg.yb - pseg.ya;
@@ -171,8 +177,35 @@ __global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_co
     }
 
     // ---------------------------------------------------------------- y-pass + epilogue
-    auto ypass = [&](int m) {
-      const float* wb = ring + ((m % NSLOT) * kM + 4 * warp) * kRingStride + 4 * lane;
+    // thread: column quad cq (4 columns), row quad rq (4 rows) of the 32-row block
+    const int cq = lane & 15;
+    const int rq = warp * 2 + (lane >> 4);
+    const int x = sg.s * kTW + 4 * cq;
+    const bool xok = x < W;
+    const float4 msk = make_float4(1.f, (x + 1 < W) ? 1.f : 0.f, (x + 2 < W) ? 1.f : 0.f, (x + 3 < W) ? 1.f : 0.f);
+    struct Pre {
+      float4 f[4], a[4], c[4];
+    };
+    // issue the epilogue's global loads early so their latency overlaps the FMAs
+    auto prefetch = [&](int m, Pre& pr) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int y = sg.ya + m * kM + 4 * rq + i;
+        pr.f[i] = pr.a[i] = pr.c[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (xok && y < sg.yb) {
+          const long off = ((long)sg.bt * H + y) * Wp + x;
+          pr.f[i] = *reinterpret_cast<const float4*>(P.F + off);
+          if (MODE == SP_FWD) {
+            if (P.pprev) pr.a[i] = *reinterpret_cast<const float4*>(P.pprev + off);
+          } else {
+            pr.a[i] = *reinterpret_cast<const float4*>(P.out + off);
+            pr.c[i] = *reinterpret_cast<const float4*>(P.u1 + off);
+          }
+        }
+      }
+    };
+    auto ypass = [&](int m, const Pre& pr) {
+      const float* wb = ring + ((m % NSLOT) * kM + 4 * rq) * kRingStride + 4 * cq;
       float4 a[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -191,26 +224,23 @@ __global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_co
           }
         }
       }
-      const int x = sg.s * kTW + 4 * lane;
-      if (x >= W) return;
-      const float m1 = (x + 1 < W) ? 1.f : 0.f, m2 = (x + 2 < W) ? 1.f : 0.f, m3 = (x + 3 < W) ? 1.f : 0.f;
-      const float4 msk = make_float4(1.f, m1, m2, m3);
+      if (!xok) return;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int y = sg.ya + m * kM + 4 * warp + i;
+        const int y = sg.ya + m * kM + 4 * rq + i;
         if (y >= sg.yb) break;
         const long off = ((long)sg.bt * H + y) * Wp + x;
-        const float4 f = f4_mul(*reinterpret_cast<const float4*>(P.F + off), msk);
+        const float4 f = f4_mul(pr.f[i], msk);
         const float4 uu = f4_mul(a[i], msk);
         if (MODE == SP_FWD) {
           const float4 yv = f4_mul(f, uu);
           acc0 += (double)f4_dot(yv, yv);
-          if (P.pprev) acc1 += (double)f4_dot(*reinterpret_cast<const float4*>(P.pprev + off), uu);
+          if (P.pprev) acc1 += (double)f4_dot(pr.a[i], uu);
           if (P.tape_u) *reinterpret_cast<float4*>(P.tape_u + off) = uu;
           *reinterpret_cast<float4*>(P.out + off) = P.last ? yv : f4_mul(f, yv);
         } else {
-          const float4 xb = *reinterpret_cast<const float4*>(P.out + off);
-          const float4 u1 = *reinterpret_cast<const float4*>(P.u1 + off);
+          const float4 xb = pr.a[i];
+          const float4 u1 = pr.c[i];
           float4 xp;
           if (P.u2) xp = f4_scale(f4_mul(f, *reinterpret_cast<const float4*>(P.u2 + off)), inv_nu_prev);
           else if (P.x0p) xp = f4_mul(*reinterpret_cast<const float4*>(P.x0p + off), msk);
@@ -235,6 +265,9 @@ __global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_co
 
     for (int n = 0; n < nxb; ++n, ++flat) {
       const int st = flat & 1;
+      const bool do_y = (n >= PRO) && (n - PRO < nyb);
+      Pre pre;
+      if (do_y) prefetch(n - PRO, pre);
       mbar_wait(&bars[st], (flat >> 1) & 1);
       // ------------------------------------------------------------ x-pass of block n
       {
@@ -243,8 +276,8 @@ __global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_co
         float* r0 = ring + (sl * kM + lane) * kRingStride;
         float* r1 = r0 + RING_ROWS * kRingStride;
 #pragma unroll 1
-        for (int oi = 0; oi < 2; ++oi) {
-          const int o = warp + 8 * oi;
+        for (int oi = 0; oi < kTW / 8 / kSpassWarps; ++oi) {
+          const int o = warp + kSpassWarps * oi;
           float in[Geo::XIN];
 #pragma unroll
           for (int i = 0; i < Geo::XIN / 4; ++i) {
@@ -261,7 +294,7 @@ __global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_co
           for (int kk = 0; kk <= 2 * R; ++kk) {
             const float gk = P.g[kk];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = fmaf(gk, in[j + kk], a[j]);
+            for (int j = 0; j < 8; ++j) a[j] = fmaf(gk, in[j + kk + Geo::D], a[j]);
           }
           const float4 lo = make_float4(a[0], a[1], a[2], a[3]);
           const float4 hi = make_float4(a[4], a[5], a[6], a[7]);
@@ -276,10 +309,14 @@ __global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_co
         fence_proxy_async();
         producer_issue(flat + 2);
       }
-      if (n >= PRO && n - PRO < nyb) ypass(n - PRO);
+      if (do_y) ypass(n - PRO, pre);
       __syncthreads();  // ring slot (n+1) % NSLOT may be overwritten next
     }
-    for (int m = max(0, nxb - PRO); m < nyb; ++m) ypass(m);
+    for (int m = max(0, nxb - PRO); m < nyb; ++m) {
+      Pre pre;
+      prefetch(m, pre);
+      ypass(m, pre);
+    }
     __syncthreads();
     u += L;
   }
@@ -288,7 +325,7 @@ __global__ void __launch_bounds__(kSpassThreads, 1) spass_kernel(const __grid_co
   // ---------------------------------------------------------------- last CTA: fixed-order fp64 finalize
   if (!last_block_arrive(P.counter, (unsigned)P.G, flag)) return;
   const long per_vol = P.U / P.B;  // units per volume
-  for (int b = warp; b < P.B; b += kSpassThreads / 32) {
+  for (int b = warp; b < P.B; b += kSpassWarps) {
     const long vs = (long)b * per_vol, ve = vs + per_vol;
     double s0 = 0.0, s1 = 0.0;
     for (int c = lane; c < P.G; c += 32) {
