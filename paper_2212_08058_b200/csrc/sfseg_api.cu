@@ -132,12 +132,15 @@ bool make_volume_tmap(CUtensorMap* map, const float* base, int64_t W, int64_t H,
 }
 
 int spass_occupancy(int R) {
-  static int occ[64] = {0};
-  if (R < 0 || R >= 64) return 1;
-  if (occ[R] == 0) {
-    occ[R] = (spass_smem_bytes(R) * 2 + 2048 <= 227 * 1024) ? 2 : 1;
+  switch (R) {
+#define OC(r) \
+  case r:     \
+    return spass_ctas_per_sm(r);
+    OC(1) OC(2) OC(3) OC(4) OC(5) OC(6) OC(8) OC(9) OC(12) OC(16) OC(18) OC(24) OC(32) OC(36) OC(48)
+#undef OC
+    default:
+      return 1;
   }
-  return occ[R];
 }
 
 // ------------------------------------------------------------------ optional per-kernel event timing
@@ -200,7 +203,8 @@ struct Plan {
   float gs[2 * kMaxRS + 1];
   int64_t vol_elems;  // B*T*H*Wp
   int S;              // strips
-  int64_t U;          // spass row units
+  int NB;             // 32-row blocks per column
+  int64_t U;          // spass block units
   int G;              // spass grid
   int gx;             // elementwise grid.x per frame
   // workspace offsets
@@ -233,9 +237,10 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   gauss_taps(g.sigma_s, P->rs, P->RS, P->gs);
   P->vol_elems = P->BT * P->H * P->Wp;
   P->S = (int)((sh.W + kTW - 1) / kTW);
-  P->U = P->BT * P->S * P->H;
+  P->NB = (int)((sh.H + kM - 1) / kM);
+  P->U = P->BT * P->S * P->NB;
   const int64_t cap = (int64_t)num_sms() * spass_occupancy(P->RS);
-  P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 64));
+  P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 4));
   const int64_t per_frame = (P->H * P->Wp + 256 * 4 - 1) / (256 * 4);
   P->gx = (int)std::max<int64_t>(1, std::min<int64_t>(per_frame, 16));
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
@@ -318,9 +323,10 @@ void fill_spass_common(SpassParams& sp, const Plan& P, void* ws) {
   sp.W = (int)P.W;
   sp.Wp = (int)P.Wp;
   sp.S = P.S;
+  sp.NB = P.NB;
   sp.G = P.G;
   sp.K = P.K;
-  for (int i = 0; i < 2 * P.RS + 1; ++i) sp.g[i] = P.gs[i];
+  for (int d = 0; d <= P.RS; ++d) sp.g[d] = P.gs[P.RS + d];
 }
 
 void fill_tpass_common(TpassParams& tp, const Plan& P, void* ws) {

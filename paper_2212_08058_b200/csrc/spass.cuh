@@ -31,13 +31,31 @@ constexpr int kMaxRS = 48;
 // "illegal instruction"), so the x-pass reads its taps at offset D = RA - R.
 __host__ __device__ constexpr int spass_ra(int R) { return (R + 3) / 4 * 4; }
 __host__ __device__ constexpr int spass_boxw(int R) {
-  // smallest width >= kTW + 2 RA with width == 4 (mod 32): the TMA box row stride then
-  // makes the x-pass LDS.128 (lane = row) bank-conflict free.
-  return ((kTW + 2 * spass_ra(R) - 4 + 31) / 32) * 32 + 4;
+  // smallest width >= kTW + 2 RA with width == 4 (mod 8): a row stride of 4*odd floats
+  // makes the x-pass LDS.128 (lane = row, 8 lanes per phase) bank-conflict free.
+  return ((kTW + 2 * spass_ra(R) - 4 + 7) / 8) * 8 + 4;
 }
-__host__ __device__ constexpr int spass_nslot(int R) { return (2 * R + kM - 1) / kM + 1; }
-__host__ __device__ constexpr size_t spass_smem_bytes(int R) {
-  return sizeof(float) * (2ull * kM * spass_boxw(R) + 2ull * spass_nslot(R) * kM * kRingStride) + 2 * 8 + 8 * 8 + 16;
+// x-block grid offset: the grid of 32-row x-blocks starts OFF rows above y_a - R.
+// OFF = (-R) mod 32 aligns the grid to image rows (blocks entirely above row 0 or
+// below row H are then skipped: no FMAs on zero padding) whenever that costs no
+// extra ring slot; otherwise 0.
+__host__ __device__ constexpr int spass_off(int R) {
+  return ((((32 - R % 32) % 32) + 2 * R + kM - 1) / kM == (2 * R + kM - 1) / kM) ? ((32 - R % 32) % 32) : 0;
+}
+__host__ __device__ constexpr int spass_pro(int R) { return (spass_off(R) + 2 * R + kM - 1) / kM; }
+__host__ __device__ constexpr int spass_nslot(int R) { return spass_pro(R) + 1; }
+__host__ __device__ constexpr size_t spass_smem_for(int R, int stages) {
+  return sizeof(float) * ((size_t)stages * kM * spass_boxw(R) + 2ull * spass_nslot(R) * kM * kRingStride) + 2 * 8 +
+         8 * 8 + 16;
+}
+constexpr size_t kSmemPerSM = 227 * 1024;
+// TMA stages: double-buffered unless a single stage is what lets 3 CTAs share an SM.
+__host__ __device__ constexpr int spass_stages(int R) {
+  return (3 * (spass_smem_for(R, 2) + 1024) <= kSmemPerSM) ? 2 : ((3 * (spass_smem_for(R, 1) + 1024) <= kSmemPerSM) ? 1 : 2);
+}
+__host__ __device__ constexpr size_t spass_smem_bytes(int R) { return spass_smem_for(R, spass_stages(R)); }
+__host__ __device__ constexpr int spass_ctas_per_sm(int R) {
+  return (int)(kSmemPerSM / (spass_smem_bytes(R) + 1024)) < 4 ? (int)(kSmemPerSM / (spass_smem_bytes(R) + 1024)) : 4;
 }
 
 enum SpassMode : int { SP_FWD = 0, SP_BWD = 1 };
@@ -58,11 +76,11 @@ struct SpassParams {
   unsigned* err;
   double* stats;           // FWD: [B][K][3] (nullable)
   double* tape_nu;         // FWD writes nu_k; BWD reads nu
-  long U;                  // total row units = B*T*S*H
-  int B, T, H, W, Wp, S, G;
+  long U;                  // total block units = B*T*S*NB (NB = ceil(H/32))
+  int B, T, H, W, Wp, S, NB, G;
   int K, k;                // iteration (FWD) or backward step (BWD), 1-based
   int last;                // FWD: write y instead of p
-  float g[2 * kMaxRS + 1]; // g[i] = weight of spatial offset i - R (same taps for y and x)
+  float g[kMaxRS + 1];     // g[d] = weight of spatial offset +-d (same taps for y and x)
 };
 
 template <int R>
@@ -72,43 +90,45 @@ struct SpassGeom {
   static constexpr int RING_ROWS = NSLOT * kM;
   static constexpr int RA = spass_ra(R);
   static constexpr int D = RA - R;                           // tap offset inside the aligned box
-  static constexpr int XIN = ((8 + 2 * R + D) + 3) / 4 * 4;  // x-pass inputs per thread (float4 multiple)
+  static constexpr int XO = 16;                               // x-pass outputs per thread (one row)
+  static constexpr int XIN = ((XO + 2 * R + D) + 3) / 4 * 4;  // x-pass inputs per thread (float4 multiple)
   static_assert(BOXW <= 256, "TMA box width limit");
 };
 
 struct Seg {
-  int bt, s, ya, yb;
+  int bt, s, yb0, yb1;  // column segment: 32-row output blocks [yb0, yb1) of strip s, frame bt
 };
 
-__device__ __forceinline__ Seg seg_decode(long u, long u_end, int H, int S) {
+__device__ __forceinline__ Seg seg_decode(long u, long u_end, int NB, int S) {
   Seg g;
-  const long col = u / H;
-  g.ya = (int)(u - col * H);
+  const long col = u / NB;
+  g.yb0 = (int)(u - col * NB);
   g.s = (int)(col % S);
   g.bt = (int)(col / S);
-  const long rem = u_end - u;
-  g.yb = (int)min((long)H, (long)g.ya + rem);
+  g.yb1 = (int)min((long)NB, (long)g.yb0 + (u_end - u));
   return g;
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_constant__ SpassParams P) {
+__global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_constant__ SpassParams P) {
   using Geo = SpassGeom<R>;
   constexpr int BOXW = Geo::BOXW;
-  constexpr int NSLOT = Geo::NSLOT;
-  constexpr int RING_ROWS = Geo::RING_ROWS;
-  constexpr int PRO = NSLOT - 1;  // x-blocks needed before the first y-block
+  constexpr int NSLOT = spass_nslot(R);
+  constexpr int RING_ROWS = NSLOT * kM;
+  constexpr int PRO = spass_pro(R);  // x-blocks written before y-block m = n - PRO runs
+  constexpr int OFF = spass_off(R);
   constexpr unsigned STAGE_BYTES = kM * BOXW * sizeof(float);
+  constexpr int NST = spass_stages(R);
 
   extern __shared__ __align__(128) unsigned char smem[];
   float* stage = reinterpret_cast<float*>(smem);
-  float* ring = stage + 2 * kM * BOXW;
+  float* ring = stage + NST * kM * BOXW;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * RING_ROWS * kRingStride);
   double* red = reinterpret_cast<double*>(bars + 2);
   int* flag = reinterpret_cast<int*>(red + 8);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int H = P.H, W = P.W, Wp = P.Wp, S = P.S, T = P.T;
+  const int H = P.H, W = P.W, Wp = P.Wp, S = P.S, T = P.T, NB = P.NB;
   const long u_begin = (long)blockIdx.x * P.U / P.G;
   const long u_end = (long)(blockIdx.x + 1) * P.U / P.G;
 
@@ -120,27 +140,35 @@ __global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_co
   }
   __syncthreads();
 
-  // ---- producer (thread 0): flat sequence of x-blocks over this CTA's segments
+  // ---- producer (thread 0): walks the same (segment, x-block) sequence as the
+  // consumers and issues a TMA load for every x-block that overlaps rows [0, H).
   long pu = u_begin;
   Seg pseg{};
-  int pn = 0, pnx = 0;
-  auto producer_issue = [&](int flat) {
-    if (pu >= u_end) return;
-    if (pn == 0) {
-      pseg = seg_decode(pu, u_end, H, S);
-      pnx = (pseg.yb - pseg.ya + 2 * R + kM - 1) / kM;
-    }
-    const int st = flat & 1;
-    mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
-    tma_load_3d(stage + st * kM * BOXW, &P.tmap, &bars[st], pseg.s * kTW - Geo::RA, pseg.ya - R + pn * kM, pseg.bt);
-    if (++pn == pnx) {
-      pn = 0;
-      pu += pseg.yb - pseg.ya;
+  int pn = 0, pnx = 0, pgs = 0;
+  unsigned pseq = 0;
+  auto producer_next = [&]() {
+    while (pu < u_end) {
+      if (pn == 0) {
+        pseg = seg_decode(pu, u_end, NB, S);
+        pnx = (pseg.yb1 - pseg.yb0) + PRO;
+        pgs = pseg.yb0 * kM - R - OFF;
+      }
+      const int row0 = pgs + pn * kM;
+      if (++pn == pnx) {
+        pn = 0;
+        pu += pseg.yb1 - pseg.yb0;
+      }
+      if (row0 + kM > 0 && row0 < H) {
+        const int st = (NST == 2) ? (pseq & 1) : 0;
+        ++pseq;
+        mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
+        tma_load_3d(stage + st * kM * BOXW, &P.tmap, &bars[st], pseg.s * kTW - Geo::RA, row0, pseg.bt);
+        return;
+      }
     }
   };
   if (tid == 0) {
-    producer_issue(0);
-    producer_issue(1);
+    for (int i = 0; i < NST; ++i) producer_next();
   }
 
   double acc0 = 0.0, acc1 = 0.0;  // per-thread partial sums of the current volume
@@ -155,16 +183,17 @@ __global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_co
     acc0 = acc1 = 0.0;
   };
 
-  // per-volume scalars for the backward epilogue (refreshed per segment)
+  // per-volume scalars for the backward epilogue (refreshed per volume)
   float cn = 0.f, inv_nu = 0.f, inv_nu_prev = 0.f;
 
-  int flat = 0;
+  unsigned cseq = 0;  // consumed TMA loads (stage / parity)
   long u = u_begin;
   while (u < u_end) {
-    const Seg sg = seg_decode(u, u_end, H, S);
-    const int L = sg.yb - sg.ya;
-    const int nxb = (L + 2 * R + kM - 1) / kM;
-    const int nyb = (L + kM - 1) / kM;
+    const Seg sg = seg_decode(u, u_end, NB, S);
+    const int nyb = sg.yb1 - sg.yb0;
+    const int nxb = nyb + PRO;
+    const int gs = sg.yb0 * kM - R - OFF;
+    const int yend = min(sg.yb1 * kM, H);
     const int vol = sg.bt / T;
     if (vol != cur_vol) {
       if (cur_vol >= 0) flush(cur_vol);
@@ -182,6 +211,7 @@ __global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_co
     const int rq = warp * 2 + (lane >> 4);
     const int x = sg.s * kTW + 4 * cq;
     const bool xok = x < W;
+    const bool xfull = x + 4 <= W;
     const float4 msk = make_float4(1.f, (x + 1 < W) ? 1.f : 0.f, (x + 2 < W) ? 1.f : 0.f, (x + 3 < W) ? 1.f : 0.f);
     struct Pre {
       float4 f[4], a[4], c[4];
@@ -190,9 +220,9 @@ __global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_co
     auto prefetch = [&](int m, Pre& pr) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int y = sg.ya + m * kM + 4 * rq + i;
+        const int y = (sg.yb0 + m) * kM + 4 * rq + i;
         pr.f[i] = pr.a[i] = pr.c[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (xok && y < sg.yb) {
+        if (xok && y < yend) {
           const long off = ((long)sg.bt * H + y) * Wp + x;
           pr.f[i] = *reinterpret_cast<const float4*>(P.F + off);
           if (MODE == SP_FWD) {
@@ -205,7 +235,7 @@ __global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_co
       }
     };
     auto ypass = [&](int m, const Pre& pr) {
-      const float* wb = ring + ((m % NSLOT) * kM + 4 * rq) * kRingStride + 4 * cq;
+      const float* wb = ring + ((m % NSLOT) * kM + OFF + 4 * rq) * kRingStride + 4 * cq;
       float4 a[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -216,7 +246,7 @@ __global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_co
         for (int i = 0; i < 4; ++i) {
           const int kk = j - i;
           if (kk >= 0 && kk <= 2 * R) {
-            const float gk = P.g[kk];
+            const float gk = P.g[kk < R ? R - kk : kk - R];
             a[i].x = fmaf(gk, q.x, a[i].x);
             a[i].y = fmaf(gk, q.y, a[i].y);
             a[i].z = fmaf(gk, q.z, a[i].z);
@@ -225,17 +255,22 @@ __global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_co
         }
       }
       if (!xok) return;
+      float s0 = 0.f, s1 = 0.f;  // this block's 16 outputs: fp32, then one fp64 add
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int y = sg.ya + m * kM + 4 * rq + i;
-        if (y >= sg.yb) break;
+        const int y = (sg.yb0 + m) * kM + 4 * rq + i;
+        if (y >= yend) break;
         const long off = ((long)sg.bt * H + y) * Wp + x;
-        const float4 f = f4_mul(pr.f[i], msk);
-        const float4 uu = f4_mul(a[i], msk);
+        float4 f = pr.f[i];
+        float4 uu = a[i];
+        if (!xfull) {
+          f = f4_mul(f, msk);
+          uu = f4_mul(uu, msk);
+        }
         if (MODE == SP_FWD) {
           const float4 yv = f4_mul(f, uu);
-          acc0 += (double)f4_dot(yv, yv);
-          if (P.pprev) acc1 += (double)f4_dot(pr.a[i], uu);
+          s0 += f4_dot(yv, yv);
+          if (P.pprev) s1 += f4_dot(pr.a[i], uu);
           if (P.tape_u) *reinterpret_cast<float4*>(P.tape_u + off) = uu;
           *reinterpret_cast<float4*>(P.out + off) = P.last ? yv : f4_mul(f, yv);
         } else {
@@ -258,67 +293,73 @@ __global__ void __launch_bounds__(kSpassThreads, 2) spass_kernel(const __grid_co
           *reinterpret_cast<float4*>(P.Fbar + off) = fb;
           const float4 xn = f4_mul(f, uu);
           *reinterpret_cast<float4*>(P.out + off) = xn;
-          acc0 += (double)f4_dot(xp, xn);
+          s0 += f4_dot(xp, xn);
         }
       }
+      acc0 += (double)s0;
+      acc1 += (double)s1;
     };
 
-    for (int n = 0; n < nxb; ++n, ++flat) {
-      const int st = flat & 1;
-      const bool do_y = (n >= PRO) && (n - PRO < nyb);
+    for (int n = 0; n < nxb; ++n) {
+      const bool do_y = n >= PRO;
       Pre pre;
       if (do_y) prefetch(n - PRO, pre);
-      mbar_wait(&bars[st], (flat >> 1) & 1);
-      // ------------------------------------------------------------ x-pass of block n
-      {
-        const float* srow = stage + st * kM * BOXW + lane * BOXW;
-        const int sl = n % NSLOT;
-        float* r0 = ring + (sl * kM + lane) * kRingStride;
-        float* r1 = r0 + RING_ROWS * kRingStride;
-#pragma unroll 1
-        for (int oi = 0; oi < kTW / 8 / kSpassWarps; ++oi) {
-          const int o = warp + kSpassWarps * oi;
-          float in[Geo::XIN];
+      const int row0 = gs + n * kM;
+      const bool live = (row0 + kM > 0) && (row0 < H);
+      const int sl = n % NSLOT;
+      float* r0 = ring + (sl * kM + lane) * kRingStride;
+      float* r1 = r0 + RING_ROWS * kRingStride;
+      if (live) {
+        const int st = (NST == 2) ? (cseq & 1) : 0;
+        mbar_wait(&bars[st], (NST == 2) ? ((cseq >> 1) & 1) : (cseq & 1));
+        // ------------------------------------------------------------ x-pass of block n
+        // thread: one row (lane) x 16 consecutive columns (warp)
+        const float* srow = stage + st * kM * BOXW + lane * BOXW + Geo::XO * warp;
+        float in[Geo::XIN];
 #pragma unroll
-          for (int i = 0; i < Geo::XIN / 4; ++i) {
-            const float4 v4 = *reinterpret_cast<const float4*>(srow + 8 * o + 4 * i);
-            in[4 * i + 0] = v4.x;
-            in[4 * i + 1] = v4.y;
-            in[4 * i + 2] = v4.z;
-            in[4 * i + 3] = v4.w;
-          }
-          float a[8];
+        for (int i = 0; i < Geo::XIN / 4; ++i) {
+          const float4 v4 = *reinterpret_cast<const float4*>(srow + 4 * i);
+          in[4 * i + 0] = v4.x;
+          in[4 * i + 1] = v4.y;
+          in[4 * i + 2] = v4.z;
+          in[4 * i + 3] = v4.w;
+        }
+        float a[Geo::XO];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) a[j] = 0.f;
+        for (int j = 0; j < Geo::XO; ++j) a[j] = 0.f;
 #pragma unroll
-          for (int kk = 0; kk <= 2 * R; ++kk) {
-            const float gk = P.g[kk];
+        for (int kk = 0; kk <= 2 * R; ++kk) {
+          const float gk = P.g[kk < R ? R - kk : kk - R];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = fmaf(gk, in[j + kk + Geo::D], a[j]);
-          }
-          const float4 lo = make_float4(a[0], a[1], a[2], a[3]);
-          const float4 hi = make_float4(a[4], a[5], a[6], a[7]);
-          *reinterpret_cast<float4*>(r0 + 8 * o) = lo;
-          *reinterpret_cast<float4*>(r0 + 8 * o + 4) = hi;
-          *reinterpret_cast<float4*>(r1 + 8 * o) = lo;
-          *reinterpret_cast<float4*>(r1 + 8 * o + 4) = hi;
+          for (int j = 0; j < Geo::XO; ++j) a[j] = fmaf(gk, in[j + kk + Geo::D], a[j]);
+        }
+#pragma unroll
+        for (int q = 0; q < Geo::XO / 4; ++q) {
+          const float4 v = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+          *reinterpret_cast<float4*>(r0 + Geo::XO * warp + 4 * q) = v;
+          *reinterpret_cast<float4*>(r1 + Geo::XO * warp + 4 * q) = v;
+        }
+      } else {
+        // block entirely in the zero padding above row 0 or below row H-1
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < Geo::XO / 4; ++q) {
+          *reinterpret_cast<float4*>(r0 + Geo::XO * warp + 4 * q) = z;
+          *reinterpret_cast<float4*>(r1 + Geo::XO * warp + 4 * q) = z;
         }
       }
-      __syncthreads();  // stage st consumed; ring slot visible
-      if (tid == 0) {
-        fence_proxy_async();
-        producer_issue(flat + 2);
+      __syncthreads();  // stage consumed; ring slot visible
+      if (live) {
+        ++cseq;
+        if (tid == 0) {
+          fence_proxy_async();
+          producer_next();
+        }
       }
       if (do_y) ypass(n - PRO, pre);
       __syncthreads();  // ring slot (n+1) % NSLOT may be overwritten next
     }
-    for (int m = max(0, nxb - PRO); m < nyb; ++m) {
-      Pre pre;
-      prefetch(m, pre);
-      ypass(m, pre);
-    }
-    __syncthreads();
-    u += L;
+    u += nyb;
   }
   if (cur_vol >= 0) flush(cur_vol);
 

@@ -32,7 +32,7 @@ struct TpassParams {
   float g[2 * kMaxRT + 1];  // g[i] = weight of temporal offset i - RT
 };
 
-template <int RT, int MODE>
+template <int RT, int MODE, bool HALO>
 __global__ void __launch_bounds__(256) tpass_kernel(const __grid_constant__ TpassParams P) {
   constexpr int NR = 2 * RT + 1;
   const int b = blockIdx.y;
@@ -61,30 +61,41 @@ __global__ void __launch_bounds__(256) tpass_kernel(const __grid_constant__ Tpas
   for (int i = 0; i < NR; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 
   // jp = j + RT enumerates input frames j = -RT .. T+RT-1; output t = jp - 2RT
-  // completes when input j = t + RT arrives.
+  // completes when input j = t + RT arrives.  Inputs are software-pipelined NR
+  // frames ahead (register queue q[]) so NR loads per thread are in flight.
+  auto load = [&](int jp) -> float4 {
+    const int j = jp - RT;
+    const int jc = min(max(j, 0), T - 1);  // clamped: always a valid address
+    float4 val;
+    if (MODE == TP_FWD) {
+      val = __ldcs(src + (long)jc * P.frame4);
+    } else {
+      const long o = (long)jc * P.frame4;
+      const float4 xb = src[o], f = Fp[o], u = U1[o];
+      val.x = f.x * ((xb.x - f.x * u.x * cn) * inv_nu);
+      val.y = f.y * ((xb.y - f.y * u.y * cn) * inv_nu);
+      val.z = f.z * ((xb.z - f.z * u.z * cn) * inv_nu);
+      val.w = f.w * ((xb.w - f.w * u.w * cn) * inv_nu);
+    }
+    if (HALO) {
+      // neighbour slab frames (time-slab sharding); absent halos read as zero
+      if (j < 0) val = (hlo != nullptr && j >= -RT) ? hlo[(long)(j + RT) * P.frame4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j >= T) val = (hhi != nullptr && j < T + RT) ? hhi[(long)(j - T) * P.frame4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (j < 0 || j >= T) {
+      val = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return val;
+  };
   const int jend = T + 2 * RT;
+  float4 q[NR];
+#pragma unroll
+  for (int d = 0; d < NR; ++d) q[d] = load(d);
   for (int j0 = 0; j0 < jend; j0 += NR) {
 #pragma unroll
     for (int d = 0; d < NR; ++d) {
       const int jp = j0 + d;
-      const int j = jp - RT;
-      float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j >= 0 && j < T) {
-        if (MODE == TP_FWD) {
-          val = __ldcs(src + (long)j * P.frame4);
-        } else {
-          const long o = (long)j * P.frame4;
-          const float4 xb = src[o], f = Fp[o], u = U1[o];
-          val.x = f.x * ((xb.x - f.x * u.x * cn) * inv_nu);
-          val.y = f.y * ((xb.y - f.y * u.y * cn) * inv_nu);
-          val.z = f.z * ((xb.z - f.z * u.z * cn) * inv_nu);
-          val.w = f.w * ((xb.w - f.w * u.w * cn) * inv_nu);
-        }
-      } else if (j < 0 && hlo != nullptr && j >= -RT) {
-        val = hlo[(long)(j + RT) * P.frame4];
-      } else if (j >= T && hhi != nullptr && j < T + RT) {
-        val = hhi[(long)(j - T) * P.frame4];
-      }
+      const float4 val = q[d];
+      q[d] = load(jp + NR);  // prefetch (harmless past the end: clamped and zeroed)
 #pragma unroll
       for (int ee = 0; ee < NR; ++ee) {
         // input j feeds output t = j - RT + ee with weight g[(j - t) + RT] = g[2RT - ee]
