@@ -170,11 +170,35 @@ sfseg_status sfseg_profile_enable(int32_t on);
 sfseg_status sfseg_profile_read(double* ms_host /*[4]*/, int64_t* count_host /*[4]*/);
 
 /* ---- multi-GPU communicator (NCCL, loaded at run time with dlopen) ---- */
-/* 128-byte NCCL unique id into id_host (call on rank 0, broadcast it). */
+/* Multi-GPU solve: call sfseg_power_iterate with dist_or_null = {comm, T_global,
+ * t_offset} on every rank (one process per GPU, ranks own consecutive slabs
+ * in rank order, each slab >= the compiled temporal radius); ch / x0 / x_out
+ * are the rank's LOCAL slab [B][C][T_local][H][W] / [B][T_local][H][W].
+ * Workspace from sfseg_workspace_bytes(..., dist, ...).  Every iteration:
+ * r_t-frame halo send/recv with ranks +-1 and an fp64 allreduce of the norm
+ * partials (NCCL, enqueued on `stream`).  Tape / F_out: SFSEG_ERR_UNSUPPORTED.
+ * 128-byte NCCL unique id into id_host (call on rank 0, broadcast it). */
 sfseg_status sfseg_get_unique_id(uint8_t id_host[128]);
 sfseg_status sfseg_comm_create(const uint8_t id_host[128], int32_t nranks, int32_t rank,
                                int32_t device, sfseg_comm** out);
 sfseg_status sfseg_comm_destroy(sfseg_comm* comm);
+
+/* ---- time-slab decomposition emulated on ONE GPU (validation of the sharded path) ----
+ * Splits every volume's T frames into nslabs consecutive slabs (slab i covers
+ * frames [i*T/n, (i+1)*T/n)) and runs the exact per-rank phases of the
+ * multi-GPU solve for all slabs on `stream`: halo frames are
+ * copied device-to-device and the norm partials summed in rank order.  Same
+ * arguments/outputs as sfseg_power_iterate on the full dense volume (no tape). */
+sfseg_status sfseg_slabs_workspace_bytes(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K,
+                                         int32_t nslabs, size_t* ws_bytes_host);
+sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* w_host, float b,
+                                       int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
+                                       int32_t nslabs, const float* x0_or_null, float* x_out,
+                                       double* stats_or_null, int32_t want_rayleigh, void* ws,
+                                       size_t ws_bytes, void* stream);
+/* Syncs `stream`; returns the first device-detected error of any slab. */
+sfseg_status sfseg_slabs_sync_status(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K,
+                                     int32_t nslabs, void* ws, void* stream);
 
 #ifdef __cplusplus
 }

@@ -88,6 +88,10 @@ _SIGS = {
                                    C.c_float, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "sfseg_profile_enable": (C.c_int, [C.c_int32]),
     "sfseg_profile_read": (C.c_int, [_P, _P]),
+    "sfseg_slabs_workspace_bytes": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
+    "sfseg_power_iterate_slabs": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
+                                            C.c_int32, _P, _P, _P, C.c_int32, _P, C.c_size_t, _P]),
+    "sfseg_slabs_sync_status": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P, _P]),
     "sfseg_get_unique_id": (C.c_int, [_P]),
     "sfseg_comm_create": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P]),
     "sfseg_comm_destroy": (C.c_int, [_P]),
@@ -264,6 +268,29 @@ def power_iterate_backward(ch, w, gauss: Gauss, K: int, dL_dx, b: float = 0.0, a
     x = s.forward(ch, w, b, act, x0=x0)
     dw, db = s.backward(ch, w, dL_dx, b, act, x0=x0)
     return x, dw, db
+
+
+def power_iterate_slabs(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, b: float = 0.0,
+                        act: int = ACT_IDENTITY, x0=None, want_rayleigh: bool = False, stream=None):
+    """Time-slab decomposition of the solve emulated on ONE GPU (sfseg_power_iterate_slabs):
+    the per-rank phases of the multi-GPU path with in-process halo copies and reduction."""
+    _require(ch, "ch", 5)
+    B, Cn, T, H, W = ch.shape
+    shp, g = Shape(B, T, H, W), gauss.c()
+    n = C.c_size_t(0)
+    _check(lib().sfseg_slabs_workspace_bytes(shp, Cn, g, int(K), int(nslabs), C.byref(n)),
+           "sfseg_slabs_workspace_bytes")
+    ws = _alloc_bytes(n.value, ch.device)
+    x = torch.empty((B, T, H, W), dtype=torch.float32, device=ch.device)
+    stats = torch.zeros((B, int(K), 3), dtype=torch.float64, device=ch.device)
+    if x0 is not None:
+        _require(x0, "x0", 4)
+    _check(lib().sfseg_power_iterate_slabs(_ptr(ch), Cn, _weights(w, Cn), float(b), int(act), shp, g, int(K),
+                                           int(nslabs), _ptr(x0), _ptr(x), _ptr(stats), int(want_rayleigh),
+                                           _ptr(ws), n.value, _stream(stream)), "sfseg_power_iterate_slabs")
+    _check(lib().sfseg_slabs_sync_status(shp, Cn, g, int(K), int(nslabs), _ptr(ws), _stream(stream)),
+           "sfseg_power_iterate_slabs (device)")
+    return x, stats
 
 
 def threshold(x: torch.Tensor, tau: float, mode: int = THR_PER_FRAME_MAX) -> torch.Tensor:

@@ -5,6 +5,7 @@
 // fp64 finalize in the last block (deterministic).
 #pragma once
 #include "common.cuh"
+#include "spass.cuh"
 
 namespace sfseg {
 
@@ -22,7 +23,9 @@ struct CombineParams {
   double* partials;     // [B][T*gx]
   unsigned* counter;
   unsigned* err;
+  double* loc;          // time-slab mode: per-volume local sum of x_0^2 -> loc[2b]
   int B, C, T, H, W, Wp, act, gx;
+  int in_T, in_t0;      // ch / x0 buffers hold in_T frames; this call's frame t is buffer frame in_t0 + t
   float bias;
   float w[kMaxC];
 };
@@ -33,14 +36,14 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
   const int bt = blockIdx.y;
   const int b = bt / P.T, t = bt - b * P.T;
   const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
-  const long vol_dense = (long)P.T * HW;
+  const long vol_dense = (long)P.in_T * HW;
   double acc = 0.0;
   for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HWp; e += (long)P.gx * kEwThreads) {
     const int y = (int)(e / P.Wp), x = (int)(e - (long)y * P.Wp);
     const long po = (long)bt * HWp + e;
     float f = 0.f, pv = 0.f, xv = 0.f;
     if (x < P.W) {
-      const long d = (long)t * HW + (long)y * P.W + x;
+      const long d = (long)(P.in_t0 + t) * HW + (long)y * P.W + x;
       const float* chb = P.ch + (long)b * P.C * vol_dense + d;
       float z = P.bias;
       for (int c = 0; c < P.C; ++c) z = fmaf(P.w[c], __ldg(chb + (long)c * vol_dense), z);
@@ -62,24 +65,72 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
   for (int bb = 0; bb < P.B; ++bb) {
     const double tot = block_sum_array<kEwThreads>(P.partials + (long)bb * nper, nper, 1, red);
     if (threadIdx.x == 0) {
-      const double xn = sqrt(tot);
-      P.sc[bb * kScal + SC_XNORM] = xn;
-      P.sc[bb * kScal + SC_S] = 1.0;
-      flag_norm(P.err, xn);
+      if (P.loc) {
+        P.loc[2 * bb] = tot;
+        P.loc[2 * bb + 1] = 0.0;
+      } else {
+        const double xn = sqrt(tot);
+        P.sc[bb * kScal + SC_XNORM] = xn;
+        P.sc[bb * kScal + SC_S] = 1.0;
+        flag_norm(P.err, xn);
+      }
     }
   }
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
+// ------------------------------------------------------------------ time-slab finalizers (after the allreduce)
+struct FinParams {
+  const double* glob;   // [B][2] global sums
+  double* sc;
+  double* stats;
+  double* tape_nu;
+  unsigned* err;
+  int B, K, k, rayleigh;
+};
+
+// k == 0: combine (||x_0||); k >= 1: forward iteration k.
+__global__ void finalize_kernel(const __grid_constant__ FinParams P) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B) return;
+  double* sc = P.sc + b * kScal;
+  if (P.k == 0) {
+    const double xn = sqrt(P.glob[2 * b]);
+    sc[SC_XNORM] = xn;
+    sc[SC_S] = 1.0;
+    flag_norm(P.err, xn);
+  } else {
+    fwd_finalize(sc, P.stats, P.tape_nu, P.err, P.K, P.k, P.rayleigh != 0, b, P.glob[2 * b], P.glob[2 * b + 1]);
+  }
+}
+
+// In-process "allreduce" for emulated ranks on one GPU: glob_r = sum over ranks (rank order) of loc_r.
+constexpr int kMaxLocalRanks = 16;
+struct LocalReduceParams {
+  const double* loc[kMaxLocalRanks];
+  double* glob[kMaxLocalRanks];
+  int nranks, n;
+};
+__global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams P) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  double s = 0.0;
+  for (int r = 0; r < P.nranks; ++r) s += P.loc[r][i];
+  for (int r = 0; r < P.nranks; ++r) P.glob[r][i] = s;
+}
+
 // ------------------------------------------------------------------ final normalisation x_K = y_K / nu_K
+// x (dense, buffer of out_T frames per volume; this slab starts at frame out_t0)
 __global__ void __launch_bounds__(kEwThreads) final_scale_kernel(const float* __restrict__ y, float* __restrict__ x,
-                                                                 const double* sc, int T, int H, int W, int Wp) {
-  const int bt = blockIdx.y, b = bt / T;
+                                                                 const double* sc, int T, int H, int W, int Wp,
+                                                                 int out_T, int out_t0) {
+  const int bt = blockIdx.y, b = bt / T, t = bt - b * T;
   const float s = (float)sc[b * kScal + SC_S];
   const long HW = (long)H * W;
+  float* xo = x + ((long)b * out_T + out_t0 + t) * HW;
   for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HW; e += (long)gridDim.x * kEwThreads) {
     const int yy = (int)(e / W), xx = (int)(e - (long)yy * W);
-    x[(long)bt * HW + e] = __ldcs(y + ((long)bt * H + yy) * Wp + xx) * s;
+    xo[e] = __ldcs(y + ((long)bt * H + yy) * Wp + xx) * s;
   }
 }
 

@@ -306,6 +306,8 @@ void fill_combine(CombineParams& cp, const Plan& P, const float* ch, const float
   cp.Wp = (int)P.Wp;
   cp.act = act;
   cp.gx = P.gx;
+  cp.in_T = (int)P.T;
+  cp.in_t0 = 0;
   cp.bias = b;
   for (int c = 0; c < P.C; ++c) cp.w[c] = w_host[c];
 }
@@ -345,14 +347,240 @@ bool finite_weights(const float* w, int C, float b) {
   return true;
 }
 
-// Time-slab sharded solve; filled in by the multi-GPU milestone.
+// ====================================================================== time-slab sharding
+// (SURVEY.md §8(e)).  Each rank owns T_r consecutive frames of every volume.
+// Per iteration only the temporal pass reads neighbour frames: the r_t
+// boundary frames of the iterate p are exchanged with ranks +-1 after every
+// spatial pass, and the per-volume norm partials are summed across ranks
+// (fp64) before the scalar finalize.  The same phase functions drive both the
+// NCCL transport (one rank per GPU) and an in-process emulation of n ranks on
+// one GPU (halo copies + a rank-ordered reduction kernel) used to test the
+// decomposition on a single device.
+struct SlabOffsets {
+  size_t off_hlo, off_hhi, off_loc, off_glob, total;
+};
+SlabOffsets slab_offsets(const Plan& P) {
+  SlabOffsets o;
+  size_t off = P.ws_fwd;
+  const size_t hb = align_up(sizeof(float) * (size_t)P.B * P.RT * P.H * P.Wp);
+  o.off_hlo = off;
+  off += hb;
+  o.off_hhi = off;
+  off += hb;
+  const size_t lb = align_up(sizeof(double) * 2 * P.B);
+  o.off_loc = off;
+  off += lb;
+  o.off_glob = off;
+  off += lb;
+  o.total = off;
+  return o;
+}
+
+struct Rank {
+  Plan P;
+  const float* ch = nullptr;
+  const float* x0 = nullptr;
+  int in_T = 0, in_t0 = 0;  // channel / x0 buffer frames and this slab's first frame in it
+  float* x_out = nullptr;
+  int out_T = 0, out_t0 = 0;
+  double* stats = nullptr;
+  int rayleigh = 0;
+  void* ws = nullptr;
+  SlabOffsets so;
+  bool has_lo = false, has_hi = false;
+  float *F = nullptr, *p = nullptr, *v = nullptr, *hlo = nullptr, *hhi = nullptr;
+  double *loc = nullptr, *glob = nullptr;
+  SpassParams sp;
+  TpassParams tp;
+};
+
+sfseg_status rank_setup(Rank& r, cudaStream_t st) {
+  const Plan& P = r.P;
+  r.so = slab_offsets(P);
+  r.F = at<float>(r.ws, P.off_F);
+  r.p = at<float>(r.ws, P.off_p);
+  r.v = at<float>(r.ws, P.off_v);
+  r.hlo = at<float>(r.ws, r.so.off_hlo);
+  r.hhi = at<float>(r.ws, r.so.off_hhi);
+  r.loc = at<double>(r.ws, r.so.off_loc);
+  r.glob = at<double>(r.ws, r.so.off_glob);
+  SF_CUDA(cudaMemsetAsync(r.ws, 0, P.off_part, st));
+  std::memset(&r.sp, 0, sizeof(r.sp));
+  if (!make_volume_tmap(&r.sp.tmap, r.v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+  fill_spass_common(r.sp, P, r.ws);
+  r.sp.stats = r.stats;
+  r.sp.loc = r.loc;
+  std::memset(&r.tp, 0, sizeof(r.tp));
+  fill_tpass_common(r.tp, P, r.ws);
+  r.tp.src = r.p;
+  r.tp.out = r.v;
+  r.tp.halo_lo = r.has_lo ? r.hlo : nullptr;
+  r.tp.halo_hi = r.has_hi ? r.hhi : nullptr;
+  return SFSEG_OK;
+}
+
+sfseg_status ph_combine(Rank& r, const float* w_host, float b, int act, cudaStream_t st) {
+  CombineParams cp;
+  fill_combine(cp, r.P, r.ch, w_host, b, act, r.ws);
+  cp.x0 = r.x0;
+  cp.F = r.F;
+  cp.p0 = r.p;
+  cp.loc = r.loc;
+  cp.in_T = r.in_T;
+  cp.in_t0 = r.in_t0;
+  combine_kernel<<<dim3(r.P.gx, (unsigned)r.P.BT), kEwThreads, 0, st>>>(cp);
+  SF_CUDA(after_launch("combine(slab)", st));
+  return SFSEG_OK;
+}
+
+sfseg_status ph_finalize(Rank& r, int k, cudaStream_t st) {
+  FinParams fp;
+  fp.glob = r.glob;
+  fp.sc = at<double>(r.ws, r.P.off_sc);
+  fp.stats = r.stats;
+  fp.tape_nu = nullptr;
+  fp.err = &at<WsHeader>(r.ws, 0)->err;
+  fp.B = (int)r.P.B;
+  fp.K = r.P.K;
+  fp.k = k;
+  fp.rayleigh = r.rayleigh;
+  finalize_kernel<<<(unsigned)((r.P.B + 127) / 128), 128, 0, st>>>(fp);
+  SF_CUDA(after_launch("finalize(slab)", st));
+  return SFSEG_OK;
+}
+
+sfseg_status ph_T(Rank& r, cudaStream_t st) {
+  ProfScope ps(st, PC_TPASS);
+  SF_CUDA(launch_tpass_fwd(r.P.RT, r.tp, (int)r.P.B, st));
+  SF_CUDA(after_launch("tpass(slab)", st));
+  return SFSEG_OK;
+}
+
+sfseg_status ph_S(Rank& r, int k, cudaStream_t st) {
+  r.sp.out = r.p;
+  r.sp.pprev = r.rayleigh ? r.p : nullptr;
+  r.sp.k = k;
+  r.sp.last = (k == r.P.K) ? 1 : 0;
+  ProfScope ps(st, PC_SPASS);
+  SF_CUDA(launch_spass_fwd(r.P.RS, r.sp, r.P.G, st));
+  SF_CUDA(after_launch("spass(slab)", st));
+  return SFSEG_OK;
+}
+
+sfseg_status ph_final(Rank& r, cudaStream_t st) {
+  const Plan& P = r.P;
+  const int64_t per = (P.H * P.W + 1023) / 1024;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(per, 64)), (unsigned)P.BT);
+  final_scale_kernel<<<grid, kEwThreads, 0, st>>>(r.p, r.x_out, at<double>(r.ws, P.off_sc), (int)P.T, (int)P.H,
+                                                  (int)P.W, (int)P.Wp, r.out_T, r.out_t0);
+  SF_CUDA(after_launch("final_scale(slab)", st));
+  return SFSEG_OK;
+}
+
+sfseg_status nccl_exchange(Rank& r, sfseg_comm* c, cudaStream_t st) {
+  NcclApi& api = nccl();
+  const Plan& P = r.P;
+  const size_t fr = (size_t)P.H * P.Wp, n = (size_t)P.RT * fr;
+  if (n == 0) return SFSEG_OK;
+  if (api.GroupStart() != ncclSuccess) return SFSEG_ERR_NCCL;
+  for (int64_t b = 0; b < P.B; ++b) {
+    float* base = r.p + (size_t)b * P.T * fr;
+    if (r.has_lo) {
+      if (api.Send(base, n, ncclFloat32, c->rank - 1, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
+      if (api.Recv(r.hlo + b * n, n, ncclFloat32, c->rank - 1, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
+    }
+    if (r.has_hi) {
+      if (api.Send(base + (P.T - P.RT) * fr, n, ncclFloat32, c->rank + 1, c->comm, st) != ncclSuccess)
+        return SFSEG_ERR_NCCL;
+      if (api.Recv(r.hhi + b * n, n, ncclFloat32, c->rank + 1, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
+    }
+  }
+  if (api.GroupEnd() != ncclSuccess) return SFSEG_ERR_NCCL;
+  return SFSEG_OK;
+}
+
+sfseg_status nccl_allreduce(Rank& r, sfseg_comm* c, cudaStream_t st) {
+  if (nccl().AllReduce(r.loc, r.glob, 2 * (size_t)r.P.B, ncclFloat64, ncclSum, c->comm, st) != ncclSuccess)
+    return SFSEG_ERR_NCCL;
+  return SFSEG_OK;
+}
+
+sfseg_status local_exchange(std::vector<Rank>& R, cudaStream_t st) {
+  const int n = (int)R.size();
+  for (int i = 0; i < n; ++i) {
+    const Plan& P = R[i].P;
+    const size_t fr = (size_t)P.H * P.Wp, cnt = (size_t)P.RT * fr;
+    for (int64_t b = 0; b < P.B; ++b) {
+      if (R[i].has_lo) {
+        const Plan& Q = R[i - 1].P;
+        SF_CUDA(cudaMemcpyAsync(R[i].hlo + b * cnt, R[i - 1].p + ((size_t)b * Q.T + (Q.T - Q.RT)) * fr,
+                                cnt * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      }
+      if (R[i].has_hi) {
+        const Plan& Q = R[i + 1].P;
+        SF_CUDA(cudaMemcpyAsync(R[i].hhi + b * cnt, R[i + 1].p + (size_t)b * Q.T * fr, cnt * sizeof(float),
+                                cudaMemcpyDeviceToDevice, st));
+      }
+    }
+  }
+  return SFSEG_OK;
+}
+
+sfseg_status local_allreduce(std::vector<Rank>& R, cudaStream_t st) {
+  LocalReduceParams lp;
+  std::memset(&lp, 0, sizeof(lp));
+  lp.nranks = (int)R.size();
+  lp.n = 2 * (int)R[0].P.B;
+  for (int i = 0; i < lp.nranks; ++i) {
+    lp.loc[i] = R[i].loc;
+    lp.glob[i] = R[i].glob;
+  }
+  local_allreduce_kernel<<<(unsigned)((lp.n + 127) / 128), 128, 0, st>>>(lp);
+  SF_CUDA(after_launch("local_allreduce", st));
+  return SFSEG_OK;
+}
+
+// One rank of an NCCL-connected time-slab solve.
 sfseg_status dist_power_iterate(const Plan& P, const float* ch, const float* w_host, float b, int act,
                                 const float* x0, float* x_out, float* F_out, double* stats, int want_rayleigh,
                                 void* tape, void* ws, size_t ws_bytes, const sfseg_dist* dist, void* stream) {
-  (void)P; (void)ch; (void)w_host; (void)b; (void)act; (void)x0; (void)x_out; (void)F_out; (void)stats;
-  (void)want_rayleigh; (void)tape; (void)ws; (void)ws_bytes; (void)dist; (void)stream;
-  return SFSEG_ERR_UNSUPPORTED;
+  if (!dist->comm || !dist->comm->comm) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (tape || F_out) return SFSEG_ERR_UNSUPPORTED;  // backward / F export are single-GPU only for now
+  sfseg_comm* c = dist->comm;
+  if (dist->t_offset < 0 || dist->t_offset + P.T > dist->T_global) return SFSEG_ERR_SHAPE;
+  if (c->nranks > 1 && P.T < P.RT) return SFSEG_ERR_SHAPE;  // halo must come from one neighbour
+  Rank r;
+  r.P = P;
+  r.ch = ch;
+  r.x0 = x0;
+  r.in_T = (int)P.T;
+  r.x_out = x_out;
+  r.out_T = (int)P.T;
+  r.stats = stats;
+  r.rayleigh = want_rayleigh;
+  r.ws = ws;
+  r.has_lo = dist->t_offset > 0 && c->rank > 0;
+  r.has_hi = dist->t_offset + P.T < dist->T_global && c->rank < c->nranks - 1;
+  sfseg_status s = check_ws(ws, ws_bytes, slab_offsets(P).total);
+  if (s != SFSEG_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((s = rank_setup(r, st)) != SFSEG_OK) return s;
+  if ((s = ph_combine(r, w_host, b, act, st)) != SFSEG_OK) return s;
+  if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) return s;
+  if ((s = ph_finalize(r, 0, st)) != SFSEG_OK) return s;
+  if ((s = nccl_exchange(r, c, st)) != SFSEG_OK) return s;
+  for (int k = 1; k <= P.K; ++k) {
+    if ((s = ph_T(r, st)) != SFSEG_OK) return s;
+    if ((s = ph_S(r, k, st)) != SFSEG_OK) return s;
+    if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) return s;
+    if ((s = ph_finalize(r, k, st)) != SFSEG_OK) return s;
+    if (k < P.K && (s = nccl_exchange(r, c, st)) != SFSEG_OK) return s;
+  }
+  return ph_final(r, st);
 }
+
+// Slab boundaries: slab i of n covers frames [i*T/n, (i+1)*T/n) (uneven when n does not divide T).
+inline int64_t slab_start(int64_t T, int n, int i) { return (T * i) / n; }
 
 }  // namespace
 
@@ -389,8 +617,7 @@ sfseg_status sfseg_workspace_bytes(sfseg_shape shape, int32_t C, sfseg_gauss gau
   Plan P;
   sfseg_status st = make_plan(shape, C, gauss, K, &P);
   if (st != SFSEG_OK) return st;
-  size_t extra = dist ? sfseg::comm_ws_bytes(P.B, P.RT, P.H, P.Wp) : 0;
-  *ws_bytes = (want_tape ? P.ws_bwd : P.ws_fwd) + extra;
+  *ws_bytes = dist ? slab_offsets(P).total : (want_tape ? P.ws_bwd : P.ws_fwd);
   if (tape_bytes) *tape_bytes = want_tape ? P.tape_bytes : 0;
   return SFSEG_OK;
 }
@@ -413,6 +640,8 @@ sfseg_status sfseg_combine_channels(const float* ch, int32_t C, sfseg_shape sh, 
   cp.W = (int)sh.W;
   cp.Wp = (int)sh.W;
   cp.act = act;
+  cp.in_T = (int)sh.T;
+  cp.in_t0 = 0;
   cp.bias = b;
   for (int c = 0; c < C; ++c) cp.w[c] = w_host[c];
   const int64_t per_frame = (sh.H * sh.W + 1023) / 1024;
@@ -496,7 +725,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     const int64_t per = (P.H * P.W + 1023) / 1024;
     dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(per, 64)), (unsigned)P.BT);
     final_scale_kernel<<<grid, kEwThreads, 0, st>>>(p, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H, (int)P.W,
-                                                    (int)P.Wp);
+                                                    (int)P.Wp, (int)P.T, 0);
     SF_CUDA(after_launch("final_scale", st));
   }
   return SFSEG_OK;
@@ -754,6 +983,100 @@ sfseg_status sfseg_profile_read(double* ms_host, int64_t* count_host) {
   }
   p.recs.clear();
   return s;
+}
+
+// n emulated ranks on one GPU (single stream): the time-slab decomposition with
+// in-process halo copies and a rank-ordered reduction (test / validation path).
+sfseg_status sfseg_slabs_workspace_bytes(sfseg_shape sh, int32_t C, sfseg_gauss gauss, int32_t K, int32_t nslabs,
+                                         size_t* ws_bytes_host) {
+  if (!ws_bytes_host || nslabs < 1 || nslabs > kMaxLocalRanks) return SFSEG_ERR_INVALID_ARGUMENT;
+  size_t tot = 0;
+  for (int i = 0; i < nslabs; ++i) {
+    sfseg_shape ls = sh;
+    ls.T = slab_start(sh.T, nslabs, i + 1) - slab_start(sh.T, nslabs, i);
+    Plan P;
+    sfseg_status s = make_plan(ls, C, gauss, K, &P);
+    if (s != SFSEG_OK) return s;
+    tot += align_up(slab_offsets(P).total);
+  }
+  *ws_bytes_host = tot;
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
+                                       sfseg_shape sh, sfseg_gauss gauss, int32_t K, int32_t nslabs,
+                                       const float* x0, float* x_out, double* stats, int32_t want_rayleigh,
+                                       void* ws, size_t ws_bytes, void* stream) {
+  if (!ch || !w_host || !x_out || !validate_act(act) || nslabs < 1 || nslabs > kMaxLocalRanks)
+    return SFSEG_ERR_INVALID_ARGUMENT;
+  if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
+  size_t need = 0;
+  sfseg_status s = sfseg_slabs_workspace_bytes(sh, C, gauss, K, nslabs, &need);
+  if (s != SFSEG_OK) return s;
+  if ((s = check_ws(ws, ws_bytes, need)) != SFSEG_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<Rank> R(nslabs);
+  size_t off = 0;
+  for (int i = 0; i < nslabs; ++i) {
+    const int64_t t0 = slab_start(sh.T, nslabs, i), t1 = slab_start(sh.T, nslabs, i + 1);
+    sfseg_shape ls = sh;
+    ls.T = t1 - t0;
+    if ((s = make_plan(ls, C, gauss, K, &R[i].P)) != SFSEG_OK) return s;
+    if (nslabs > 1 && R[i].P.T < R[i].P.RT) return SFSEG_ERR_SHAPE;
+    R[i].ch = ch;
+    R[i].x0 = x0;
+    R[i].in_T = (int)sh.T;
+    R[i].in_t0 = (int)t0;
+    R[i].x_out = x_out;
+    R[i].out_T = (int)sh.T;
+    R[i].out_t0 = (int)t0;
+    R[i].stats = stats;
+    R[i].rayleigh = want_rayleigh;
+    R[i].ws = static_cast<char*>(ws) + off;
+    R[i].has_lo = i > 0;
+    R[i].has_hi = i < nslabs - 1;
+    off += align_up(slab_offsets(R[i].P).total);
+  }
+  for (auto& r : R)
+    if ((s = rank_setup(r, st)) != SFSEG_OK) return s;
+  for (auto& r : R)
+    if ((s = ph_combine(r, w_host, b, act, st)) != SFSEG_OK) return s;
+  if ((s = local_allreduce(R, st)) != SFSEG_OK) return s;
+  for (auto& r : R)
+    if ((s = ph_finalize(r, 0, st)) != SFSEG_OK) return s;
+  if ((s = local_exchange(R, st)) != SFSEG_OK) return s;
+  for (int k = 1; k <= K; ++k) {
+    for (auto& r : R)
+      if ((s = ph_T(r, st)) != SFSEG_OK) return s;
+    for (auto& r : R)
+      if ((s = ph_S(r, k, st)) != SFSEG_OK) return s;
+    if ((s = local_allreduce(R, st)) != SFSEG_OK) return s;
+    for (auto& r : R)
+      if ((s = ph_finalize(r, k, st)) != SFSEG_OK) return s;
+    if (k < K && (s = local_exchange(R, st)) != SFSEG_OK) return s;
+  }
+  for (auto& r : R)
+    if ((s = ph_final(r, st)) != SFSEG_OK) return s;
+  return SFSEG_OK;
+}
+
+// Device error word of slab i inside a sfseg_power_iterate_slabs workspace.
+sfseg_status sfseg_slabs_sync_status(sfseg_shape sh, int32_t C, sfseg_gauss gauss, int32_t K, int32_t nslabs,
+                                     void* ws, void* stream) {
+  if (!ws || nslabs < 1 || nslabs > kMaxLocalRanks) return SFSEG_ERR_INVALID_ARGUMENT;
+  size_t off = 0;
+  sfseg_status worst = SFSEG_OK;
+  for (int i = 0; i < nslabs; ++i) {
+    sfseg_shape ls = sh;
+    ls.T = slab_start(sh.T, nslabs, i + 1) - slab_start(sh.T, nslabs, i);
+    Plan P;
+    sfseg_status s = make_plan(ls, C, gauss, K, &P);
+    if (s != SFSEG_OK) return s;
+    s = sfseg_sync_status(static_cast<char*>(ws) + off, stream);
+    if (s != SFSEG_OK && worst == SFSEG_OK) worst = s;
+    off += align_up(slab_offsets(P).total);
+  }
+  return worst;
 }
 
 }  // extern "C"

@@ -75,6 +75,7 @@ struct SpassParams {
   unsigned* counter;
   unsigned* err;
   double* stats;           // FWD: [B][K][3] (nullable)
+  double* loc;             // time-slab mode: per-volume local sums [B][2] (finalize after the allreduce)
   double* tape_nu;         // FWD writes nu_k; BWD reads nu
   long U;                  // total block units = B*T*S*NB (NB = ceil(H/32))
   int B, T, H, W, Wp, S, NB, G;
@@ -82,6 +83,35 @@ struct SpassParams {
   int last;                // FWD: write y instead of p
   float g[kMaxRS + 1];     // g[d] = weight of spatial offset +-d (same taps for y and x)
 };
+
+// Per-volume finalize of forward iteration k from the global sums s0 = ||y_k||^2 and
+// s1 = <p_{k-1}, u_k> (used in-kernel on one GPU, by finalize_kernel after an allreduce).
+__device__ __forceinline__ void fwd_finalize(double* sc, double* stats, double* tape_nu, unsigned* err, int K, int k,
+                                             bool rayleigh, int b, double s0, double s1) {
+  const double nu = sqrt(s0);
+  const double xn = sc[SC_XNORM];
+  if (stats) {
+    double* st = stats + ((long)b * K + (k - 1)) * 3;
+    st[0] = nu;
+    st[1] = nu / xn;
+    st[2] = rayleigh ? sc[SC_S] * s1 / (xn * xn) : 0.0;
+  }
+  if (tape_nu) tape_nu[(long)b * K + (k - 1)] = nu;
+  flag_norm(err, nu);
+  sc[SC_S] = 1.0 / nu;
+  sc[SC_XNORM] = 1.0;
+  sc[SC_NU] = nu;
+}
+
+// Backward step k produced x_bar_{k-1}; s0 = c_{k-1} = <x_{k-1}, x_bar_{k-1}>.
+__device__ __forceinline__ void bwd_finalize(double* sc, const double* tape_nu, int K, int k, int b, double s0) {
+  if (k >= 2) {
+    const double nu1 = tape_nu[(long)b * K + (k - 2)];
+    sc[SC_CN] = s0 / nu1;
+    sc[SC_INV_NU] = 1.0 / nu1;
+    sc[SC_INV_NU_PREV] = (k >= 3) ? 1.0 / tape_nu[(long)b * K + (k - 3)] : 0.0;
+  }
+}
 
 template <int R>
 struct SpassGeom {
@@ -382,29 +412,13 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
       s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     }
     if (lane == 0) {
-      double* sc = P.sc + b * kScal;
-      if (MODE == SP_FWD) {
-        const double nu = sqrt(s0);
-        const double xn = sc[SC_XNORM];
-        if (P.stats) {
-          double* st = P.stats + ((long)b * P.K + (P.k - 1)) * 3;
-          st[0] = nu;
-          st[1] = nu / xn;
-          st[2] = P.pprev ? sc[SC_S] * s1 / (xn * xn) : 0.0;
-        }
-        if (P.tape_nu) P.tape_nu[(long)b * P.K + (P.k - 1)] = nu;
-        flag_norm(P.err, nu);
-        sc[SC_S] = 1.0 / nu;
-        sc[SC_XNORM] = 1.0;
-        sc[SC_NU] = nu;
+      if (P.loc) {
+        P.loc[2 * b] = s0;
+        P.loc[2 * b + 1] = s1;
+      } else if (MODE == SP_FWD) {
+        fwd_finalize(P.sc + b * kScal, P.stats, P.tape_nu, P.err, P.K, P.k, P.pprev != nullptr, b, s0, s1);
       } else {
-        // step k produced x_bar_{k-1}; s0 = c_{k-1} = <x_{k-1}, x_bar_{k-1}>
-        if (P.k >= 2) {
-          const double nu1 = P.tape_nu[(long)b * P.K + (P.k - 2)];
-          sc[SC_CN] = s0 / nu1;
-          sc[SC_INV_NU] = 1.0 / nu1;
-          sc[SC_INV_NU_PREV] = (P.k >= 3) ? 1.0 / P.tape_nu[(long)b * P.K + (P.k - 3)] : 0.0;
-        }
+        bwd_finalize(P.sc + b * kScal, P.tape_nu, P.K, P.k, b, s0);
       }
     }
   }

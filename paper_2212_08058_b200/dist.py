@@ -1,0 +1,87 @@
+"""Multi-GPU plumbing for the time-slab decomposition.
+
+One process per GPU.  Rank r owns frames ``slab_range(T, n, r)`` of every
+volume.  ``torch.distributed`` only carries the 128-byte NCCL unique id from
+rank 0 to the others; the solve itself runs in libsfseg.so, which drives NCCL
+(halo send/recv with ranks +-1 and an fp64 allreduce of the norm partials)
+on the caller's CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Tuple
+
+import torch
+
+from . import (DistC, Gauss, Shape, _alloc_bytes, _check, _ptr, _require, _stream, _weights, lib,
+               ACT_IDENTITY)
+
+
+def slab_range(T: int, n: int, r: int) -> Tuple[int, int]:
+    """Frames [t0, t1) of slab r of n (uneven when n does not divide T; same rule as the C library)."""
+    if not (0 <= r < n):
+        raise ValueError("rank out of range")
+    return (T * r) // n, (T * (r + 1)) // n
+
+
+def broadcast_unique_id(rank: int, group=None) -> bytes:
+    """NCCL unique id created on rank 0 (sfseg_get_unique_id) and broadcast to all ranks."""
+    import torch.distributed as dist
+    buf = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        raw = (C.c_uint8 * 128)()
+        _check(lib().sfseg_get_unique_id(raw), "sfseg_get_unique_id")
+        buf = torch.tensor(list(bytes(raw)), dtype=torch.uint8)
+    backend = dist.get_backend(group)
+    dev_buf = buf.cuda() if backend == "nccl" else buf
+    dist.broadcast(dev_buf, src=0, group=group)
+    return bytes(dev_buf.cpu().tolist())
+
+
+class Comm:
+    """sfseg_comm (NCCL communicator created from a broadcast unique id)."""
+
+    def __init__(self, nranks: int, rank: int, device: int, uid: bytes):
+        self.nranks, self.rank, self.device = nranks, rank, device
+        self._h = C.c_void_p()
+        raw = (C.c_uint8 * 128)(*uid)
+        _check(lib().sfseg_comm_create(raw, nranks, rank, device, C.byref(self._h)), "sfseg_comm_create")
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def close(self) -> None:
+        if self._h:
+            _check(lib().sfseg_comm_destroy(self._h), "sfseg_comm_destroy")
+            self._h = C.c_void_p()
+
+
+class SlabSolver:
+    """One rank of a time-slab sharded solve (ch / x are this rank's local slab)."""
+
+    def __init__(self, comm: Comm, local_shape, T_global: int, t_offset: int, C_: int, gauss: Gauss, K: int,
+                 device="cuda"):
+        self.comm, self.shape = comm, tuple(int(v) for v in local_shape)
+        self.C, self.gauss, self.K = int(C_), gauss, int(K)
+        self.dist = DistC(comm.handle, int(T_global), int(t_offset))
+        ws, _ = C.c_size_t(0), None
+        n = C.c_size_t(0)
+        _check(lib().sfseg_workspace_bytes(Shape(*self.shape), self.C, gauss.c(), self.K, 0, C.byref(self.dist),
+                                           C.byref(n), None), "sfseg_workspace_bytes(dist)")
+        self.ws_bytes = n.value
+        self.ws = _alloc_bytes(n.value, device)
+        self.stats = torch.zeros((self.shape[0], self.K, 3), dtype=torch.float64, device=device)
+
+    def forward(self, ch: torch.Tensor, w, b: float = 0.0, act: int = ACT_IDENTITY,
+                x_out: Optional[torch.Tensor] = None, check: bool = True, stream=None) -> torch.Tensor:
+        _require(ch, "ch", 5)
+        if x_out is None:
+            x_out = torch.empty(self.shape, dtype=torch.float32, device=ch.device)
+        _check(lib().sfseg_power_iterate(
+            _ptr(ch), self.C, _weights(w, self.C), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
+            None, _ptr(x_out), None, _ptr(self.stats), 0, None, _ptr(self.ws), self.ws_bytes,
+            C.byref(self.dist), _stream(stream)), "sfseg_power_iterate(dist)")
+        if check:
+            _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate(dist, device)")
+        return x_out

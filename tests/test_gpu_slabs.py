@@ -1,0 +1,59 @@
+"""GPU: the time-slab decomposition (multi-GPU path's per-rank phases, emulated
+on one device: halo copies + rank-ordered norm reduction) matches the single-GPU
+solve and the oracle, including uneven slabs and B > 1."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as WL
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2212_08058_b200 as m
+    m.lib()
+    return m
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("name,shape,nslabs,K", [
+    ("c2", dict(T=26, H=70, W=150), 1, 6),
+    ("c2", dict(T=26, H=70, W=150), 2, 6),
+    ("c2", dict(T=26, H=70, W=150), 4, 6),      # uneven: 6,7,6,7 frames, r_t = 6
+    ("c5", dict(T=40, H=64, W=140), 3, 5),      # r_t = 9, r_s = 36
+    ("c4", dict(B=2, T=23, H=48, W=70), 2, 5),  # B > 1
+])
+def test_slabs_match_single_gpu_and_oracle(sf, name, shape, nslabs, K):
+    cfg = WL.get_config(name, **shape)
+    wl = WL.generate(name, cfg=cfg)
+    g = sf.Gauss(cfg.sigma_t, cfg.sigma_s, cfg.radius_t, cfg.radius_s)
+    ch = torch.from_numpy(wl.ch).cuda()
+    xs, sts = sf.power_iterate_slabs(ch, wl.w, g, K, nslabs, want_rayleigh=True)
+    B, C, T, H, W = wl.ch.shape
+    solver = sf.Solver((B, T, H, W), C, g, K)
+    x1 = solver.forward(ch, wl.w, want_rayleigh=True)
+    xs, x1 = xs.cpu().numpy(), x1.cpu().numpy()
+    for b in range(B):
+        assert _rel(xs[b], x1[b].astype(np.float64)) < 1e-6
+    np.testing.assert_allclose(sts.cpu().numpy(), solver.stats.cpu().numpy(), rtol=1e-6)
+    F, _ = O.combine(wl.ch, wl.w)
+    xo, sto = O.power_iterate(F, O.gaussian_taps(cfg.sigma_t, cfg.radius_t),
+                              O.gaussian_taps(cfg.sigma_s, cfg.radius_s), K)
+    for b in range(B):
+        assert _rel(xs[b], xo[b]) <= 1e-4
+    np.testing.assert_allclose(sts.cpu().numpy()[..., 1], sto["gain"], rtol=1e-5)
+
+
+def test_slab_too_thin_rejected(sf):
+    ch = torch.rand((1, 1, 8, 20, 20), device="cuda")
+    with pytest.raises(sf.SfsegError) as e:
+        sf.power_iterate_slabs(ch, [1.0], sf.Gauss(2.0, 2.0, 6, 6), 3, 4)   # 2-frame slabs < r_t = 6
+    assert e.value.status == 2
