@@ -9,7 +9,9 @@ pass with F multiplies and norm) + final normalisation + per-frame threshold
 (SURVEY.md §8(a) rows a1-a9).  At N=1 the workload is BASELINE.json configs[1]
 ("c2": 1x70x480x854, C=1, sigma_t=2, sigma_s=8, 15 iterations, tau=0.5).
 For N>1 (torchrun, one rank per GPU) every rank solves its own c2 volume
-(data-parallel over independent volumes, weak scaling, no data-path collective).
+(data-parallel over independent volumes, weak scaling, no data-path collective);
+with --shard slab the ranks split ONE volume into time slabs (NCCL halo
+exchange of r_t frames + fp64 norm allreduce every iteration, strong scaling).
 
 metric: voxel-iterations/s = B*T*H*W*K_iter per step, whole job.
 """
@@ -177,20 +179,34 @@ def run_ours(args):
     sf.lib()
 
     cfg = WL.get_config(args.config)
-    wl = WL.generate(args.config, with_mask=False)
-    B, Cn, T, H, W = wl.ch.shape
+    slab = world > 1 and args.shard == "slab"
     K = cfg.K
     gauss = sf.Gauss(cfg.sigma_t, cfg.sigma_s, cfg.radius_t, cfg.radius_s)
+    if slab:
+        from paper_2212_08058_b200.dist import Comm, SlabSolver, broadcast_unique_id, slab_range
+        t0, t1 = slab_range(cfg.T, world, rank)
+        wl = WL.generate(args.config, t_range=(t0, t1), with_mask=False)
+        uid = broadcast_unique_id(rank)
+        comm = Comm(world, rank, local, uid)
+    else:
+        wl = WL.generate(args.config, with_mask=False)
+    B, Cn, T, H, W = wl.ch.shape
     ch_host = torch.from_numpy(wl.ch).pin_memory()
     ch = ch_host.to(dev)
-    solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev)
+    if slab:
+        solver = SlabSolver(comm, (B, T, H, W), cfg.T, t0, Cn, gauss, K, device=dev)
+    else:
+        solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev)
     x = torch.empty((B, T, H, W), dtype=torch.float32, device=dev)
     mask = torch.empty((B, T, H, W), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    # the per-frame threshold (a9) is frame-local: each rank thresholds its own slab
+    thr_solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev) if slab else solver
+
     def step():
         solver.forward(ch, wl.w, wl.b, cfg.act, x_out=x, check=False)
-        solver.threshold(x, cfg.tau, sf.THR_PER_FRAME_MAX, mask=mask)
+        thr_solver.threshold(x, cfg.tau, sf.THR_PER_FRAME_MAX, mask=mask)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -227,7 +243,10 @@ def run_ours(args):
 
     vox = B * T * H * W
     units_per_step = vox * K
-    value = world * units_per_step * args.steps / (ms_max / 1e3)
+    if slab:   # strong scaling: the ranks together process one volume per step
+        value = B * cfg.T * H * W * K * args.steps / (ms_max / 1e3)
+    else:
+        value = world * units_per_step * args.steps / (ms_max / 1e3)
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     peaks, peaks_src = _peaks()
@@ -267,7 +286,7 @@ def run_ours(args):
 
     # ---------------------------------------------------------------- e2e through the C ABI with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not slab:
         d_ch = torch.empty_like(ch)
         x_host = torch.empty((B, T, H, W), dtype=torch.float32).pin_memory()
         m_host = torch.empty((B, T, H, W), dtype=torch.uint8).pin_memory()
@@ -296,11 +315,13 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (workloads/ generator; DAVIS-2016-shaped blobs, seed 0)",
             "config": {"workload": f"{args.config}: {cfg.note}", "shape": [B, T, H, W], "C": Cn,
                        "sigma_t": cfg.sigma_t, "sigma_s": cfg.sigma_s, "radius_t": r_t, "radius_s": r_s,
-                       "iters": K, "tau": cfg.tau, "parallelism": f"dp{world} (one volume per GPU)",
+                       "iters": K, "tau": cfg.tau,
+                       "parallelism": (f"time-slab x{world} (NCCL halo r_t frames + fp64 norm allreduce / iter)"
+                                       if slab else f"dp{world} (one volume per GPU)"),
                        "l2": "inputs > L2 (ch 115 MB + F/p/v 344 MB vs 126 MB L2); no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": (2 * K + 4) * args.steps,
@@ -308,6 +329,8 @@ def run_ours(args):
             "clock_samples": ck["samples"],
         }
         print(json.dumps(line), flush=True)
+    if slab:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -322,6 +345,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", default="volume", choices=["volume", "slab"],
+                    help="N>1: one volume per GPU (weak scaling) or time slabs of one volume with NCCL halos (strong)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -83,5 +83,8 @@ class SlabSolver:
             None, _ptr(x_out), None, _ptr(self.stats), 0, None, _ptr(self.ws), self.ws_bytes,
             C.byref(self.dist), _stream(stream)), "sfseg_power_iterate(dist)")
         if check:
-            _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate(dist, device)")
+            self.sync(stream)
         return x_out
+
+    def sync(self, stream=None) -> None:
+        _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate(dist, device)")

@@ -57,3 +57,29 @@ def test_slab_too_thin_rejected(sf):
     with pytest.raises(sf.SfsegError) as e:
         sf.power_iterate_slabs(ch, [1.0], sf.Gauss(2.0, 2.0, 6, 6), 3, 4)   # 2-frame slabs < r_t = 6
     assert e.value.status == 2
+
+
+def test_nccl_single_rank_dist_path(sf):
+    """The NCCL-driven per-rank path (sfseg_comm + dist) with one rank: exercises
+    dlopen'd NCCL (unique id, comm init, fp64 allreduce) and the dist finalize."""
+    import ctypes as C
+    from paper_2212_08058_b200.dist import Comm, SlabSolver
+    raw = (C.c_uint8 * 128)()
+    st = sf.lib().sfseg_get_unique_id(raw)
+    if st == 8:
+        pytest.skip("NCCL not loadable")
+    assert st == 0
+    comm = Comm(1, 0, torch.cuda.current_device(), bytes(raw))
+    try:
+        cfg = WL.get_config("c2", T=12, H=60, W=100)
+        wl = WL.generate("c2", cfg=cfg)
+        g = sf.Gauss(2.0, 8.0, 6, 24)
+        ch = torch.from_numpy(wl.ch).cuda()
+        s = SlabSolver(comm, (1, 12, 60, 100), 12, 0, 1, g, 6)
+        xd = s.forward(ch, wl.w).cpu().numpy()
+        ref = sf.Solver((1, 12, 60, 100), 1, g, 6)
+        x1 = ref.forward(ch, wl.w).cpu().numpy()
+        assert _rel(xd, x1.astype(np.float64)) < 1e-6
+        np.testing.assert_allclose(s.stats.cpu().numpy(), ref.stats.cpu().numpy(), rtol=1e-6)
+    finally:
+        comm.close()
