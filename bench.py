@@ -264,7 +264,8 @@ def run_ours(args):
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(args.config, {}).get("spass_dram_bytes_per_launch")
+            # {config: {"spass": {"dram_bytes_per_launch": ..., "source": "profiles/<round>/..."}}}
+            traffic = json.load(open(tfile)).get(args.config, {}).get("spass", {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
