@@ -30,6 +30,15 @@ struct CombineParams {
   float w[kMaxC];
 };
 
+// Row-parallel layout shared by the streaming kernels: grid (gx, B*T); block
+// (bx, bt) handles rows y = bx*kRows + j (+ gx*kRows per pass) of frame bt;
+// thread tid covers columns tid + i*kEwThreads.  Lanes map to consecutive
+// columns (coalesced 128-byte rows for dense and pitched layouts alike); kRows
+// rows x kCols column chunks are unrolled so every thread keeps kRows*kCols
+// independent loads in flight (HBM latency hiding without any index division).
+constexpr int kRows = 2;
+constexpr int kCols = 4;
+
 __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_constant__ CombineParams P) {
   __shared__ double red[kEwThreads / 32];
   __shared__ int flag;
@@ -37,25 +46,59 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
   const int b = bt / P.T, t = bt - b * P.T;
   const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
   const long vol_dense = (long)P.in_T * HW;
+  const float* chf = P.ch + (long)b * P.C * vol_dense + (long)(P.in_t0 + t) * HW;  // frame base, channel 0
+  const long dbase = (long)b * vol_dense + (long)(P.in_t0 + t) * HW;              // dense x0 / F_out frame base
   double acc = 0.0;
-  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HWp; e += (long)P.gx * kEwThreads) {
-    const int y = (int)(e / P.Wp), x = (int)(e - (long)y * P.Wp);
-    const long po = (long)bt * HWp + e;
-    float f = 0.f, pv = 0.f, xv = 0.f;
-    if (x < P.W) {
-      const long d = (long)(P.in_t0 + t) * HW + (long)y * P.W + x;
-      const float* chb = P.ch + (long)b * P.C * vol_dense + d;
-      float z = P.bias;
-      for (int c = 0; c < P.C; ++c) z = fmaf(P.w[c], __ldg(chb + (long)c * vol_dense), z);
-      f = (P.act == 1) ? 1.f / (1.f + expf(-z)) : z;
-      xv = P.x0 ? __ldg(P.x0 + (long)b * vol_dense + d) : f;
-      pv = f * xv;
-      if (P.F_out) P.F_out[(long)b * vol_dense + d] = f;
-      acc += (double)xv * (double)xv;
+  for (int y0 = blockIdx.x * kRows; y0 < P.H; y0 += P.gx * kRows) {
+    for (int c0 = 0; c0 < P.Wp; c0 += kEwThreads * kCols) {
+      float z[kRows][kCols];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) z[r][i] = P.bias;
+      for (int c = 0; c < P.C; ++c) {
+        float v[kRows][kCols];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r)
+#pragma unroll
+          for (int i = 0; i < kCols; ++i) {
+            const int y = y0 + r, x = c0 + i * kEwThreads + threadIdx.x;
+            v[r][i] = (y < P.H && x < P.W) ? __ldcs(chf + (long)c * vol_dense + (long)y * P.W + x) : 0.f;
+          }
+#pragma unroll
+        for (int r = 0; r < kRows; ++r)
+#pragma unroll
+          for (int i = 0; i < kCols; ++i) z[r][i] = fmaf(P.w[c], v[r][i], z[r][i]);
+      }
+      float xv[kRows][kCols];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) {
+          const int y = y0 + r, x = c0 + i * kEwThreads + threadIdx.x;
+          xv[r][i] = 0.f;
+          if (P.x0 && y < P.H && x < P.W) xv[r][i] = __ldcs(P.x0 + dbase + (long)y * P.W + x);
+        }
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) {
+          const int y = y0 + r, x = c0 + i * kEwThreads + threadIdx.x;
+          if (y >= P.H || x >= P.Wp) continue;
+          const long po = (long)bt * HWp + (long)y * P.Wp + x;
+          float f = 0.f, pv = 0.f, xx = 0.f;
+          if (x < P.W) {
+            f = (P.act == 1) ? 1.f / (1.f + expf(-z[r][i])) : z[r][i];
+            xx = P.x0 ? xv[r][i] : f;
+            pv = f * xx;
+            if (P.F_out) P.F_out[dbase + (long)y * P.W + x] = f;
+            acc += (double)xx * (double)xx;
+          }
+          P.F[po] = f;  // pad columns x >= W hold zeros
+          if (P.p0) P.p0[po] = pv;
+          if (P.x0p) P.x0p[po] = xx;
+        }
     }
-    P.F[po] = f;
-    if (P.p0) P.p0[po] = pv;
-    if (P.x0p) P.x0p[po] = xv;
   }
   if (P.partials == nullptr) return;  // plain combine (sfseg_combine_channels): no reduction
   const double s = block_sum<kEwThreads>(acc, red);
@@ -120,7 +163,7 @@ __global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams
 }
 
 // ------------------------------------------------------------------ final normalisation x_K = y_K / nu_K
-// x (dense, buffer of out_T frames per volume; this slab starts at frame out_t0)
+// x (dense, buffer of out_T frames per volume; this slab starts at frame out_t0).  grid (gx, B*T).
 __global__ void __launch_bounds__(kEwThreads) final_scale_kernel(const float* __restrict__ y, float* __restrict__ x,
                                                                  const double* sc, int T, int H, int W, int Wp,
                                                                  int out_T, int out_t0) {
@@ -128,18 +171,59 @@ __global__ void __launch_bounds__(kEwThreads) final_scale_kernel(const float* __
   const float s = (float)sc[b * kScal + SC_S];
   const long HW = (long)H * W;
   float* xo = x + ((long)b * out_T + out_t0 + t) * HW;
-  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HW; e += (long)gridDim.x * kEwThreads) {
-    const int yy = (int)(e / W), xx = (int)(e - (long)yy * W);
-    xo[e] = __ldcs(y + ((long)bt * H + yy) * Wp + xx) * s;
+  const float* yi = y + (long)bt * H * Wp;
+  for (int y0 = blockIdx.x * kRows; y0 < H; y0 += gridDim.x * kRows) {
+    for (int c0 = 0; c0 < W; c0 += kEwThreads * kCols) {
+      float v[kRows][kCols];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) {
+          const int yy = y0 + r, xx = c0 + i * kEwThreads + threadIdx.x;
+          v[r][i] = (yy < H && xx < W) ? __ldcs(yi + (long)yy * Wp + xx) : 0.f;
+        }
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) {
+          const int yy = y0 + r, xx = c0 + i * kEwThreads + threadIdx.x;
+          if (yy < H && xx < W) __stcs(xo + (long)yy * W + xx, v[r][i] * s);
+        }
+    }
   }
 }
 
 // ------------------------------------------------------------------ threshold
-__global__ void __launch_bounds__(kEwThreads) frame_max_kernel(const float* __restrict__ x, float* fmax, long HW) {
+// Per-frame maximum in two deterministic steps (max is order independent):
+// frame_max_kernel writes one partial per (frame, block) -> part[bt * gx + bx],
+// threshold_kernel folds the gx partials of its frame (or of the whole volume).
+constexpr int kThrGx = 16;
+
+__global__ void __launch_bounds__(kEwThreads) frame_max_kernel(const float* __restrict__ x, float* part, long HW) {
   __shared__ float red[kEwThreads / 32];
-  const long base = (long)blockIdx.x * HW;
+  const float* xf = x + (long)blockIdx.y * HW;
   float m = -INFINITY;
-  for (long e = threadIdx.x; e < HW; e += kEwThreads) m = fmaxf(m, x[base + e]);
+  const bool vec = ((HW & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  if (vec) {
+    const float4* x4 = reinterpret_cast<const float4*>(xf);
+    const long n4 = HW >> 2;
+    long e = (long)blockIdx.x * kEwThreads + threadIdx.x;
+    const long step = (long)gridDim.x * kEwThreads;
+    for (; e + 3 * step < n4; e += 4 * step) {
+      float4 a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = __ldg(x4 + e + i * step);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) m = fmaxf(m, fmaxf(fmaxf(a[i].x, a[i].y), fmaxf(a[i].z, a[i].w)));
+    }
+    for (; e < n4; e += step) {
+      const float4 a = __ldg(x4 + e);
+      m = fmaxf(m, fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)));
+    }
+  } else {
+    for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HW; e += (long)gridDim.x * kEwThreads)
+      m = fmaxf(m, __ldg(xf + e));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -147,12 +231,13 @@ __global__ void __launch_bounds__(kEwThreads) frame_max_kernel(const float* __re
   if (threadIdx.x == 0) {
     float r = red[0];
     for (int i = 1; i < kEwThreads / 32; ++i) r = fmaxf(r, red[i]);
-    fmax[blockIdx.x] = r;
+    part[(long)blockIdx.y * gridDim.x + blockIdx.x] = r;
   }
 }
 
+// grid (gx, B*T); `part` holds npart partials per frame (ignored for mode 2).
 __global__ void __launch_bounds__(kEwThreads) threshold_kernel(const float* __restrict__ x, uint8_t* __restrict__ mask,
-                                                               const float* fmax, int T, long HW, float tau,
+                                                               const float* part, int npart, int T, long HW, float tau,
                                                                int mode) {
   const int bt = blockIdx.y, b = bt / T;
   float thr;
@@ -160,19 +245,32 @@ __global__ void __launch_bounds__(kEwThreads) threshold_kernel(const float* __re
   if (mode == 2) {
     thr = tau;
   } else {
-    float m;
-    if (mode == 0) {
-      m = fmax[bt];
-    } else {
-      m = fmax[b * T];
-      for (int t = 1; t < T; ++t) m = fmaxf(m, fmax[b * T + t]);
-    }
+    float m = -INFINITY;
+    const int f0 = (mode == 0) ? bt : b * T, f1 = (mode == 0) ? bt + 1 : (b + 1) * T;
+    for (long i = (long)f0 * npart; i < (long)f1 * npart; ++i) m = fmaxf(m, part[i]);
     none = !(m > 0.f);
     thr = tau * m;
   }
   const long base = (long)bt * HW;
-  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HW; e += (long)gridDim.x * kEwThreads)
-    mask[base + e] = (!none && x[base + e] > thr) ? 1 : 0;
+  const bool vec = ((HW & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(mask) & 3) == 0);
+  if (vec) {
+    const float4* x4 = reinterpret_cast<const float4*>(x + base);
+    uchar4* m4 = reinterpret_cast<uchar4*>(mask + base);
+    const long n4 = HW >> 2;
+    for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < n4; e += (long)gridDim.x * kEwThreads) {
+      const float4 a = __ldcs(x4 + e);
+      uchar4 o;
+      o.x = (!none && a.x > thr) ? 1 : 0;
+      o.y = (!none && a.y > thr) ? 1 : 0;
+      o.z = (!none && a.z > thr) ? 1 : 0;
+      o.w = (!none && a.w > thr) ? 1 : 0;
+      __stcs(m4 + e, o);
+    }
+  } else {
+    for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HW; e += (long)gridDim.x * kEwThreads)
+      mask[base + e] = (!none && x[base + e] > thr) ? 1 : 0;
+  }
 }
 
 // ------------------------------------------------------------------ backward set-up: x_bar_K, F_bar = 0, c_K

@@ -193,6 +193,14 @@ struct ProfScope {
   }
 };
 
+// Blocks per frame for the row-parallel streaming kernels (misc.cuh): enough
+// CTAs in total to fill 148 SMs several times over, at most one per kRows rows.
+int ew_gx(int64_t H, int64_t BT) {
+  const int64_t want = (8 * (int64_t)num_sms() + BT - 1) / BT;
+  const int64_t rows = (H + kRows - 1) / kRows;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, rows), 16));
+}
+
 // ------------------------------------------------------------------ problem plan
 struct Plan {
   int64_t B, T, H, W, Wp, BT;
@@ -241,10 +249,9 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->U = P->BT * P->S * P->NB;
   const int64_t cap = (int64_t)num_sms() * spass_occupancy(P->RS);
   P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 4));
-  const int64_t per_frame = (P->H * P->Wp + 256 * 4 - 1) / (256 * 4);
-  P->gx = (int)std::max<int64_t>(1, std::min<int64_t>(per_frame, 16));
+  P->gx = ew_gx(P->H, P->BT);
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
-  size_t n_part = std::max<size_t>(2 * (size_t)P->B * P->G, (size_t)P->BT * P->gx);
+  size_t n_part = std::max<size_t>(2 * (size_t)P->B * P->G * kCW, (size_t)P->BT * P->gx);
   n_part = std::max<size_t>(n_part, (size_t)4 * num_sms() * (kMaxC + 1));
   P->n_part = n_part;
   size_t off = align_up(sizeof(WsHeader));
@@ -469,8 +476,7 @@ sfseg_status ph_S(Rank& r, int k, cudaStream_t st) {
 
 sfseg_status ph_final(Rank& r, cudaStream_t st) {
   const Plan& P = r.P;
-  const int64_t per = (P.H * P.W + 1023) / 1024;
-  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(per, 64)), (unsigned)P.BT);
+  dim3 grid((unsigned)P.gx, (unsigned)P.BT);
   final_scale_kernel<<<grid, kEwThreads, 0, st>>>(r.p, r.x_out, at<double>(r.ws, P.off_sc), (int)P.T, (int)P.H,
                                                   (int)P.W, (int)P.Wp, r.out_T, r.out_t0);
   SF_CUDA(after_launch("final_scale(slab)", st));
@@ -644,8 +650,7 @@ sfseg_status sfseg_combine_channels(const float* ch, int32_t C, sfseg_shape sh, 
   cp.in_t0 = 0;
   cp.bias = b;
   for (int c = 0; c < C; ++c) cp.w[c] = w_host[c];
-  const int64_t per_frame = (sh.H * sh.W + 1023) / 1024;
-  cp.gx = (int)std::max<int64_t>(1, std::min<int64_t>(per_frame, 16));
+  cp.gx = ew_gx(sh.H, sh.B * sh.T);
   cp.partials = nullptr;  // no ||x_0|| reduction for the standalone combine
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   combine_kernel<<<dim3(cp.gx, (unsigned)(sh.B * sh.T)), kEwThreads, 0, st>>>(cp);
@@ -722,8 +727,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
   }
   // (a8) x_K = y_K / nu_K (dense output)
   {
-    const int64_t per = (P.H * P.W + 1023) / 1024;
-    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(per, 64)), (unsigned)P.BT);
+    dim3 grid((unsigned)P.gx, (unsigned)P.BT);
     final_scale_kernel<<<grid, kEwThreads, 0, st>>>(p, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H, (int)P.W,
                                                     (int)P.Wp, (int)P.T, 0);
     SF_CUDA(after_launch("final_scale", st));
@@ -853,7 +857,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
 
 size_t sfseg_threshold_ws_bytes(sfseg_shape sh) {
   if (sh.B < 1 || sh.T < 1) return 0;
-  return align_up(sizeof(float) * (size_t)(sh.B * sh.T));
+  return align_up(sizeof(float) * (size_t)(sh.B * sh.T) * kThrGx);
 }
 
 sfseg_status sfseg_threshold(const float* x, sfseg_shape sh, float tau, int32_t mode, uint8_t* mask, void* ws,
@@ -865,14 +869,14 @@ sfseg_status sfseg_threshold(const float* x, sfseg_shape sh, float tau, int32_t 
   if (s != SFSEG_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const long HW = (long)(sh.H * sh.W);
-  float* fmax = static_cast<float*>(ws);
+  float* part = static_cast<float*>(ws);
+  const unsigned BT = (unsigned)(sh.B * sh.T);
+  const int gx = ew_gx(sh.H * sh.W / 1024 + 1, sh.B * sh.T);
   if (mode != SFSEG_THR_ABSOLUTE) {
-    frame_max_kernel<<<(unsigned)(sh.B * sh.T), kEwThreads, 0, st>>>(x, fmax, HW);
+    frame_max_kernel<<<dim3(kThrGx, BT), kEwThreads, 0, st>>>(x, part, HW);
     SF_CUDA(cudaGetLastError());
   }
-  const int64_t per = (HW + 1023) / 1024;
-  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(per, 64)), (unsigned)(sh.B * sh.T));
-  threshold_kernel<<<grid, kEwThreads, 0, st>>>(x, mask, fmax, (int)sh.T, HW, tau, mode);
+  threshold_kernel<<<dim3(gx, BT), kEwThreads, 0, st>>>(x, mask, part, kThrGx, (int)sh.T, HW, tau, mode);
   return map_cuda(cudaGetLastError());
 }
 

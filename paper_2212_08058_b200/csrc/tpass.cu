@@ -4,14 +4,14 @@
 namespace sfseg {
 template <int MODE>
 static cudaError_t launch_tpass_t(int RT, const TpassParams& P, int B, cudaStream_t st) {
-  dim3 grid((unsigned)((P.frame4 + 255) / 256), (unsigned)B);
+  dim3 grid((unsigned)((P.frame4 + kTpThreads - 1) / kTpThreads), (unsigned)B);
   switch (RT) {
 #define TP_CASE(r)                                             \
   case r:                                                      \
     if (P.halo_lo || P.halo_hi)                                \
-      tpass_kernel<r, MODE, true><<<grid, 256, 0, st>>>(P);    \
+      tpass_kernel<r, MODE, true><<<grid, kTpThreads, 0, st>>>(P);    \
     else                                                       \
-      tpass_kernel<r, MODE, false><<<grid, 256, 0, st>>>(P);   \
+      tpass_kernel<r, MODE, false><<<grid, kTpThreads, 0, st>>>(P);   \
     return cudaGetLastError();
     TP_CASE(0) TP_CASE(1) TP_CASE(2) TP_CASE(3) TP_CASE(4) TP_CASE(5) TP_CASE(6) TP_CASE(8) TP_CASE(9)
     TP_CASE(12) TP_CASE(16)

@@ -32,70 +32,116 @@ struct TpassParams {
   float g[2 * kMaxRT + 1];  // g[i] = weight of temporal offset i - RT
 };
 
+constexpr int kTpThreads = 128;
+// Resident CTAs per SM the register budget is sized for: the ring of 2RT+1
+// float4 accumulators dominates (RT=6: 52 registers).  At c2 (frame4 = 102,720
+// float4 columns) 6 x 128 threads per SM hold every column in ONE wave.
+__host__ __device__ constexpr int tpass_min_blocks(int RT) { return RT <= 6 ? 6 : (RT <= 9 ? 4 : 2); }
+// cp.async stages per input stream (frames prefetched ahead of the ring).
+__host__ __device__ constexpr int tpass_stages(int MODE) { return MODE == TP_FWD ? 8 : 4; }
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One thread = one float4 column (b, y, 4x..4x+3) of the pitched volume, walked
+// through all frames.  Input frames are prefetched NS frames ahead with cp.async
+// into a per-thread shared-memory slot (no register cost for loads in flight;
+// each thread reads back only its own slots, so no block barrier is needed);
+// the 2RT+1 partial outputs an input frame feeds live in a register ring
+// (unrolled by 2RT+1 so ring slots are static registers).
 template <int RT, int MODE, bool HALO>
-__global__ void __launch_bounds__(256) tpass_kernel(const __grid_constant__ TpassParams P) {
+__global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel(const __grid_constant__ TpassParams P) {
   constexpr int NR = 2 * RT + 1;
+  constexpr int NS = tpass_stages(MODE);
+  constexpr int NIN = (MODE == TP_FWD) ? 1 : 3;
+  __shared__ float4 sq[NS][NIN][kTpThreads];
   const int b = blockIdx.y;
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= P.frame4) return;
+  const int tid = threadIdx.x;
+  const long e = (long)blockIdx.x * kTpThreads + tid;
+  const bool active = e < P.frame4;
   const int T = P.T;
   const long vol4 = (long)T * P.frame4;
-  const float4* src = reinterpret_cast<const float4*>(P.src) + b * vol4 + e;
+  const long ec = active ? e : 0;  // inactive threads keep valid addresses and skip the stores
+  const float4* src = reinterpret_cast<const float4*>(P.src) + b * vol4 + ec;
   const float4* Fp = nullptr;
   const float4* U1 = nullptr;
   float cn = 0.f, inv_nu = 0.f, scale = 1.f;
   if (MODE == TP_FWD) {
     scale = (float)P.sc[b * kScal + SC_S];
   } else {
-    Fp = reinterpret_cast<const float4*>(P.F) + b * vol4 + e;
-    U1 = reinterpret_cast<const float4*>(P.u1) + b * vol4 + e;
+    Fp = reinterpret_cast<const float4*>(P.F) + b * vol4 + ec;
+    U1 = reinterpret_cast<const float4*>(P.u1) + b * vol4 + ec;
     cn = (float)P.sc[b * kScal + SC_CN];
     inv_nu = (float)P.sc[b * kScal + SC_INV_NU];
   }
-  const float4* hlo = P.halo_lo ? reinterpret_cast<const float4*>(P.halo_lo) + (long)b * RT * P.frame4 + e : nullptr;
-  const float4* hhi = P.halo_hi ? reinterpret_cast<const float4*>(P.halo_hi) + (long)b * RT * P.frame4 + e : nullptr;
-  float4* out = reinterpret_cast<float4*>(P.out) + b * vol4 + e;
-
-  float4 acc[NR];
-#pragma unroll
-  for (int i = 0; i < NR; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4* hlo = P.halo_lo ? reinterpret_cast<const float4*>(P.halo_lo) + (long)b * RT * P.frame4 + ec : nullptr;
+  const float4* hhi = P.halo_hi ? reinterpret_cast<const float4*>(P.halo_hi) + (long)b * RT * P.frame4 + ec : nullptr;
+  float4* out = reinterpret_cast<float4*>(P.out) + b * vol4 + ec;
 
   // jp = j + RT enumerates input frames j = -RT .. T+RT-1; output t = jp - 2RT
-  // completes when input j = t + RT arrives.  Inputs are software-pipelined NR
-  // frames ahead (register queue q[]) so NR loads per thread are in flight.
-  auto load = [&](int jp) -> float4 {
+  // completes when input j = t + RT arrives.
+  auto frame_src = [&](int jp, int w) -> const float4* {
     const int j = jp - RT;
-    const int jc = min(max(j, 0), T - 1);  // clamped: always a valid address
-    float4 val;
+    if (j >= 0 && j < T) {
+      const long o = (long)j * P.frame4;
+      return (w == 0) ? src + o : (w == 1 ? Fp + o : U1 + o);
+    }
+    if (HALO && w == 0) {  // neighbour slab frames (time-slab sharding)
+      if (j < 0 && j >= -RT && hlo) return hlo + (long)(j + RT) * P.frame4;
+      if (j >= T && j < T + RT && hhi) return hhi + (long)(j - T) * P.frame4;
+    }
+    return nullptr;  // zero padding
+  };
+  const int jend = T + 2 * RT;
+  auto issue = [&](int jp) {
+    if (jp < jend) {
+#pragma unroll
+      for (int w = 0; w < NIN; ++w) {
+        const float4* g = frame_src(jp, w);
+        if (g) cp_async16(&sq[jp % NS][w][tid], g);
+      }
+    }
+    cp_async_commit();  // one group per frame, possibly empty: keeps wait_group counting uniform
+  };
+  auto fetch = [&](int jp) -> float4 {
+    const int j = jp - RT;
+    const int sl = jp % NS;
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
     if (MODE == TP_FWD) {
-      val = __ldcs(src + (long)jc * P.frame4);
-    } else {
-      const long o = (long)jc * P.frame4;
-      const float4 xb = src[o], f = Fp[o], u = U1[o];
+      if (frame_src(jp, 0)) val = sq[sl][0][tid];
+    } else if (j >= 0 && j < T) {
+      const float4 xb = sq[sl][0][tid], f = sq[sl][1][tid], u = sq[sl][2][tid];
       val.x = f.x * ((xb.x - f.x * u.x * cn) * inv_nu);
       val.y = f.y * ((xb.y - f.y * u.y * cn) * inv_nu);
       val.z = f.z * ((xb.z - f.z * u.z * cn) * inv_nu);
       val.w = f.w * ((xb.w - f.w * u.w * cn) * inv_nu);
-    }
-    if (HALO) {
-      // neighbour slab frames (time-slab sharding); absent halos read as zero
-      if (j < 0) val = (hlo != nullptr && j >= -RT) ? hlo[(long)(j + RT) * P.frame4] : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j >= T) val = (hhi != nullptr && j < T + RT) ? hhi[(long)(j - T) * P.frame4] : make_float4(0.f, 0.f, 0.f, 0.f);
-    } else if (j < 0 || j >= T) {
-      val = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (HALO) {
+      // backward halos arrive pre-multiplied (F * y_bar of the neighbour slab)
+      const float4* g = frame_src(jp, 0);
+      if (g) val = sq[sl][0][tid];
     }
     return val;
   };
-  const int jend = T + 2 * RT;
-  float4 q[NR];
+
+  float4 acc[NR];
 #pragma unroll
-  for (int d = 0; d < NR; ++d) q[d] = load(d);
+  for (int i = 0; i < NR; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int d = 0; d < NS; ++d) issue(d);
   for (int j0 = 0; j0 < jend; j0 += NR) {
 #pragma unroll
     for (int d = 0; d < NR; ++d) {
       const int jp = j0 + d;
-      const float4 val = q[d];
-      q[d] = load(jp + NR);  // prefetch (harmless past the end: clamped and zeroed)
+      if (jp >= jend) break;
+      cp_async_wait<NS - 1>();  // frame jp has landed (this thread's own copies)
+      const float4 val = fetch(jp);
+      issue(jp + NS);  // refill the slot just read
 #pragma unroll
       for (int ee = 0; ee < NR; ++ee) {
         // input j feeds output t = j - RT + ee with weight g[(j - t) + RT] = g[2RT - ee]
@@ -108,10 +154,11 @@ __global__ void __launch_bounds__(256) tpass_kernel(const __grid_constant__ Tpas
       }
       const int slot0 = (((d - 2 * RT) % NR) + NR) % NR;
       const int t = jp - 2 * RT;
-      if (t >= 0 && t < T) out[(long)t * P.frame4] = f4_scale(acc[slot0], scale);
+      if (active && t >= 0 && t < T) __stcg(out + (long)t * P.frame4, f4_scale(acc[slot0], scale));
       acc[slot0] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
+  cp_async_wait<0>();
 }
 
 }  // namespace sfseg
