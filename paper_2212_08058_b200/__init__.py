@@ -88,6 +88,7 @@ _SIGS = {
                                    C.c_float, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "sfseg_profile_enable": (C.c_int, [C.c_int32]),
     "sfseg_profile_read": (C.c_int, [_P, _P]),
+    "sfseg_set_algorithm": (C.c_int, [C.c_int32]),
     "sfseg_slabs_workspace_bytes": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
     "sfseg_power_iterate_slabs": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                             C.c_int32, _P, _P, _P, C.c_int32, _P, C.c_size_t, _P]),
@@ -154,11 +155,21 @@ def profile_enable(on: bool = True) -> None:
 
 def profile_read():
     """Sync the recorded events; returns {category: (total_ms, launches)} and resets."""
-    ms = (C.c_double * 4)()
-    n = (C.c_int64 * 4)()
+    ms = (C.c_double * 5)()
+    n = (C.c_int64 * 5)()
     _check(lib().sfseg_profile_read(ms, n), "sfseg_profile_read")
-    names = ("tpass", "spass", "once", "backward")
-    return {names[i]: (ms[i], n[i]) for i in range(4)}
+    names = ("tpass", "spass", "once", "backward", "f3d")
+    return {names[i]: (ms[i], n[i]) for i in range(5)}
+
+
+ALGO_AUTO = 0
+ALGO_TWO_PASS = 1
+
+
+def set_algorithm(algo: int) -> None:
+    """Forward-path selection: ALGO_AUTO (fused single-pass 3D kernel for small
+    radii, else two-pass) or ALGO_TWO_PASS (always temporal + spatial pass)."""
+    _check(lib().sfseg_set_algorithm(int(algo)), "sfseg_set_algorithm")
 
 
 def workspace_bytes(shape, C_: int, gauss: Gauss, K: int, want_tape: bool = False):

@@ -19,6 +19,7 @@ constexpr int kTW = 64;         // output columns per spatial-pass strip
 constexpr int kM = 32;          // rows per spatial-pass block
 constexpr int kSpassThreads = 128;
 constexpr int kSpassWarps = kSpassThreads / 32;
+constexpr int kSpassPartSlots = 1;    // norm partial slots per CTA
 constexpr int kRingStride = kTW + 4;  // ring row stride in floats (== 4 mod 32: conflict-free)
 constexpr int kMaxC = 64;       // channels passed by value in kernel parameters
 constexpr int kScal = 8;        // doubles of per-volume scalars

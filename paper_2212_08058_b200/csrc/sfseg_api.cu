@@ -35,6 +35,10 @@ namespace {
     }                                                                   \
   } while (0)
 
+// Process-wide forward-path selection (sfseg_set_algorithm): auto / force the
+// two-pass tpass+spass iteration (tests compare both paths on small radii).
+int g_algorithm = SFSEG_ALGO_AUTO;
+
 cudaError_t& last_cuda_error() {
   static thread_local cudaError_t e = cudaSuccess;
   return e;
@@ -118,12 +122,13 @@ PFN_encodeTiled get_encode() {
   return fn;
 }
 
-bool make_volume_tmap(CUtensorMap* map, const float* base, int64_t W, int64_t H, int64_t BT, int64_t Wp, int boxw) {
+bool make_volume_tmap(CUtensorMap* map, const float* base, int64_t W, int64_t H, int64_t BT, int64_t Wp, int boxw,
+                      int boxh = kM) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)BT};
   cuuint64_t strides[2] = {(cuuint64_t)(Wp * 4), (cuuint64_t)(H * Wp * 4)};
-  cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)kM, 1u};
+  cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)boxh, 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -169,7 +174,7 @@ Profiler& prof() {
   static Profiler p;
   return p;
 }
-enum ProfCat { PC_TPASS = 0, PC_SPASS = 1, PC_ONCE = 2, PC_BWD = 3, PC_N = 4 };
+enum ProfCat { PC_TPASS = 0, PC_SPASS = 1, PC_ONCE = 2, PC_BWD = 3, PC_F3D = 4, PC_N = 5 };
 
 // RAII scope that brackets a launch with events when profiling is on.
 struct ProfScope {
@@ -215,6 +220,10 @@ struct Plan {
   int64_t U;          // spass block units
   int G;              // spass grid
   int gx;             // elementwise grid.x per frame
+  bool f3d;           // single-pass fused 3D kernel (small radii) for the single-GPU forward
+  int TX, TY;         // f3d tiles per frame (64 columns x f3d_th(RS) rows)
+  int64_t U3;         // f3d units = B * TY * TX * T
+  int G3;             // f3d grid
   // workspace offsets
   size_t off_sc, off_part, off_out, off_F, off_p, off_v, off_xbar, off_Fbar, off_x0p, ws_fwd, ws_bwd;
   size_t n_part;
@@ -250,8 +259,14 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   const int64_t cap = (int64_t)num_sms() * spass_occupancy(P->RS);
   P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 4));
   P->gx = ew_gx(P->H, P->BT);
+  P->f3d = g_algorithm != SFSEG_ALGO_TWO_PASS && f3d_supported(P->RT, P->RS);
+  P->TX = (int)((sh.W + kF3dTW - 1) / kF3dTW);
+  P->TY = (int)((sh.H + f3d_th(std::min(P->RS, kF3dMaxR)) - 1) / f3d_th(std::min(P->RS, kF3dMaxR)));
+  P->U3 = P->B * P->TY * P->TX * P->T;
+  P->G3 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * f3d_occupancy(P->RT, P->RS), P->U3 / 4));
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
-  size_t n_part = std::max<size_t>(2 * (size_t)P->B * P->G * kCW, (size_t)P->BT * P->gx);
+  size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max((size_t)P->G * kSpassPartSlots, (size_t)P->G3 * kF3dCW),
+                                   (size_t)P->BT * P->gx);
   n_part = std::max<size_t>(n_part, (size_t)4 * num_sms() * (kMaxC + 1));
   P->n_part = n_part;
   size_t off = align_up(sizeof(WsHeader));
@@ -612,6 +627,12 @@ int32_t sfseg_abi_version(void) { return SFSEG_ABI_VERSION; }
 
 const char* sfseg_last_cuda_error(void) { return cudaGetErrorString(last_cuda_error()); }
 
+sfseg_status sfseg_set_algorithm(int32_t algo) {
+  if (algo != SFSEG_ALGO_AUTO && algo != SFSEG_ALGO_TWO_PASS) return SFSEG_ERR_INVALID_ARGUMENT;
+  g_algorithm = algo;
+  return SFSEG_OK;
+}
+
 void sfseg_max_radii(int32_t* rs, int32_t* rt) {
   if (rs) *rs = kMaxRS;
   if (rt) *rt = kMaxRT;
@@ -693,6 +714,54 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
   cp.F_out = F_out;
   combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
   SF_CUDA(after_launch("combine", st));
+
+  if (P.f3d) {
+    // single-pass fused 3D iteration: p_{k-1} -> p_k ping-pong between the p and v buffers
+    F3dParams fp;
+    std::memset(&fp, 0, sizeof(fp));
+    CUtensorMap map_p, map_v;
+    if (!make_volume_tmap(&map_p, p, P.W, P.H, P.BT, P.Wp, f3d_boxw(P.RS))) return SFSEG_ERR_CUDA;
+    if (!make_volume_tmap(&map_v, v, P.W, P.H, P.BT, P.Wp, f3d_boxw(P.RS))) return SFSEG_ERR_CUDA;
+    if (!make_volume_tmap(&fp.fmap, F, P.W, P.H, P.BT, P.Wp, kF3dTW, f3d_th(P.RS))) return SFSEG_ERR_CUDA;
+    fp.F = F;
+    fp.sc = at<double>(ws, P.off_sc);
+    fp.partials = at<double>(ws, P.off_part);
+    fp.counter = &at<WsHeader>(ws, 0)->counter[0];
+    fp.err = &at<WsHeader>(ws, 0)->err;
+    fp.stats = stats;
+    fp.tape_nu = tape_nu;
+    fp.U = P.U3;
+    fp.B = (int)P.B;
+    fp.T = (int)P.T;
+    fp.H = (int)P.H;
+    fp.W = (int)P.W;
+    fp.Wp = (int)P.Wp;
+    fp.TX = P.TX;
+    fp.TY = P.TY;
+    fp.G = P.G3;
+    fp.K = K;
+    fp.rayleigh = want_rayleigh ? 1 : 0;
+    for (int i = 0; i < 2 * P.RT + 1; ++i) fp.gt[i] = P.gt[i];
+    for (int d = 0; d <= P.RS; ++d) fp.gs[d] = P.gs[P.RS + d];
+    float* last_out = p;
+    for (int k = 1; k <= K; ++k) {
+      const bool odd = (k & 1) != 0;
+      fp.tmap = odd ? map_p : map_v;
+      fp.out = odd ? v : p;
+      fp.tape_u = tape ? tape_u(k - 1) : nullptr;
+      fp.k = k;
+      fp.last = (k == K) ? 1 : 0;
+      ProfScope ps(st, PC_F3D);
+      SF_CUDA(launch_f3d(P.RT, P.RS, fp, P.G3, st));
+      SF_CUDA(after_launch("f3d", st));
+      last_out = fp.out;
+    }
+    dim3 grid((unsigned)P.gx, (unsigned)P.BT);
+    final_scale_kernel<<<grid, kEwThreads, 0, st>>>(last_out, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H,
+                                                    (int)P.W, (int)P.Wp, (int)P.T, 0);
+    SF_CUDA(after_launch("final_scale", st));
+    return SFSEG_OK;
+  }
 
   SpassParams sp;
   std::memset(&sp, 0, sizeof(sp));

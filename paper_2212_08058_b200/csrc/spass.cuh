@@ -237,9 +237,12 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
 
     // ---------------------------------------------------------------- y-pass + epilogue
     // thread: column quad cq (4 columns), row quad rq (4 rows) of the 32-row block
-    const int cq = lane & 15;
-    const int rq = warp * 2 + (lane >> 4);
-    const int x = sg.s * kTW + 4 * cq;
+    // y-pass: warp w owns the 16 columns its own x-pass produced (w*16 .. w*16+15):
+    // lane -> rows 4rq..4rq+3 x columns 4cq..4cq+3 (conflict-free LDS.128 on the stride-68 ring)
+    const int cq = lane & 3;
+    const int rq = lane >> 2;
+    const int x = sg.s * kTW + 16 * warp + 4 * cq;
+    const bool wlive = sg.s * kTW + 16 * warp < W;  // warp-uniform: ragged last strip
     const bool xok = x < W;
     const bool xfull = x + 4 <= W;
     const float4 msk = make_float4(1.f, (x + 1 < W) ? 1.f : 0.f, (x + 2 < W) ? 1.f : 0.f, (x + 3 < W) ? 1.f : 0.f);
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
       }
     };
     auto ypass = [&](int m, const Pre& pr) {
-      const float* wb = ring + ((m % NSLOT) * kM + OFF + 4 * rq) * kRingStride + 4 * cq;
+      const float* wb = ring + ((m % NSLOT) * kM + OFF + 4 * rq) * kRingStride + 16 * warp + 4 * cq;
       float4 a[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
     };
 
     for (int n = 0; n < nxb; ++n) {
-      const bool do_y = n >= PRO;
+      const bool do_y = wlive && n >= PRO;
       Pre pre;
       if (do_y) prefetch(n - PRO, pre);
       const int row0 = gs + n * kM;
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
       const int sl = n % NSLOT;
       float* r0 = ring + (sl * kM + lane) * kRingStride;
       float* r1 = r0 + RING_ROWS * kRingStride;
-      if (live) {
+      if (live && wlive) {
         const int st = (NST == 2) ? (cseq & 1) : 0;
         mbar_wait(&bars[st], (NST == 2) ? ((cseq >> 1) & 1) : (cseq & 1));
         // ------------------------------------------------------------ x-pass of block n
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
           *reinterpret_cast<float4*>(r0 + Geo::XO * warp + 4 * q) = v;
           *reinterpret_cast<float4*>(r1 + Geo::XO * warp + 4 * q) = v;
         }
-      } else {
+      } else if (wlive) {
         // block entirely in the zero padding above row 0 or below row H-1
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll

@@ -104,6 +104,36 @@ def test_probe_small_radius(sf):
     _check_forward(sf, wl.ch, wl.w, 0.5, 1.0, 1, 3, 15)
 
 
+@pytest.mark.parametrize("case", ["c1", "probe", "edge"])
+def test_two_pass_path_small_radius(sf, case):
+    """Small radii run the fused single-pass 3D kernel by default; the two-pass
+    (temporal + spatial) path must give the same result against the oracle."""
+    sf.set_algorithm(sf.ALGO_TWO_PASS)
+    try:
+        if case == "c1":
+            wl = WL.generate("c1")
+            c = wl.cfg
+            _check_forward(sf, wl.ch, wl.w, c.sigma_t, c.sigma_s, c.radius_t, c.radius_s, c.K)
+        elif case == "probe":
+            cfg = WL.get_config("c2", T=10, H=64, W=140)
+            wl = WL.generate("c2", cfg=cfg)
+            _check_forward(sf, wl.ch, wl.w, 0.5, 1.0, 1, 3, 15)
+        else:
+            rng = np.random.default_rng(11)
+            ch = (rng.random((2, 1, 7, 45, 150)) * 0.8 + 0.1).astype(np.float32)
+            _check_forward(sf, ch, [1.0], 1.0, 2.0, 3, 6, 4)
+    finally:
+        sf.set_algorithm(sf.ALGO_AUTO)
+
+
+def test_fused_probe_ragged_tiles_and_runs(sf):
+    """Fused path: tiles ragged in x and y (W=300, H=61 with 24-row tiles), T long
+    enough that CTA ranges split a tile's frames into several runs."""
+    cfg = WL.get_config("c2", T=37, H=61, W=300)
+    wl = WL.generate("c2", cfg=cfg)
+    _check_forward(sf, wl.ch, wl.w, 0.5, 1.0, 1, 3, 7)
+
+
 @pytest.mark.parametrize("shape,radii", [
     ((1, 1, 1, 1), (0, 1)),          # single voxel: y = F^2 x
     ((1, 1, 5, 7), (2, 3)),          # T = 1 (temporal radius > T)
