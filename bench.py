@@ -271,7 +271,29 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     tp_bytes = 8.0 * B * T * H * W
     f3_ms, f3_n = prof["f3d"]
-    if f3_n:
+    mk_ms, mk_n = prof["mk"]
+    if mk_n:
+        # large radii: ONE persistent launch runs all K iterations (temporal + spatial work
+        # items): FP32-FMA-bound.  Algorithmic flops per launch = K * voxels * 2 *
+        # (x taps + y taps + t taps + 3 epilogue FMAs)
+        mk_avg_s = mk_ms / mk_n / 1e3
+        mk_flops = 2.0 * K * vox * (2 * (2 * r_s + 1) + (2 * r_t + 1) + 3)
+        mk_traffic = None
+        try:
+            mk_traffic = json.load(open(tfile)).get(args.config, {}).get("mk", {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        roofline = {
+            "kernel": f"mk_kernel<R={r_s}, RT={r_t}> (all {K} iterations: temporal + fused spatial work items)",
+            "bound": "alu", "achieved": mk_flops / mk_avg_s / 1e12, "peak": alu_peak_tflops, "unit": "TFLOP/s",
+            "frac": mk_flops / mk_avg_s / 1e12 / alu_peak_tflops, "traffic": mk_traffic,
+            "peak_source": f"derived: {SM_COUNT} SM x {ALU_PEAK_FMA_PER_CLK_PER_SM} FP32 FMA/clk x 2 x "
+                           f"{sm_max:.0f} MHz ({peaks_src} sm_max_mhz)",
+            "algorithmic_flops_per_launch": mk_flops, "launch_ms": mk_avg_s * 1e3, "launches": mk_n,
+            "share_of_step": mk_ms / ms if ms > 0 else None,
+            "path_hbm_frac_algorithmic_12B": 12.0 * value / world / 1e9 / hbm_peak,
+        }
+    elif f3_n:
         # small radii: the fused single-pass 3D kernel is the whole iteration (HBM-bound):
         # algorithmic bytes = read p_{k-1} + read F + write p_k = 12 B per voxel
         f3_avg_s = f3_ms / f3_n / 1e3
@@ -307,7 +329,7 @@ def run_ours(args):
         }
     # our kernels launched in the timed region: the passes (counted by the library's
     # event instrumentation) + combine, final scale, frame max and threshold per step
-    n_launch = int(sp_n + tp_n + f3_n + 4 * args.steps)
+    n_launch = int(sp_n + tp_n + f3_n + 2 * mk_n + 4 * args.steps)   # mk: + its finalize kernel
 
     # ---------------------------------------------------------------- e2e through the C ABI with host buffers
     e2e = None

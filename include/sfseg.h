@@ -165,21 +165,28 @@ sfseg_status sfseg_solve_host(const float* ch_host, int32_t C, const float* w_ho
  * When enabled, every pass launch is bracketed by CUDA events recorded on the
  * launching stream.  sfseg_profile_read syncs those events and returns, per
  * category [0]=temporal pass, [1]=spatial pass, [2]=once-per-solve kernels,
- * [3]=backward passes, [4]=fused single-pass 3D iteration (small radii), the
- * summed milliseconds and launch counts, then resets. */
+ * [3]=backward passes, [4]=fused single-pass 3D iteration (small radii),
+ * [5]=persistent all-iterations megakernel (large radii), the summed
+ * milliseconds and launch counts, then resets. */
 sfseg_status sfseg_profile_enable(int32_t on);
-sfseg_status sfseg_profile_read(double* ms_host /*[5]*/, int64_t* count_host /*[5]*/);
+sfseg_status sfseg_profile_read(double* ms_host /*[6]*/, int64_t* count_host /*[6]*/);
 
 /* ---- forward-path selection (process-wide tuning knob) ----
  * SFSEG_ALGO_AUTO: the single-GPU forward uses the fused single-pass 3D kernel
  * (one HBM read of p_{k-1} and F, one write of p_k per voxel-iteration) when the
  * compiled radii allow it (r_t <= 3, r_s <= 8; PAPER.md:319's 3x7x7 support is
- * such a case), otherwise the temporal pass + fused spatial pass.
- * SFSEG_ALGO_TWO_PASS: always the two-pass iteration.  Both compute the same
- * operator (Eq.7 with p = 1) up to fp32 rounding order.  Not thread-safe
- * against concurrent solves; set it once, before solving. */
+ * such a case), otherwise one temporal pass + one fused spatial pass per
+ * iteration.
+ * SFSEG_ALGO_TWO_PASS: always the two-pass iteration.
+ * SFSEG_ALGO_MEGAKERNEL: for (r_s, r_t) in {(24,6), (18,5), (36,9)} without a
+ * tape, all K iterations as one persistent wavefront kernel (temporal and
+ * spatial work items overlapped, lagged normalisation); else as AUTO.  Measured
+ * on par with the two-pass path at config 2, hence not the default.
+ * All compute the same operator (Eq.7 with p = 1) up to fp32 rounding order.
+ * Not thread-safe against concurrent solves; set it once, before solving. */
 #define SFSEG_ALGO_AUTO 0
 #define SFSEG_ALGO_TWO_PASS 1
+#define SFSEG_ALGO_MEGAKERNEL 2
 sfseg_status sfseg_set_algorithm(int32_t algo);
 
 /* ---- multi-GPU communicator (NCCL, loaded at run time with dlopen) ---- */

@@ -155,20 +155,22 @@ def profile_enable(on: bool = True) -> None:
 
 def profile_read():
     """Sync the recorded events; returns {category: (total_ms, launches)} and resets."""
-    ms = (C.c_double * 5)()
-    n = (C.c_int64 * 5)()
+    ms = (C.c_double * 6)()
+    n = (C.c_int64 * 6)()
     _check(lib().sfseg_profile_read(ms, n), "sfseg_profile_read")
-    names = ("tpass", "spass", "once", "backward", "f3d")
-    return {names[i]: (ms[i], n[i]) for i in range(5)}
+    names = ("tpass", "spass", "once", "backward", "f3d", "mk")
+    return {names[i]: (ms[i], n[i]) for i in range(6)}
 
 
 ALGO_AUTO = 0
 ALGO_TWO_PASS = 1
+ALGO_MEGAKERNEL = 2
 
 
 def set_algorithm(algo: int) -> None:
     """Forward-path selection: ALGO_AUTO (fused single-pass 3D kernel for small
-    radii, else two-pass) or ALGO_TWO_PASS (always temporal + spatial pass)."""
+    radii, else two-pass), ALGO_TWO_PASS (always temporal + spatial pass) or
+    ALGO_MEGAKERNEL (all iterations in one persistent launch, large radii)."""
     _check(lib().sfseg_set_algorithm(int(algo)), "sfseg_set_algorithm")
 
 

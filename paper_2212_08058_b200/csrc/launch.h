@@ -6,6 +6,7 @@
 #include "spass.cuh"
 #include "tpass.cuh"
 #include "f3d.cuh"
+#include "mk.cuh"
 
 namespace sfseg {
 cudaError_t launch_spass_fwd(int R, const SpassParams& P, int grid, cudaStream_t st);
@@ -15,4 +16,6 @@ cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t s
 bool f3d_supported(int RT, int R);
 int f3d_occupancy(int RT, int R);
 cudaError_t launch_f3d(int RT, int R, const F3dParams& P, int grid, cudaStream_t st);
+bool mk_supported(int RT, int R);
+cudaError_t launch_mk(int RT, int R, const MkParams& P, int* grid_out, cudaStream_t st, bool launch);
 }  // namespace sfseg

@@ -174,7 +174,7 @@ Profiler& prof() {
   static Profiler p;
   return p;
 }
-enum ProfCat { PC_TPASS = 0, PC_SPASS = 1, PC_ONCE = 2, PC_BWD = 3, PC_F3D = 4, PC_N = 5 };
+enum ProfCat { PC_TPASS = 0, PC_SPASS = 1, PC_ONCE = 2, PC_BWD = 3, PC_F3D = 4, PC_MK = 5, PC_N = 6 };
 
 // RAII scope that brackets a launch with events when profiling is on.
 struct ProfScope {
@@ -224,8 +224,11 @@ struct Plan {
   int TX, TY;         // f3d tiles per frame (64 columns x f3d_th(RS) rows)
   int64_t U3;         // f3d units = B * TY * TX * T
   int G3;             // f3d grid
+  bool mk;            // persistent wavefront megakernel for the forward (large radii, no tape)
+  int NF, NFC, NCC, NCOLS;  // megakernel T-item geometry
   // workspace offsets
-  size_t off_sc, off_part, off_out, off_F, off_p, off_v, off_xbar, off_Fbar, off_x0p, ws_fwd, ws_bwd;
+  size_t off_sc, off_part, off_out, off_F, off_p, off_v, off_p2, off_mk, off_xbar, off_Fbar, off_x0p, ws_fwd, ws_bwd;
+  size_t mk_part, mk_nu, mk_ctr, mk_ctr_bytes;  // offsets inside the megakernel region
   size_t n_part;
   size_t tape_nu_bytes, tape_bytes;
 };
@@ -264,6 +267,11 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->TY = (int)((sh.H + f3d_th(std::min(P->RS, kF3dMaxR)) - 1) / f3d_th(std::min(P->RS, kF3dMaxR)));
   P->U3 = P->B * P->TY * P->TX * P->T;
   P->G3 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * f3d_occupancy(P->RT, P->RS), P->U3 / 4));
+  P->mk = g_algorithm == SFSEG_ALGO_MEGAKERNEL && !P->f3d && mk_supported(P->RT, P->RS);
+  P->NF = (int)std::min<int64_t>(P->T, mk_nf(P->RT));
+  P->NFC = (int)((P->T + P->NF - 1) / P->NF);
+  P->NCOLS = 4;
+  P->NCC = (int)((P->H * P->Wp / 4 + 128 * P->NCOLS - 1) / (128 * P->NCOLS));
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
   size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max((size_t)P->G * kSpassPartSlots, (size_t)P->G3 * kF3dCW),
                                    (size_t)P->BT * P->gx);
@@ -283,6 +291,20 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   off += vb;
   P->off_v = off;
   off += vb;
+  P->off_p2 = off;  // second iterate buffer (megakernel ping-pong)
+  off += vb;
+  P->off_mk = off;
+  {
+    const size_t nk = (size_t)(K + 1) * P->B;
+    P->mk_part = 0;
+    size_t m = align_up(sizeof(double) * nk * (size_t)P->T * P->S * 2);
+    P->mk_nu = m;
+    m += align_up(sizeof(double) * nk * 2);
+    P->mk_ctr = m;
+    P->mk_ctr_bytes = sizeof(unsigned) * (1 + nk * ((size_t)P->NFC + P->T + 2));
+    m += align_up(P->mk_ctr_bytes);
+    off += m;
+  }
   P->ws_fwd = off;
   P->off_xbar = off;
   off += vb;
@@ -628,7 +650,8 @@ int32_t sfseg_abi_version(void) { return SFSEG_ABI_VERSION; }
 const char* sfseg_last_cuda_error(void) { return cudaGetErrorString(last_cuda_error()); }
 
 sfseg_status sfseg_set_algorithm(int32_t algo) {
-  if (algo != SFSEG_ALGO_AUTO && algo != SFSEG_ALGO_TWO_PASS) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (algo != SFSEG_ALGO_AUTO && algo != SFSEG_ALGO_TWO_PASS && algo != SFSEG_ALGO_MEGAKERNEL)
+    return SFSEG_ERR_INVALID_ARGUMENT;
   g_algorithm = algo;
   return SFSEG_OK;
 }
@@ -759,6 +782,80 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     dim3 grid((unsigned)P.gx, (unsigned)P.BT);
     final_scale_kernel<<<grid, kEwThreads, 0, st>>>(last_out, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H,
                                                     (int)P.W, (int)P.Wp, (int)P.T, 0);
+    SF_CUDA(after_launch("final_scale", st));
+    return SFSEG_OK;
+  }
+
+  if (P.mk && !tape) {
+    // all K iterations in one persistent launch (mk.cuh), then the lagged-norm finalize
+    MkParams mp;
+    std::memset(&mp, 0, sizeof(mp));
+    if (!make_volume_tmap(&mp.sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+    fill_spass_common(mp.sp, P, ws);
+    char* mkb = static_cast<char*>(ws) + P.off_mk;
+    mp.pbuf0 = p;
+    mp.pbuf1 = at<float>(ws, P.off_p2);
+    mp.v = v;
+    mp.sc = at<double>(ws, P.off_sc);
+    mp.part = reinterpret_cast<double*>(mkb + P.mk_part);
+    mp.nu = reinterpret_cast<double*>(mkb + P.mk_nu);
+    unsigned* ctr = reinterpret_cast<unsigned*>(mkb + P.mk_ctr);
+    const size_t nk = (size_t)(K + 1) * P.B;
+    mp.ticket = ctr;
+    mp.tdone = ctr + 1;
+    mp.sdone = mp.tdone + nk * P.NFC;
+    mp.sall = mp.sdone + nk * P.T;
+    mp.nready = mp.sall + nk;
+    mp.frame4 = P.H * P.Wp / 4;
+    mp.B = (int)P.B;
+    mp.T = (int)P.T;
+    mp.S = P.S;
+    mp.K = K;
+    mp.NF = P.NF;
+    mp.NFC = P.NFC;
+    mp.NCC = P.NCC;
+    mp.NCOLS = P.NCOLS;
+    mp.rayleigh = want_rayleigh ? 1 : 0;
+    for (int i = 0; i < 2 * P.RT + 1; ++i) mp.gt[i] = P.gt[i];
+    SF_CUDA(cudaMemsetAsync(ctr, 0, P.mk_ctr_bytes, st));
+    // debug: SFSEG_MK_TRACE=<file> records per-item timestamps of this solve (syncs)
+    const char* trace_path = std::getenv("SFSEG_MK_TRACE");
+    const long n_items = (long)K * P.B * ((long)P.NFC * P.NCC + (long)P.T * P.S);
+    if (trace_path && *trace_path) SF_CUDA(cudaMalloc(&mp.trace, sizeof(unsigned long long) * 4 * n_items));
+    int grid = 0;
+    {
+      ProfScope ps(st, PC_MK);
+      SF_CUDA(launch_mk(P.RT, P.RS, mp, &grid, st, true));
+      SF_CUDA(after_launch("mk", st));
+    }
+    if (mp.trace) {
+      std::vector<unsigned long long> h((size_t)4 * n_items);
+      SF_CUDA(cudaMemcpyAsync(h.data(), mp.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+      SF_CUDA(cudaStreamSynchronize(st));
+      cudaFree(mp.trace);
+      mp.trace = nullptr;
+      if (FILE* f = std::fopen(trace_path, "w")) {
+        std::fprintf(f, "# grid=%d NF=%d NFC=%d NCC=%d S=%d T=%d K=%d\nticket,sm,kind,t_grab,t_ready,t_done\n", grid,
+                     P.NF, P.NFC, P.NCC, P.S, (int)P.T, K);
+        for (long i = 0; i < n_items; ++i)
+          std::fprintf(f, "%ld,%llu,%llu,%llu,%llu,%llu\n", i, h[4 * i] >> 8, h[4 * i] & 255ull, h[4 * i + 1],
+                       h[4 * i + 2], h[4 * i + 3]);
+        std::fclose(f);
+      }
+    }
+    MkFinParams fp;
+    fp.nu = mp.nu;
+    fp.sc = at<double>(ws, P.off_sc);
+    fp.stats = stats;
+    fp.err = &at<WsHeader>(ws, 0)->err;
+    fp.B = (int)P.B;
+    fp.K = K;
+    fp.rayleigh = mp.rayleigh;
+    mk_finalize_kernel<<<(unsigned)((P.B + 127) / 128), 128, 0, st>>>(fp);
+    SF_CUDA(after_launch("mk_finalize", st));
+    dim3 grid2((unsigned)P.gx, (unsigned)P.BT);
+    final_scale_kernel<<<grid2, kEwThreads, 0, st>>>((K & 1) ? mp.pbuf1 : mp.pbuf0, x_out, at<double>(ws, P.off_sc),
+                                                     (int)P.T, (int)P.H, (int)P.W, (int)P.Wp, (int)P.T, 0);
     SF_CUDA(after_launch("final_scale", st));
     return SFSEG_OK;
   }

@@ -139,8 +139,16 @@ __device__ __forceinline__ Seg seg_decode(long u, long u_end, int NB, int S) {
   return g;
 }
 
-template <int R, int MODE>
-__global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_constant__ SpassParams P) {
+// One CTA's walk over the block units [u_begin, u_end) (see the header comment).
+// TMA stage parity continues across calls through pseq_io / cseq_io (persistent
+// callers such as the megakernel run many ranges per CTA); every load a call
+// issues is consumed before it returns.  flush_fn(vol, acc0, acc1) receives each
+// thread's fp64 partial sums of ||y||^2 and <p_{k-1}, u> whenever the range
+// leaves a volume (collective: all threads call it).
+template <int R, int MODE, class FlushFn>
+__device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, long u_end, float* stage, float* ring,
+                                          uint64_t* bars, unsigned& pseq_io, unsigned& cseq_io, FlushFn&& flush_fn,
+                                          float* out_, const float* pprev_, float* tape_, int last_) {
   using Geo = SpassGeom<R>;
   constexpr int BOXW = Geo::BOXW;
   constexpr int NSLOT = spass_nslot(R);
@@ -149,33 +157,15 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
   constexpr int OFF = spass_off(R);
   constexpr unsigned STAGE_BYTES = kM * BOXW * sizeof(float);
   constexpr int NST = spass_stages(R);
-
-  extern __shared__ __align__(128) unsigned char smem[];
-  float* stage = reinterpret_cast<float*>(smem);
-  float* ring = stage + NST * kM * BOXW;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * RING_ROWS * kRingStride);
-  double* red = reinterpret_cast<double*>(bars + 2);
-  int* flag = reinterpret_cast<int*>(red + 8);
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = P.H, W = P.W, Wp = P.Wp, S = P.S, T = P.T, NB = P.NB;
-  const long u_begin = (long)blockIdx.x * P.U / P.G;
-  const long u_end = (long)(blockIdx.x + 1) * P.U / P.G;
-
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_barrier_init();
-    prefetch_tmap(&P.tmap);
-  }
-  __syncthreads();
 
   // ---- producer (thread 0): walks the same (segment, x-block) sequence as the
   // consumers and issues a TMA load for every x-block that overlaps rows [0, H).
   long pu = u_begin;
   Seg pseg{};
   int pn = 0, pnx = 0, pgs = 0;
-  unsigned pseq = 0;
+  unsigned pseq = pseq_io;
   auto producer_next = [&]() {
     while (pu < u_end) {
       if (pn == 0) {
@@ -204,19 +194,14 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
   double acc0 = 0.0, acc1 = 0.0;  // per-thread partial sums of the current volume
   int cur_vol = -1;
   auto flush = [&](int vol) {
-    const double s0 = block_sum<kSpassThreads>(acc0, red);
-    const double s1 = block_sum<kSpassThreads>(acc1, red);
-    if (tid == 0) {
-      P.partials[(long)vol * P.G + blockIdx.x] = s0;
-      P.partials[(long)(P.B + vol) * P.G + blockIdx.x] = s1;
-    }
+    flush_fn(vol, acc0, acc1);
     acc0 = acc1 = 0.0;
   };
 
   // per-volume scalars for the backward epilogue (refreshed per volume)
   float cn = 0.f, inv_nu = 0.f, inv_nu_prev = 0.f;
 
-  unsigned cseq = 0;  // consumed TMA loads (stage / parity)
+  unsigned cseq = cseq_io;  // consumed TMA loads (stage / parity)
   long u = u_begin;
   while (u < u_end) {
     const Seg sg = seg_decode(u, u_end, NB, S);
@@ -259,9 +244,9 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
           const long off = ((long)sg.bt * H + y) * Wp + x;
           pr.f[i] = *reinterpret_cast<const float4*>(P.F + off);
           if (MODE == SP_FWD) {
-            if (P.pprev) pr.a[i] = *reinterpret_cast<const float4*>(P.pprev + off);
+            if (pprev_) pr.a[i] = __ldcg(reinterpret_cast<const float4*>(pprev_ + off));
           } else {
-            pr.a[i] = *reinterpret_cast<const float4*>(P.out + off);
+            pr.a[i] = *reinterpret_cast<const float4*>(out_ + off);
             pr.c[i] = *reinterpret_cast<const float4*>(P.u1 + off);
           }
         }
@@ -303,9 +288,9 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
         if (MODE == SP_FWD) {
           const float4 yv = f4_mul(f, uu);
           s0 += f4_dot(yv, yv);
-          if (P.pprev) s1 += f4_dot(pr.a[i], uu);
-          if (P.tape_u) *reinterpret_cast<float4*>(P.tape_u + off) = uu;
-          *reinterpret_cast<float4*>(P.out + off) = P.last ? yv : f4_mul(f, yv);
+          if (pprev_) s1 += f4_dot(pr.a[i], uu);
+          if (tape_) *reinterpret_cast<float4*>(tape_ + off) = uu;
+          *reinterpret_cast<float4*>(out_ + off) = last_ ? yv : f4_mul(f, yv);
         } else {
           const float4 xb = pr.a[i];
           const float4 u1 = pr.c[i];
@@ -325,7 +310,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
           fb.w += yb.w * u1.w + xp.w * uu.w;
           *reinterpret_cast<float4*>(P.Fbar + off) = fb;
           const float4 xn = f4_mul(f, uu);
-          *reinterpret_cast<float4*>(P.out + off) = xn;
+          *reinterpret_cast<float4*>(out_ + off) = xn;
           s0 += f4_dot(xp, xn);
         }
       }
@@ -395,6 +380,44 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
     u += nyb;
   }
   if (cur_vol >= 0) flush(cur_vol);
+  pseq_io = pseq;
+  cseq_io = cseq;
+}
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_constant__ SpassParams P) {
+  using Geo = SpassGeom<R>;
+  constexpr int BOXW = Geo::BOXW;
+  constexpr int RING_ROWS = spass_nslot(R) * kM;
+  constexpr int NST = spass_stages(R);
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* stage = reinterpret_cast<float*>(smem);
+  float* ring = stage + NST * kM * BOXW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * RING_ROWS * kRingStride);
+  double* red = reinterpret_cast<double*>(bars + 2);
+  int* flag = reinterpret_cast<int*>(red + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long u_begin = (long)blockIdx.x * P.U / P.G;
+  const long u_end = (long)(blockIdx.x + 1) * P.U / P.G;
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+    prefetch_tmap(&P.tmap);
+  }
+  __syncthreads();
+  unsigned pseq = 0, cseq = 0;
+  spass_run<R, MODE>(P, u_begin, u_end, stage, ring, bars, pseq, cseq, [&](int vol, double a0, double a1) {
+    const double s0 = block_sum<kSpassThreads>(a0, red);
+    const double s1 = block_sum<kSpassThreads>(a1, red);
+    if (tid == 0) {
+      P.partials[(long)vol * P.G + blockIdx.x] = s0;
+      P.partials[(long)(P.B + vol) * P.G + blockIdx.x] = s1;
+    }
+  }, P.out, P.pprev, P.tape_u, P.last);
 
   // ---------------------------------------------------------------- last CTA: fixed-order fp64 finalize
   if (!last_block_arrive(P.counter, (unsigned)P.G, flag)) return;

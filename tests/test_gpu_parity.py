@@ -104,10 +104,10 @@ def test_probe_small_radius(sf):
     _check_forward(sf, wl.ch, wl.w, 0.5, 1.0, 1, 3, 15)
 
 
-@pytest.mark.parametrize("case", ["c1", "probe", "edge"])
-def test_two_pass_path_small_radius(sf, case):
-    """Small radii run the fused single-pass 3D kernel by default; the two-pass
-    (temporal + spatial) path must give the same result against the oracle."""
+@pytest.mark.parametrize("case", ["c1", "probe", "edge", "c2", "c4"])
+def test_two_pass_path(sf, case):
+    """Small radii run the fused single-pass 3D kernel by default; the two-pass (one
+    temporal + one spatial launch per iteration) path must give the same result."""
     sf.set_algorithm(sf.ALGO_TWO_PASS)
     try:
         if case == "c1":
@@ -118,12 +118,59 @@ def test_two_pass_path_small_radius(sf, case):
             cfg = WL.get_config("c2", T=10, H=64, W=140)
             wl = WL.generate("c2", cfg=cfg)
             _check_forward(sf, wl.ch, wl.w, 0.5, 1.0, 1, 3, 15)
+        elif case == "c2":
+            cfg = WL.get_config("c2", T=16, H=150, W=300)
+            wl = WL.generate("c2", cfg=cfg)
+            _check_forward(sf, wl.ch, wl.w, 2.0, 8.0, 6, 24, 15)
+        elif case == "c4":
+            cfg = WL.get_config("c4", B=3, T=12, H=64, W=96)
+            wl = WL.generate("c4", cfg=cfg)
+            _check_forward(sf, wl.ch, wl.w, 1.5, 6.0, 5, 18, 10)
         else:
             rng = np.random.default_rng(11)
             ch = (rng.random((2, 1, 7, 45, 150)) * 0.8 + 0.1).astype(np.float32)
             _check_forward(sf, ch, [1.0], 1.0, 2.0, 3, 6, 4)
     finally:
         sf.set_algorithm(sf.ALGO_AUTO)
+
+
+@pytest.fixture
+def mega(sf):
+    sf.set_algorithm(sf.ALGO_MEGAKERNEL)
+    yield sf
+    sf.set_algorithm(sf.ALGO_AUTO)
+
+
+def test_megakernel_long_volume_many_chunks(mega):
+    """Megakernel path: many frame chunks (T=45 -> 4 chunks of 14), 2 volumes, ragged
+    strips and blocks, K large enough that the lagged normalisation matters."""
+    rng = np.random.default_rng(5)
+    ch = (rng.random((2, 1, 45, 70, 200)) * 0.7 + 0.05).astype(np.float32)
+    _check_forward(mega, ch, [1.0], 2.0, 8.0, 6, 24, 12)
+
+
+def test_megakernel_tiny_norm_no_underflow(mega):
+    """Lagged normalisation keeps magnitudes bounded even when lambda is tiny
+    (F ~ 1e-3 everywhere: each raw iteration would shrink the iterate ~1e-6)."""
+    rng = np.random.default_rng(6)
+    ch = (rng.random((1, 1, 20, 64, 130)) * 1e-3 + 1e-4).astype(np.float32)
+    _check_forward(mega, ch, [1.0], 2.0, 8.0, 6, 24, 15)
+
+
+@pytest.mark.parametrize("case", ["c3", "c4", "c5"])
+def test_megakernel_recipes(mega, case):
+    if case == "c3":
+        cfg = WL.get_config("c3", T=14, H=100, W=200)
+        wl = WL.generate("c3", cfg=cfg)
+        _check_forward(mega, wl.ch, wl.w, 2.0, 8.0, 6, 24, 15)
+    elif case == "c4":
+        cfg = WL.get_config("c4", B=3, T=12, H=64, W=96)
+        wl = WL.generate("c4", cfg=cfg)
+        _check_forward(mega, wl.ch, wl.w, 1.5, 6.0, 5, 18, 10)
+    else:
+        cfg = WL.get_config("c5", T=24, H=90, W=260)
+        wl = WL.generate("c5", cfg=cfg)
+        _check_forward(mega, wl.ch, wl.w, 3.0, 12.0, 9, 36, 6)
 
 
 def test_fused_probe_ragged_tiles_and_runs(sf):
