@@ -34,7 +34,7 @@ constexpr int kF3dQS = kF3dXO + 4;       // per-warp q row stride (floats): 20 -
 constexpr int kF3dThreads = (kF3dCW + 1) * 32;  // + one TMA producer warp
 constexpr int kF3dMaxRT = 3;
 constexpr int kF3dMaxR = 8;
-constexpr int kF3dNPF = 2;  // frames prefetched beyond the 2RT+1 the current output needs
+constexpr int kF3dNPF = 3;  // frames prefetched beyond the 2RT+1 the current output needs
 
 __host__ __device__ constexpr int f3d_ra(int R) { return (R + 3) / 4 * 4; }
 // box width >= 64 + 2 RA with width == 4 (mod 8): conflict-free x-pass LDS.128 (lane = row)
