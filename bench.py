@@ -189,14 +189,15 @@ def run_ours(args):
         uid = broadcast_unique_id(rank)
         comm = Comm(world, rank, local, uid)
     else:
-        wl = WL.generate(args.config, with_mask=False)
+        # c3 (SFSeg++ ensemble) times forward + backward (dL/dw for the MSE loss, reading A13)
+        wl = WL.generate(args.config, with_mask=(args.config == "c3"))
     B, Cn, T, H, W = wl.ch.shape
     ch_host = torch.from_numpy(wl.ch).pin_memory()
     ch = ch_host.to(dev)
     if slab:
         solver = SlabSolver(comm, (B, T, H, W), cfg.T, t0, Cn, gauss, K, device=dev)
     else:
-        solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev)
+        solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev, want_tape=(args.config == "c3"))
     x = torch.empty((B, T, H, W), dtype=torch.float32, device=dev)
     mask = torch.empty((B, T, H, W), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -204,8 +205,20 @@ def run_ours(args):
     # the per-frame threshold (a9) is frame-local: each rank thresholds its own slab
     thr_solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev) if slab else solver
 
+    train = args.config == "c3" and not slab
+    if train:
+        # loss gradient of reading A13 (harness side, outside the ABI): L = mean (x_K - m_hat)^2
+        m_hat = torch.from_numpy(wl.mask.astype(np.float32)).to(dev)
+        m_hat /= torch.linalg.vector_norm(m_hat.double()).float()
+        nvox = float(x.numel())
+        grad = torch.empty_like(x)
+        last_dw = {}
+
     def step():
         solver.forward(ch, wl.w, wl.b, cfg.act, x_out=x, check=False)
+        if train:
+            torch.sub(x, m_hat, out=grad).mul_(2.0 / nvox)
+            last_dw["dw"], last_dw["db"] = solver.backward(ch, wl.w, grad, wl.b, cfg.act)
         thr_solver.threshold(x, cfg.tau, sf.THR_PER_FRAME_MAX, mask=mask)
 
     for _ in range(max(args.warmup, 0)):
@@ -334,23 +347,35 @@ def run_ours(args):
     # ---------------------------------------------------------------- e2e through the C ABI with host buffers
     e2e = None
     if not args.no_e2e and not slab:
-        d_ch = torch.empty_like(ch)
-        x_host = torch.empty((B, T, H, W), dtype=torch.float32).pin_memory()
-        m_host = torch.empty((B, T, H, W), dtype=torch.uint8).pin_memory()
-        e2e_steps = max(1, min(args.steps, 10))
-        sf.solve_host(ch_host, wl.w, gauss, K, cfg.tau, solver, d_ch, x, mask, x_host, m_host)
+        # end to end over pinned HOST buffers through the public API: HostStream pipelines the
+        # H2D copy of volume i+1 and the D2H copy of volume i-1 under the solve of volume i
+        # (three streams); every step copies its full input in and its x + mask out.
+        x_hosts = [torch.empty((B, T, H, W), dtype=torch.float32).pin_memory() for _ in range(2)]
+        m_hosts = [torch.empty((B, T, H, W), dtype=torch.uint8).pin_memory() for _ in range(2)]
+        e2e_steps = max(2, min(args.steps, 10))
+        hs = sf.HostStream(solver, device=dev)
+        hs.run([ch_host] * 2, wl.w, cfg.tau, x_hosts, m_hosts, wl.b, cfg.act)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            sf.solve_host(ch_host, wl.w, gauss, K, cfg.tau, solver, d_ch, x, mask, x_host, m_host)
+        hs.run([ch_host] * e2e_steps, wl.w, cfg.tau, [x_hosts[i % 2] for i in range(e2e_steps)],
+               [m_hosts[i % 2] for i in range(e2e_steps)], wl.b, cfg.act)
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * units_per_step * e2e_steps / float(dt.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(ch_host.numel() * 4),
-               "d2h_bytes_per_step": int(x_host.numel() * 4 + m_host.numel()),
-               "steps": e2e_steps, "api": "sfseg_solve_host (pinned host in/out)"}
+               "d2h_bytes_per_step": int(x_hosts[0].numel() * 4 + m_hosts[0].numel()),
+               "steps": e2e_steps,
+               "api": "HostStream.run: sfseg_power_iterate + sfseg_threshold per volume, H2D/D2H of pinned "
+                      "host buffers on copy streams overlapped with the previous/next solve"}
+        # the unpipelined single call (sfseg_solve_host: H2D, solve, threshold, D2H, sync) for reference
+        d_ch = torch.empty_like(ch)
+        sf.solve_host(ch_host, wl.w, gauss, K, cfg.tau, solver, d_ch, x, mask, x_hosts[0], m_hosts[0])
+        t0 = time.perf_counter()
+        for _ in range(2):
+            sf.solve_host(ch_host, wl.w, gauss, K, cfg.tau, solver, d_ch, x, mask, x_hosts[0], m_hosts[0])
+        e2e["unpipelined_value"] = units_per_step * 2 / (time.perf_counter() - t0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -371,10 +396,19 @@ def run_ours(args):
                                        if slab else f"dp{world} (one volume per GPU)"),
                        "l2": "inputs > L2 (ch 115 MB + F/p/v 344 MB vs 126 MB L2); no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": n_launch,
+            "gpu_launches": n_launch + (int(prof["backward"][1]) + 2 * args.steps if train else 0),
             "clocks": {k: ck[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
             "clock_samples": ck["samples"],
         }
+        if train:
+            bw_ms, bw_n = prof["backward"]
+            line["step"] = ("forward (K iterations, tape) + MSE loss gradient (torch, harness) + backward "
+                            "dL/dw (sfseg_power_iterate_backward) + threshold; value counts the forward's "
+                            "K voxel-iterations only")
+            line["backward"] = {"pass_ms_per_step": bw_ms / args.steps, "pass_launches": int(bw_n),
+                                "dL_dw": last_dw.get("dw"), "dL_db": last_dw.get("db")}
+            if e2e:
+                e2e["api"] += " -- forward + threshold only"
         print(json.dumps(line), flush=True)
     if slab:
         comm.close()

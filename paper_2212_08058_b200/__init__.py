@@ -328,3 +328,56 @@ def solve_host(ch_host: torch.Tensor, w, gauss: Gauss, K: int, tau: float, solve
         None if x_out_host is None else C.c_void_p(x_out_host.data_ptr()),
         None if mask_out_host is None else C.c_void_p(mask_out_host.data_ptr()),
         _ptr(solver.ws), solver.ws.numel(), _stream(stream)), "sfseg_solve_host")
+
+
+class HostStream:
+    """End-to-end solves of a sequence of volumes held in (pinned) HOST memory,
+    pipelined over three CUDA streams: the host->device copy of volume i+1 and
+    the device->host copy of volume i-1 overlap the solve of volume i
+    (sfseg_power_iterate + sfseg_threshold on the compute stream).  Two device
+    slots (channels, x, mask) alternate; events order the reuse.  All compute
+    is the library's kernels; the copies are cudaMemcpyAsync (torch)."""
+
+    def __init__(self, solver: "Solver", device="cuda"):
+        self.solver = solver
+        self.device = torch.device(device)
+        B, T, H, W = solver.shape
+        self.slots = []
+        for _ in range(2):
+            self.slots.append({
+                "ch": torch.empty((B, solver.C, T, H, W), dtype=torch.float32, device=self.device),
+                "x": torch.empty((B, T, H, W), dtype=torch.float32, device=self.device),
+                "m": torch.empty((B, T, H, W), dtype=torch.uint8, device=self.device),
+                "ev_in": torch.cuda.Event(), "ev_cmp": torch.cuda.Event(), "ev_out": torch.cuda.Event(),
+                "used": False,
+            })
+        self.s_h2d = torch.cuda.Stream(self.device)
+        self.s_d2h = torch.cuda.Stream(self.device)
+
+    def run(self, ch_hosts, w, tau: float, x_hosts, mask_hosts, b: float = 0.0, act: int = ACT_IDENTITY,
+            thr_mode: int = THR_PER_FRAME_MAX) -> None:
+        """Solve len(ch_hosts) volumes; results land in x_hosts[i] / mask_hosts[i]. Syncs."""
+        s_cmp = torch.cuda.current_stream(self.device)
+        for i, chh in enumerate(ch_hosts):
+            sl = self.slots[i % 2]
+            if sl["used"]:
+                self.s_h2d.wait_event(sl["ev_cmp"])   # the solve that read this slot's channels is done
+            with torch.cuda.stream(self.s_h2d):
+                sl["ch"].copy_(chh, non_blocking=True)
+                sl["ev_in"].record(self.s_h2d)
+            s_cmp.wait_event(sl["ev_in"])
+            if sl["used"]:
+                s_cmp.wait_event(sl["ev_out"])       # x / mask of this slot have been copied out
+            self.solver.forward(sl["ch"], w, b, act, x_out=sl["x"], stream=s_cmp, check=False)
+            self.solver.threshold(sl["x"], tau, thr_mode, mask=sl["m"], stream=s_cmp)
+            sl["ev_cmp"].record(s_cmp)
+            self.s_d2h.wait_event(sl["ev_cmp"])
+            with torch.cuda.stream(self.s_d2h):
+                if x_hosts is not None:
+                    x_hosts[i].copy_(sl["x"], non_blocking=True)
+                if mask_hosts is not None:
+                    mask_hosts[i].copy_(sl["m"], non_blocking=True)
+                sl["ev_out"].record(self.s_d2h)
+            sl["used"] = True
+        self.s_d2h.synchronize()
+        self.solver.sync(s_cmp)

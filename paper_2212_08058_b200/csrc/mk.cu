@@ -6,7 +6,7 @@ namespace sfseg {
 namespace {
 template <int R, int RT>
 cudaError_t mk_one(const MkParams& P, int* grid_out, cudaStream_t st, bool launch) {
-  const size_t smem = spass_smem_bytes(R);
+  const size_t smem = mk_smem_bytes(R, RT);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(mk_kernel<R, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

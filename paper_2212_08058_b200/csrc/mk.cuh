@@ -147,6 +147,15 @@ __device__ __forceinline__ void mk_titem(const MkParams& P, const float4* src, f
   }
 }
 
+// dynamic smem: max(S-item stage + ring, T-item input frames) + 256 bytes of scratch at the end
+__host__ __device__ constexpr size_t mk_smem_bytes(int R, int RT) {
+  return (sizeof(float) * ((size_t)spass_stages(R) * kM * spass_boxw(R) + (size_t)spass_ring_alloc(R) * kRingStride) >
+                  (size_t)(mk_nf(RT) + 2 * RT) * kMkThreads * 16
+              ? sizeof(float) * ((size_t)spass_stages(R) * kM * spass_boxw(R) + (size_t)spass_ring_alloc(R) * kRingStride)
+              : (size_t)(mk_nf(RT) + 2 * RT) * kMkThreads * 16) +
+         256;
+}
+
 template <int R, int RT>
 __global__ void __launch_bounds__(kMkThreads, 3) mk_kernel(const __grid_constant__ MkParams P) {
   using Geo = SpassGeom<R>;
@@ -157,12 +166,13 @@ __global__ void __launch_bounds__(kMkThreads, 3) mk_kernel(const __grid_constant
   extern __shared__ __align__(128) unsigned char smem[];
   float* stage = reinterpret_cast<float*>(smem);
   float* ring = stage + NST * kM * BOXW;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * RING_ROWS * kRingStride);
+  // barriers / reduction scratch / ticket words live in the last 256 bytes, past both the
+  // S-item layout and the T-item input frames (which alias the stage + ring)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + mk_smem_bytes(R, RT) - 256);
   double* red = reinterpret_cast<double*>(bars + 2);
   unsigned* sh = reinterpret_cast<unsigned*>(red + 8);  // [0] ticket, [1] next ticket, [2] last flag
   float4* sq = reinterpret_cast<float4*>(smem);         // T-item input frames alias the (idle) S stage + ring
-  static_assert((mk_nf(RT) + 2 * RT) * kMkThreads * 16 <= NST * kM * BOXW * 4 + 2 * RING_ROWS * kRingStride * 4,
-                "T-item inputs fit in the S-item smem");
+
 
   const int tid = threadIdx.x;
   const int B = P.B, T = P.T, S = P.S, K = P.K, NF = P.NF, NFC = P.NFC, NCC = P.NCC;

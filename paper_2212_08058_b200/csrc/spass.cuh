@@ -44,8 +44,16 @@ __host__ __device__ constexpr int spass_off(int R) {
 }
 __host__ __device__ constexpr int spass_pro(int R) { return (spass_off(R) + 2 * R + kM - 1) / kM; }
 __host__ __device__ constexpr int spass_nslot(int R) { return spass_pro(R) + 1; }
+// Ring rows actually addressed: NSLOT*32 rows plus a duplicate of the first
+// (max y-window row + 1 - NSLOT*32) rows, so every y window (4 + 2R rows from
+// slot base + OFF + 4rq) is contiguous.  Duplicating only those rows instead of
+// the whole ring is what lets two TMA stages and 3 CTAs share an SM (R = 24:
+// 152 instead of 192 rows).
+__host__ __device__ constexpr int spass_ring_alloc(int R) {
+  return (spass_nslot(R) - 1) * kM + spass_off(R) + 31 + 2 * R + 1;
+}
 __host__ __device__ constexpr size_t spass_smem_for(int R, int stages) {
-  return sizeof(float) * ((size_t)stages * kM * spass_boxw(R) + 2ull * spass_nslot(R) * kM * kRingStride) + 2 * 8 +
+  return sizeof(float) * ((size_t)stages * kM * spass_boxw(R) + (size_t)spass_ring_alloc(R) * kRingStride) + 2 * 8 +
          8 * 8 + 16;
 }
 constexpr size_t kSmemPerSM = 227 * 1024;
@@ -327,6 +335,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
       const int sl = n % NSLOT;
       float* r0 = ring + (sl * kM + lane) * kRingStride;
       float* r1 = r0 + RING_ROWS * kRingStride;
+      const bool dup = sl * kM + lane < spass_ring_alloc(R) - RING_ROWS;  // row also needed past the wrap
       if (live && wlive) {
         const int st = (NST == 2) ? (cseq & 1) : 0;
         mbar_wait(&bars[st], (NST == 2) ? ((cseq >> 1) & 1) : (cseq & 1));
@@ -355,7 +364,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
         for (int q = 0; q < Geo::XO / 4; ++q) {
           const float4 v = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
           *reinterpret_cast<float4*>(r0 + Geo::XO * warp + 4 * q) = v;
-          *reinterpret_cast<float4*>(r1 + Geo::XO * warp + 4 * q) = v;
+          if (dup) *reinterpret_cast<float4*>(r1 + Geo::XO * warp + 4 * q) = v;
         }
       } else if (wlive) {
         // block entirely in the zero padding above row 0 or below row H-1
@@ -363,7 +372,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
 #pragma unroll
         for (int q = 0; q < Geo::XO / 4; ++q) {
           *reinterpret_cast<float4*>(r0 + Geo::XO * warp + 4 * q) = z;
-          *reinterpret_cast<float4*>(r1 + Geo::XO * warp + 4 * q) = z;
+          if (dup) *reinterpret_cast<float4*>(r1 + Geo::XO * warp + 4 * q) = z;
         }
       }
       __syncthreads();  // stage consumed; ring slot visible
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
   extern __shared__ __align__(128) unsigned char smem[];
   float* stage = reinterpret_cast<float*>(smem);
   float* ring = stage + NST * kM * BOXW;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * RING_ROWS * kRingStride);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + spass_ring_alloc(R) * kRingStride);
   double* red = reinterpret_cast<double*>(bars + 2);
   int* flag = reinterpret_cast<int*>(red + 8);
 
