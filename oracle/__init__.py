@@ -18,9 +18,14 @@ Parity status per function:
   normalize_l2           pinned
   threshold              parity unpinned beyond its definition (SURVEY A12 reading)
   power_iterate_backward pinned (central finite differences, Euler identity)
+  full.full_step / power_iterate_full (Eq.7 with p, alpha and
+                         a pairwise map) pinned (entry-by-entry Eq.2 matrix, SPEC
+                         closed forms S:196-198, reduction to the hot path)
 """
 from .sfseg_oracle import (  # noqa: F401
     ACT_IDENTITY, ACT_SIGMOID, THR_PER_FRAME_MAX, THR_GLOBAL_MAX, THR_ABSOLUTE,
     DegenerateError, gaussian_taps, combine, correlate_axis, gaussian_filter,
     apply_M, normalize_l2, power_iterate, threshold, power_iterate_backward,
 )
+from .full import full_step, combine_full, power_iterate_full  # noqa: F401,E402
+from .dense import dense_M_taylor  # noqa: F401,E402

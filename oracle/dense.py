@@ -38,3 +38,15 @@ def dense_M(F: np.ndarray, g_t, g_y, g_x) -> np.ndarray:
     G = dense_G(T, H, W, g_t, g_y, g_x)
     f = F.ravel()
     return f[:, None] * G * f[None, :]
+
+
+def dense_M_taylor(S: np.ndarray, F: np.ndarray, p: float, alpha: float, g_t, g_y, g_x) -> np.ndarray:
+    """Eq.2 built entry by entry, divided by alpha (the scale of Eq.7):
+    M_ij = s_i^p s_j^p [alpha^-1 - (f_i - f_j)^2] G_ij  for one volume [T][H][W]."""
+    S, F = np.asarray(S, np.float64), np.asarray(F, np.float64)
+    T, H, W = S.shape
+    G = dense_G(T, H, W, g_t, g_y, g_x)
+    u = np.power(S.ravel(), float(p))
+    f = F.ravel()
+    bracket = 1.0 / alpha - (f[:, None] - f[None, :]) ** 2
+    return u[:, None] * u[None, :] * bracket * G
