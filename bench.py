@@ -121,10 +121,16 @@ def cpu_oracle_sample(cfg_name: str, t_crop: int = 0):
         wl = WL.generate(cfg_name, t_range=(0, min(t_crop, cfg.T)))
     else:
         wl = WL.generate(cfg_name)
-    F, _ = O.combine(wl.ch, wl.w, wl.b, cfg.act)
     gt, gs = O.gaussian_taps(cfg.sigma_t, cfg.radius_t), O.gaussian_taps(cfg.sigma_s, cfg.radius_s)
-    t0 = time.perf_counter()
-    O.power_iterate(F, gt, gs, 1)
+    if cfg_name == "c2f":   # full SFSeg operator (f1): three convolutions per iteration
+        e = wl.extra
+        S, U, F = O.combine_full(wl.ch, wl.w, wl.b, 0, e["f_ch"], e["wf"], 0.0, 0, e["p"])
+        t0 = time.perf_counter()
+        O.power_iterate_full(S, U, F, e["alpha"], gt, gs, 1)
+    else:
+        F, _ = O.combine(wl.ch, wl.w, wl.b, cfg.act)
+        t0 = time.perf_counter()
+        O.power_iterate(F, gt, gs, 1)
     dt = time.perf_counter() - t0
     nvox = F.size
     sample = (f"1 of {cfg.K} power iterations (combine excluded) of {cfg_name} "
@@ -138,7 +144,7 @@ def run_reference(args):
         return 0
     import workloads as WL
     cfg = WL.get_config(args.config)
-    t_crop = 16 if args.config in ("c2", "c3", "probe") else 8
+    t_crop = 16 if args.config in ("c2", "c3", "probe", "c2f") else 8
     for _ in range(args.warmup):
         cpu_oracle_sample(args.config, t_crop)
     total_t, total_units = 0.0, 0
@@ -198,6 +204,10 @@ def run_ours(args):
         solver = SlabSolver(comm, (B, T, H, W), cfg.T, t0, Cn, gauss, K, device=dev)
     else:
         solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev, want_tape=(args.config == "c3"))
+    full = args.config == "c2f" and not slab
+    if full:   # the full SFSeg operator replaces the hot-path solve
+        fsolver = sf.FullSolver((B, T, H, W), Cn, 2, gauss, K, device=dev)
+        f_ch = torch.from_numpy(wl.extra["f_ch"]).to(dev)
     x = torch.empty((B, T, H, W), dtype=torch.float32, device=dev)
     mask = torch.empty((B, T, H, W), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -215,6 +225,11 @@ def run_ours(args):
         last_dw = {}
 
     def step():
+        if full:
+            e = wl.extra
+            fsolver.forward(ch, wl.w, f_ch, e["wf"], e["p"], e["alpha"], x_out=x, check=False)
+            thr_solver.threshold(x, cfg.tau, sf.THR_PER_FRAME_MAX, mask=mask)
+            return
         solver.forward(ch, wl.w, wl.b, cfg.act, x_out=x, check=False)
         if train:
             torch.sub(x, m_hat, out=grad).mul_(2.0 / nvox)
@@ -223,7 +238,8 @@ def run_ours(args):
 
     for _ in range(max(args.warmup, 0)):
         step()
-    solver.sync()   # raises on a device-detected error
+    (fsolver.forward(ch, wl.w, f_ch, wl.extra["wf"], wl.extra["p"], wl.extra["alpha"], x_out=x) if full
+     else solver.sync())   # raises on a device-detected error
 
     clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
                           if os.environ.get("CUDA_VISIBLE_DEVICES", "").isdigit() else local)
@@ -268,7 +284,7 @@ def run_ours(args):
     sp_avg_s = sp_ms / max(sp_n, 1) / 1e3
     tp_avg_s = tp_ms / max(tp_n, 1) / 1e3
     r_s, r_t = cfg.radius_s, cfg.radius_t
-    fma_per_vox = 2 * (2 * r_s + 1) + 3            # x taps + y taps + F*u, F*y, y*y
+    fma_per_vox = 2 * (2 * r_s + 1) + (0 if full else 3)   # x taps + y taps (+ F*u, F*y, y*y)
     flops_per_launch = 2.0 * fma_per_vox * vox
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak_tflops = SM_COUNT * ALU_PEAK_FMA_PER_CLK_PER_SM * 2 * sm_max * 1e6 / 1e12
@@ -343,10 +359,12 @@ def run_ours(args):
     # our kernels launched in the timed region: the passes (counted by the library's
     # event instrumentation) + combine, final scale, frame max and threshold per step
     n_launch = int(sp_n + tp_n + f3_n + 2 * mk_n + 4 * args.steps)   # mk: + its finalize kernel
+    if full:
+        n_launch += K * args.steps   # the full operator's per-iteration epilogue kernel
 
     # ---------------------------------------------------------------- e2e through the C ABI with host buffers
     e2e = None
-    if not args.no_e2e and not slab:
+    if not args.no_e2e and not slab and not full:
         # end to end over pinned HOST buffers through the public API: HostStream pipelines the
         # H2D copy of volume i+1 and the D2H copy of volume i-1 under the solve of volume i
         # (three streams); every step copies its full input in and its x + mask out.
@@ -422,7 +440,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "probe"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "probe", "c2f"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

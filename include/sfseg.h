@@ -139,6 +139,30 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
                                           double* dL_db_host, void* ws, size_t ws_bytes,
                                           const sfseg_dist* dist_or_null, void* stream);
 
+/* ---- full SFSeg / SFSeg++ operator ----
+ * The general power iteration of Eq.7 / Eq.10: a unary
+ * map S with exponent p and a pairwise map F with the first-order Taylor
+ * bracket of Eq.2,
+ *   X_crt = S^p [ (alpha^-1 - F^2) G*(S^p X) - G*(F^2 S^p X) + 2 F G*(F S^p X) ],
+ *   X_{k+1} = X_crt / ||X_crt||_2                                   (Eq.8 / Eq.11)
+ * i.e. M_ij = s_i^p s_j^p [alpha^-1 - (f_i - f_j)^2] G_ij.  S and F come from
+ * their own channel stacks by Eq.9 (act as in sfseg_combine_channels);
+ * x_0 = S (Alg.1 line 3) or x0_or_null.  No clamping (reading A18): with S, F in
+ * [0,1] and alpha <= 1 the operator is non-negative.  S^p needs S >= 0 (A19): a
+ * negative S gives NaN, reported as SFSEG_ERR_NONFINITE by sfseg_sync_status.
+ *   s_ch [B][Cs][T][H][W], f_ch [B][Cf][T][H][W]; ws_host / wf_host: Cs / Cf floats (host).
+ *   p > 0, alpha > 0 (finite), else SFSEG_ERR_INVALID_ARGUMENT.
+ *   stats_or_null: DEVICE double [B][K][3] as sfseg_power_iterate (Rayleigh slot = 0).
+ *   ws: >= sfseg_workspace_bytes_full(...), 256-byte aligned.  Asynchronous. */
+sfseg_status sfseg_workspace_bytes_full(sfseg_shape shape, int32_t Cs, int32_t Cf, sfseg_gauss gauss,
+                                        int32_t K, size_t* ws_bytes_host);
+sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float* ws_host, float bs,
+                                      int32_t act_s, const float* f_ch, int32_t Cf,
+                                      const float* wf_host, float bf, int32_t act_f, double p,
+                                      double alpha, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
+                                      const float* x0_or_null, float* x_out, double* stats_or_null,
+                                      void* ws, size_t ws_bytes, void* stream);
+
 /* Hard threshold ("simply obtained by thresholding"): uint8 mask.
  * Mode per sfseg_thr_mode; strict '>' in fp32 against tau*max; a frame (or
  * volume) whose max is <= 0 yields zeros.  ws: >= sfseg_threshold_ws_bytes. */

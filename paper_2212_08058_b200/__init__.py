@@ -89,6 +89,10 @@ _SIGS = {
     "sfseg_profile_enable": (C.c_int, [C.c_int32]),
     "sfseg_profile_read": (C.c_int, [_P, _P]),
     "sfseg_set_algorithm": (C.c_int, [C.c_int32]),
+    "sfseg_workspace_bytes_full": (C.c_int, [Shape, C.c_int32, C.c_int32, GaussC, C.c_int32, _P]),
+    "sfseg_power_iterate_full": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, _P, C.c_int32, _P, C.c_float,
+                                           C.c_int32, C.c_double, C.c_double, Shape, GaussC, C.c_int32, _P, _P,
+                                           _P, _P, C.c_size_t, _P]),
     "sfseg_slabs_workspace_bytes": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
     "sfseg_power_iterate_slabs": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                             C.c_int32, _P, _P, _P, C.c_int32, _P, C.c_size_t, _P]),
@@ -381,3 +385,36 @@ class HostStream:
             sl["used"] = True
         self.s_d2h.synchronize()
         self.solver.sync(s_cmp)
+
+
+class FullSolver:
+    """The full SFSeg / SFSeg++ operator (Eq.7 / Eq.10 with
+    unary exponent p, pairwise map F and alpha) through sfseg_power_iterate_full."""
+
+    def __init__(self, shape, Cs: int, Cf: int, gauss: Gauss, K: int, device="cuda"):
+        self.shape = tuple(int(v) for v in shape)
+        self.Cs, self.Cf, self.gauss, self.K = int(Cs), int(Cf), gauss, int(K)
+        self.device = torch.device(device)
+        n = C.c_size_t(0)
+        _check(lib().sfseg_workspace_bytes_full(Shape(*self.shape), self.Cs, self.Cf, gauss.c(), self.K,
+                                                C.byref(n)), "sfseg_workspace_bytes_full")
+        self.ws_bytes = n.value
+        self.ws = _alloc_bytes(self.ws_bytes, self.device)
+        self.stats = torch.zeros((self.shape[0], self.K, 3), dtype=torch.float64, device=self.device)
+
+    def forward(self, s_ch: torch.Tensor, ws, f_ch: torch.Tensor, wf, p: float, alpha: float,
+                bs: float = 0.0, act_s: int = ACT_IDENTITY, bf: float = 0.0, act_f: int = ACT_IDENTITY,
+                x0=None, x_out: Optional[torch.Tensor] = None, stream=None, check: bool = True) -> torch.Tensor:
+        _require(s_ch, "s_ch", 5)
+        _require(f_ch, "f_ch", 5)
+        if x_out is None:
+            x_out = torch.empty(self.shape, dtype=torch.float32, device=s_ch.device)
+        st = lib().sfseg_power_iterate_full(
+            _ptr(s_ch), self.Cs, _weights(ws, self.Cs), float(bs), int(act_s),
+            _ptr(f_ch), self.Cf, _weights(wf, self.Cf), float(bf), int(act_f), float(p), float(alpha),
+            Shape(*self.shape), self.gauss.c(), self.K, _ptr(x0), _ptr(x_out), _ptr(self.stats),
+            _ptr(self.ws), self.ws_bytes, _stream(stream))
+        _check(st, "sfseg_power_iterate_full")
+        if check:
+            _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate_full (device)")
+        return x_out

@@ -1,0 +1,148 @@
+// Full SFSeg / SFSeg++ operator: the general power
+// iteration of Eq.7 / Eq.10 with a unary map S
+// (exponent p), a pairwise map F and the Taylor bracket of Eq.2:
+//
+//   X_crt = S^p [ (alpha^-1 - F^2) G*(S^p X) - G*(F^2 S^p X) + 2 F G*(F S^p X) ]
+//
+// per iteration: three temporal passes (tpass TP_FWDF: inputs a, F a, F^2 a with
+// a = S^p X carried as the stored iterate and the normaliser folded in), three
+// spatial passes (spass, plain mode: u = G_s v), then this file's epilogue
+// combining the three filtered volumes per voxel (+ norm partials).  Eq.9 gives
+// S and F (combine_full_kernel); x_0 = S (Alg.1 line 3) or a user x0.
+#pragma once
+#include "common.cuh"
+#include "misc.cuh"
+#include "spass.cuh"
+
+namespace sfseg {
+
+struct CombineFullParams {
+  const float* s_ch;    // dense [B][Cs][T][H][W] (unary channels)
+  const float* f_ch;    // dense [B][Cf][T][H][W] (pairwise channels)
+  const float* x0;      // dense [B][T][H][W] or null (x_0 = S)
+  float* U;             // pitched: S^p
+  float* F;             // pitched: pairwise map
+  float* a0;            // pitched: U * x_0
+  double* sc;
+  double* partials;     // [B][T*gx]
+  unsigned* counter;
+  unsigned* err;
+  int B, Cs, Cf, T, H, W, Wp, act_s, act_f, gx;
+  float bs, bf, p;
+  float ws[kMaxC];
+  float wf[kMaxC];
+};
+
+// Eq.9 for both maps, U = S^p (reading A19: 0^p = 0; S < 0 gives NaN -> NONFINITE),
+// a_0 = U x_0, ||x_0||.  Row-parallel like combine_kernel; grid (gx, B*T).
+__global__ void __launch_bounds__(kEwThreads) combine_full_kernel(const __grid_constant__ CombineFullParams P) {
+  __shared__ double red[kEwThreads / 32];
+  __shared__ int flag;
+  const int bt = blockIdx.y;
+  const int b = bt / P.T, t = bt - b * P.T;
+  const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
+  const long vol = (long)P.T * HW;
+  const float* sf = P.s_ch + (long)b * P.Cs * vol + (long)t * HW;
+  const float* ff = P.f_ch + (long)b * P.Cf * vol + (long)t * HW;
+  const long dbase = (long)b * vol + (long)t * HW;
+  double acc = 0.0;
+  for (int y = blockIdx.x; y < P.H; y += P.gx) {
+    for (int x = threadIdx.x; x < P.Wp; x += kEwThreads) {
+      const long po = (long)bt * HWp + (long)y * P.Wp + x;
+      float u = 0.f, f = 0.f, a = 0.f;
+      if (x < P.W) {
+        const long d = (long)y * P.W + x;
+        float zs = P.bs, zf = P.bf;
+        for (int c = 0; c < P.Cs; ++c) zs = fmaf(P.ws[c], __ldg(sf + (long)c * vol + d), zs);
+        for (int c = 0; c < P.Cf; ++c) zf = fmaf(P.wf[c], __ldg(ff + (long)c * vol + d), zf);
+        const float s = (P.act_s == 1) ? 1.f / (1.f + expf(-zs)) : zs;
+        f = (P.act_f == 1) ? 1.f / (1.f + expf(-zf)) : zf;
+        u = (P.p == 1.f) ? s : ((s == 0.f) ? 0.f : powf(s, P.p));
+        const float xv = P.x0 ? __ldg(P.x0 + dbase + d) : s;
+        a = u * xv;
+        acc += (double)xv * (double)xv;
+      }
+      P.U[po] = u;
+      P.F[po] = f;
+      P.a0[po] = a;
+    }
+  }
+  const double s = block_sum<kEwThreads>(acc, red);
+  const long nper = (long)P.T * P.gx;
+  if (threadIdx.x == 0) P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = s;
+  if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
+  for (int bb = 0; bb < P.B; ++bb) {
+    const double tot = block_sum_array<kEwThreads>(P.partials + (long)bb * nper, nper, 1, red);
+    if (threadIdx.x == 0) {
+      const double xn = sqrt(tot);
+      P.sc[bb * kScal + SC_XNORM] = xn;
+      P.sc[bb * kScal + SC_S] = 1.0;
+      flag_norm(P.err, xn);
+    }
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+struct FullEpiParams {
+  const float* ua;      // pitched G * (s a)
+  const float* ub;      // pitched G * (s F^2 a)
+  const float* uc;      // pitched G * (s F a)
+  const float* U;       // S^p
+  const float* F;
+  float* out;           // a_k = U y_k (or y_k when last)
+  double* sc;
+  double* partials;
+  unsigned* counter;
+  unsigned* err;
+  double* stats;
+  int B, T, H, Wp, W, K, k, last, gx;
+  float inv_alpha;
+};
+
+// y_k = U [ (alpha^-1 - F^2) ua - ub + 2 F uc ]  (Eq.7), a_k = U y_k, ||y_k||^2 partials,
+// last block: fwd_finalize (nu_k, gain; the Rayleigh slot is 0 on this path).
+__global__ void __launch_bounds__(kEwThreads) full_epilogue_kernel(const __grid_constant__ FullEpiParams P) {
+  __shared__ double red[kEwThreads / 32];
+  __shared__ int flag;
+  const int bt = blockIdx.y;
+  const int b = bt / P.T, t = bt - b * P.T;
+  const long HWp = (long)P.H * P.Wp;
+  const long W4 = P.Wp / 4;
+  double acc = 0.0;
+  for (int y = blockIdx.x; y < P.H; y += P.gx) {
+    for (long x4 = threadIdx.x; x4 < W4; x4 += kEwThreads) {
+      const long po = (long)bt * HWp + (long)y * P.Wp + 4 * x4;
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(P.ua + po));
+      const float4 bb = __ldcs(reinterpret_cast<const float4*>(P.ub + po));
+      const float4 c = __ldcs(reinterpret_cast<const float4*>(P.uc + po));
+      const float4 u = *reinterpret_cast<const float4*>(P.U + po);
+      const float4 f = *reinterpret_cast<const float4*>(P.F + po);
+      float yv[4], o[4];
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w}, cv[4] = {c.x, c.y, c.z, c.w};
+      const float uv[4] = {u.x, u.y, u.z, u.w}, fv[4] = {f.x, f.y, f.z, f.w};
+      float s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool in = 4 * x4 + i < P.W;
+        const float fi = fv[i];
+        const float val = (P.inv_alpha - fi * fi) * av[i] - bv[i] + 2.f * fi * cv[i];
+        yv[i] = in ? uv[i] * val : 0.f;
+        o[i] = P.last ? yv[i] : uv[i] * yv[i];
+        s2 = fmaf(yv[i], yv[i], s2);
+      }
+      *reinterpret_cast<float4*>(P.out + po) = make_float4(o[0], o[1], o[2], o[3]);
+      acc += (double)s2;
+    }
+  }
+  const double s = block_sum<kEwThreads>(acc, red);
+  const long nper = (long)P.T * P.gx;
+  if (threadIdx.x == 0) P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = s;
+  if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
+  for (int v = 0; v < P.B; ++v) {
+    const double tot = block_sum_array<kEwThreads>(P.partials + (long)v * nper, nper, 1, red);
+    if (threadIdx.x == 0) fwd_finalize(P.sc + v * kScal, P.stats, nullptr, P.err, P.K, P.k, false, v, tot, 0.0);
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+}  // namespace sfseg

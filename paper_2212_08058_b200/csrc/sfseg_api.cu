@@ -20,6 +20,7 @@
 #include "spass.cuh"
 #include "tpass.cuh"
 #include "comm.cuh"
+#include "full.cuh"
 #include "launch.h"
 
 using namespace sfseg;
@@ -1019,6 +1020,169 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
   for (int c = 0; c < C; ++c) dL_dw_host[c] = out[c];
   if (dL_db_host) *dL_db_host = out[C];
   return s;
+}
+
+// ====================================================================== full SFSeg operator
+namespace {
+struct FullLayout {
+  size_t off_U, off_F, off_a, off_v, off_ua, off_ub, off_uc, total;
+};
+FullLayout full_layout(const Plan& P) {
+  FullLayout L;
+  const size_t vb = align_up(sizeof(float) * (size_t)P.vol_elems);
+  size_t off = P.off_F;  // header, scalars, partials and the reduction output block as in the hot path
+  L.off_U = off;
+  off += vb;
+  L.off_F = off;
+  off += vb;
+  L.off_a = off;
+  off += vb;
+  L.off_v = off;
+  off += vb;
+  L.off_ua = off;
+  off += vb;
+  L.off_ub = off;
+  off += vb;
+  L.off_uc = off;
+  off += vb;
+  L.total = off;
+  return L;
+}
+sfseg_status full_check(int32_t Cs, int32_t Cf, double p, double alpha) {
+  if (Cs < 1 || Cf < 1) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (Cs > kMaxC || Cf > kMaxC) return SFSEG_ERR_UNSUPPORTED;
+  if (!(p > 0.0) || !std::isfinite(p) || !(alpha > 0.0) || !std::isfinite(alpha)) return SFSEG_ERR_INVALID_ARGUMENT;
+  return SFSEG_OK;
+}
+}  // namespace
+
+sfseg_status sfseg_workspace_bytes_full(sfseg_shape sh, int32_t Cs, int32_t Cf, sfseg_gauss gauss, int32_t K,
+                                        size_t* ws_bytes_host) {
+  if (!ws_bytes_host) return SFSEG_ERR_INVALID_ARGUMENT;
+  sfseg_status s = full_check(Cs, Cf, 1.0, 1.0);
+  if (s != SFSEG_OK) return s;
+  Plan P;
+  if ((s = make_plan(sh, std::max(Cs, Cf), gauss, K, &P)) != SFSEG_OK) return s;
+  *ws_bytes_host = full_layout(P).total;
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float* ws_host, float bs, int32_t act_s,
+                                      const float* f_ch, int32_t Cf, const float* wf_host, float bf, int32_t act_f,
+                                      double p, double alpha, sfseg_shape sh, sfseg_gauss gauss, int32_t K,
+                                      const float* x0, float* x_out, double* stats, void* ws, size_t ws_bytes,
+                                      void* stream) {
+  if (!s_ch || !f_ch || !ws_host || !wf_host || !x_out || !validate_act(act_s) || !validate_act(act_f))
+    return SFSEG_ERR_INVALID_ARGUMENT;
+  sfseg_status s = full_check(Cs, Cf, p, alpha);
+  if (s != SFSEG_OK) return s;
+  Plan P;
+  if ((s = make_plan(sh, std::max(Cs, Cf), gauss, K, &P)) != SFSEG_OK) return s;
+  if (!finite_weights(ws_host, Cs, bs) || !finite_weights(wf_host, Cf, bf)) return SFSEG_ERR_INVALID_ARGUMENT;
+  const FullLayout L = full_layout(P);
+  if ((s = check_ws(ws, ws_bytes, L.total)) != SFSEG_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SF_CUDA(cudaMemsetAsync(ws, 0, P.off_part, st));
+  float* U = at<float>(ws, L.off_U);
+  float* F = at<float>(ws, L.off_F);
+  float* a = at<float>(ws, L.off_a);
+  float* v = at<float>(ws, L.off_v);
+  float* uo[3] = {at<float>(ws, L.off_ua), at<float>(ws, L.off_ub), at<float>(ws, L.off_uc)};
+
+  // Eq.9 for S and F, U = S^p, a_0 = U x_0, ||x_0||
+  CombineFullParams cp;
+  std::memset(&cp, 0, sizeof(cp));
+  cp.s_ch = s_ch;
+  cp.f_ch = f_ch;
+  cp.x0 = x0;
+  cp.U = U;
+  cp.F = F;
+  cp.a0 = a;
+  cp.sc = at<double>(ws, P.off_sc);
+  cp.partials = at<double>(ws, P.off_part);
+  cp.counter = &at<WsHeader>(ws, 0)->counter[1];
+  cp.err = &at<WsHeader>(ws, 0)->err;
+  cp.B = (int)P.B;
+  cp.Cs = Cs;
+  cp.Cf = Cf;
+  cp.T = (int)P.T;
+  cp.H = (int)P.H;
+  cp.W = (int)P.W;
+  cp.Wp = (int)P.Wp;
+  cp.act_s = act_s;
+  cp.act_f = act_f;
+  cp.gx = P.gx;
+  cp.bs = bs;
+  cp.bf = bf;
+  cp.p = (float)p;
+  for (int c = 0; c < Cs; ++c) cp.ws[c] = ws_host[c];
+  for (int c = 0; c < Cf; ++c) cp.wf[c] = wf_host[c];
+  combine_full_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
+  SF_CUDA(after_launch("combine_full", st));
+
+  SpassParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  if (!make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+  fill_spass_common(sp, P, ws);
+  sp.plain = 1;
+  TpassParams tp;
+  std::memset(&tp, 0, sizeof(tp));
+  fill_tpass_common(tp, P, ws);
+  tp.src = a;
+  tp.F = F;
+  tp.out = v;
+  FullEpiParams ep;
+  std::memset(&ep, 0, sizeof(ep));
+  ep.ua = uo[0];
+  ep.ub = uo[1];
+  ep.uc = uo[2];
+  ep.U = U;
+  ep.F = F;
+  ep.out = a;
+  ep.sc = at<double>(ws, P.off_sc);
+  ep.partials = at<double>(ws, P.off_part);
+  ep.counter = &at<WsHeader>(ws, 0)->counter[1];
+  ep.err = &at<WsHeader>(ws, 0)->err;
+  ep.stats = stats;
+  ep.B = (int)P.B;
+  ep.T = (int)P.T;
+  ep.H = (int)P.H;
+  ep.Wp = (int)P.Wp;
+  ep.W = (int)P.W;
+  ep.K = K;
+  ep.gx = P.gx;
+  ep.inv_alpha = (float)(1.0 / alpha);
+  const int fexp[3] = {0, 2, 1};  // G*(S^p X), G*(F^2 S^p X), G*(F S^p X)
+  for (int k = 1; k <= K; ++k) {
+    for (int c = 0; c < 3; ++c) {
+      {
+        ProfScope ps(st, PC_TPASS);
+        if (fexp[c] == 0) {
+          SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
+        } else {
+          tp.fexp = fexp[c];
+          SF_CUDA(launch_tpass_fwdf(P.RT, tp, (int)P.B, st));
+        }
+        SF_CUDA(after_launch("tpass_full", st));
+      }
+      sp.out = uo[c];
+      sp.k = k;
+      {
+        ProfScope ps(st, PC_SPASS);
+        SF_CUDA(launch_spass_fwd(P.RS, sp, P.G, st));
+        SF_CUDA(after_launch("spass_plain", st));
+      }
+    }
+    ep.k = k;
+    ep.last = (k == K) ? 1 : 0;
+    full_epilogue_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ep);
+    SF_CUDA(after_launch("full_epilogue", st));
+  }
+  dim3 grid((unsigned)P.gx, (unsigned)P.BT);
+  final_scale_kernel<<<grid, kEwThreads, 0, st>>>(a, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H, (int)P.W,
+                                                  (int)P.Wp, (int)P.T, 0);
+  SF_CUDA(after_launch("final_scale", st));
+  return SFSEG_OK;
 }
 
 size_t sfseg_threshold_ws_bytes(sfseg_shape sh) {

@@ -89,6 +89,7 @@ struct SpassParams {
   int B, T, H, W, Wp, S, NB, G;
   int K, k;                // iteration (FWD) or backward step (BWD), 1-based
   int last;                // FWD: write y instead of p
+  int plain;               // FWD: write u = G_s v only (no F multiplies, no norm; full-operator path)
   float g[kMaxRS + 1];     // g[d] = weight of spatial offset +-d (same taps for y and x)
 };
 
@@ -248,7 +249,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
       for (int i = 0; i < 4; ++i) {
         const int y = (sg.yb0 + m) * kM + 4 * rq + i;
         pr.f[i] = pr.a[i] = pr.c[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (xok && y < yend) {
+        if (xok && y < yend && !P.plain) {
           const long off = ((long)sg.bt * H + y) * Wp + x;
           pr.f[i] = *reinterpret_cast<const float4*>(P.F + off);
           if (MODE == SP_FWD) {
@@ -293,7 +294,9 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
           f = f4_mul(f, msk);
           uu = f4_mul(uu, msk);
         }
-        if (MODE == SP_FWD) {
+        if (MODE == SP_FWD && P.plain) {
+          *reinterpret_cast<float4*>(out_ + off) = uu;
+        } else if (MODE == SP_FWD) {
           const float4 yv = f4_mul(f, uu);
           s0 += f4_dot(yv, yv);
           if (pprev_) s1 += f4_dot(pr.a[i], uu);
@@ -428,6 +431,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
     }
   }, P.out, P.pprev, P.tape_u, P.last);
 
+  if (P.plain) return;  // no norm in the plain (full-operator) mode
   // ---------------------------------------------------------------- last CTA: fixed-order fp64 finalize
   if (!last_block_arrive(P.counter, (unsigned)P.G, flag)) return;
   const long per_vol = P.U / P.B;  // units per volume

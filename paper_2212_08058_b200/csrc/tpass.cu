@@ -26,4 +26,7 @@ cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t s
 cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st) {
   return launch_tpass_t<TP_BWD>(RT, P, B, st);
 }
+cudaError_t launch_tpass_fwdf(int RT, const TpassParams& P, int B, cudaStream_t st) {
+  return launch_tpass_t<TP_FWDF>(RT, P, B, st);
+}
 }  // namespace sfseg

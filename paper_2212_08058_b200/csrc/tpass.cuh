@@ -17,11 +17,12 @@ constexpr int kMaxRT = 16;
 enum TpassMode : int {
   TP_FWD = 0,   // src = p (stored iterate), out = s_{k-1} * G_t * p
   TP_BWD = 1,   // src = F * y_bar_k, y_bar_k = (x_bar_k - F u_{k-1} cn) * inv_nu  (Appendix A)
+  TP_FWDF = 2,  // full SFSeg operator (f1): src = F^fexp * a, out = s_{k-1} * G_t * src  (Eq.7's three inputs)
 };
 
 struct TpassParams {
   const float* src;      // FWD: p ; BWD: x_bar_k            pitched [B*T][H][Wp]
-  const float* F;        // BWD
+  const float* F;        // BWD, FWDF
   const float* u1;       // BWD: tape u_{k-1}
   const float* halo_lo;  // [B][RT][H][Wp] frames t = -RT..-1 (time slabs) or null
   const float* halo_hi;  // [B][RT][H][Wp] frames t = T..T+RT-1 or null
@@ -29,6 +30,7 @@ struct TpassParams {
   const double* sc;      // per-volume scalars [B][kScal]
   long frame4;           // H*Wp/4 float4 per frame
   int T;
+  int fexp;              // FWDF: exponent of F multiplying the source (1 or 2)
   float g[2 * kMaxRT + 1];  // g[i] = weight of temporal offset i - RT
 };
 
@@ -38,7 +40,7 @@ constexpr int kTpThreads = 128;
 // float4 columns) 6 x 128 threads per SM hold every column in ONE wave.
 __host__ __device__ constexpr int tpass_min_blocks(int RT) { return RT <= 6 ? 6 : (RT <= 9 ? 4 : 2); }
 // cp.async stages per input stream (frames prefetched ahead of the ring).
-__host__ __device__ constexpr int tpass_stages(int MODE) { return MODE == TP_FWD ? 8 : 4; }
+__host__ __device__ constexpr int tpass_stages(int MODE) { return MODE == TP_FWD ? 8 : (MODE == TP_FWDF ? 6 : 4); }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
@@ -59,7 +61,7 @@ template <int RT, int MODE, bool HALO>
 __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel(const __grid_constant__ TpassParams P) {
   constexpr int NR = 2 * RT + 1;
   constexpr int NS = tpass_stages(MODE);
-  constexpr int NIN = (MODE == TP_FWD) ? 1 : 3;
+  constexpr int NIN = (MODE == TP_FWD) ? 1 : (MODE == TP_FWDF ? 2 : 3);
   __shared__ float4 sq[NS][NIN][kTpThreads];
   const int b = blockIdx.y;
   const int tid = threadIdx.x;
@@ -74,6 +76,9 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   float cn = 0.f, inv_nu = 0.f, scale = 1.f;
   if (MODE == TP_FWD) {
     scale = (float)P.sc[b * kScal + SC_S];
+  } else if (MODE == TP_FWDF) {
+    scale = (float)P.sc[b * kScal + SC_S];
+    Fp = reinterpret_cast<const float4*>(P.F) + b * vol4 + ec;
   } else {
     Fp = reinterpret_cast<const float4*>(P.F) + b * vol4 + ec;
     U1 = reinterpret_cast<const float4*>(P.u1) + b * vol4 + ec;
@@ -115,6 +120,12 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
     float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
     if (MODE == TP_FWD) {
       if (frame_src(jp, 0)) val = sq[sl][0][tid];
+    } else if (MODE == TP_FWDF) {
+      if (j >= 0 && j < T) {
+        const float4 a = sq[sl][0][tid], f = sq[sl][1][tid];
+        const float4 fe = (P.fexp == 2) ? f4_mul(f, f) : f;
+        val = f4_mul(fe, a);
+      }
     } else if (j >= 0 && j < T) {
       const float4 xb = sq[sl][0][tid], f = sq[sl][1][tid], u = sq[sl][2][tid];
       val.x = f.x * ((xb.x - f.x * u.x * cn) * inv_nu);

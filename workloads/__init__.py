@@ -83,7 +83,16 @@ CONFIGS = {
                  note="BASELINE configs[4]: long 1080p volume"),
     "probe": Config("probe", 2, 1, 70, 480, 854, 1, 0.5, 1.0, 1, 3, 15,
                     note="supplementary: c2 data with the paper's 3x7x7 support (PAPER.md:319)"),
+    # the full SFSeg operator; S = the c2 soft mask, F = two
+    # optical-flow-magnitude stand-ins (direct / reverse), p = 0.2,
+    # alpha = 1, N_i = 5 iterations
+    "c2f": Config("c2f", 6, 1, 70, 480, 854, 1, 2.0, 8.0, 6, 24, 5,
+                  note="f1: full SFSeg operator on the c2 volume (S = soft mask, F = 2 flow-magnitude maps)"),
 }
+
+# full-operator hyper-parameters of "c2f" (alpha = 1, p = 0.2 semi-supervised)
+FULL_P = 0.2
+FULL_ALPHA = 1.0
 
 
 def get_config(name: str, **overrides) -> Config:
@@ -220,6 +229,22 @@ def generate(name: str, seed: int = 0, t_range: Optional[tuple] = None,
     assert 0 <= t0 <= t1 <= T
     nt = t1 - t0
     recipe = name if name in ("c1", "c2", "c3", "c4", "c5") else "c2"
+    if name == "c2f":
+        # unary map S: the c2 soft mask; pairwise channels F: flow-magnitude stand-ins --
+        # 0.5 (~3 px/frame of a 6 px/frame scale) where the blob union of frames t and
+        # t+1 (direct) / t-1 and t (reverse) moves, background U[0,0.05] + N(0,0.02^2), clip
+        base = generate("c2", seed, t_range, cfg=get_config("c2", T=T, H=H, W=W), with_mask=with_mask)
+        blobs = _video_blobs(seed, 2, H, W, (24.0, 72.0), (2.5, 3.5))
+        f_ch = np.empty((1, 2, nt, H, W), np.float32)
+        for i, t in enumerate(range(t0, t1)):
+            m0 = _blob_mask(blobs, t, H, W)
+            for c, t2 in enumerate((t + 1, t - 1)):
+                moving = m0 | _blob_mask(blobs, t2, H, W)
+                rng = np.random.default_rng([seed, 6, 1 + c, t])
+                bg = rng.random((H, W)) * 0.05
+                f_ch[0, c, i] = np.clip(np.where(moving, 0.5, bg) + rng.normal(0.0, 0.02, (H, W)), 0.0, 1.0)
+        return Workload(cfg, base.ch, base.w, 0.0, base.mask, t0,
+                        {"f_ch": f_ch, "wf": np.array([0.5, 0.5], np.float32), "p": FULL_P, "alpha": FULL_ALPHA})
 
     if recipe == "c1":
         if (T, H, W, C) != (8, 32, 32, 1):
