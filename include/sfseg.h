@@ -153,7 +153,18 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
  *   s_ch [B][Cs][T][H][W], f_ch [B][Cf][T][H][W]; ws_host / wf_host: Cs / Cf floats (host).
  *   p > 0, alpha > 0 (finite), else SFSEG_ERR_INVALID_ARGUMENT.
  *   stats_or_null: DEVICE double [B][K][3] as sfseg_power_iterate (Rayleigh slot = 0).
+ *   bin_or_null: soft-binarisation (Alg.1 STEP 3): after the
+ *     normalisation of every iteration k > n_cont, x_k <- sigma(kappa_k (x_k - theta_k)) with
+ *     theta_k = mean of the positive entries of x_k and kappa_k = kappa0 * growth^(k-n_cont-1)
+ *     (reading A21); the binarised x_k is the next iterate as is, and when
+ *     K > n_cont x_out is the last binarised iterate (values in (0,1), not unit norm; hard
+ *     mask: sfseg_threshold with SFSEG_THR_ABSOLUTE, tau = 0.5).  NULL: no binarisation.
  *   ws: >= sfseg_workspace_bytes_full(...), 256-byte aligned.  Asynchronous. */
+typedef struct {
+  int32_t n_cont;   /* continuous iterations before binarisation starts (>= 0) */
+  float kappa0;     /* steepness of the first binarised iteration (> 0) */
+  float growth;     /* geometric growth of the steepness per iteration (> 0) */
+} sfseg_binarize;
 sfseg_status sfseg_workspace_bytes_full(sfseg_shape shape, int32_t Cs, int32_t Cf, sfseg_gauss gauss,
                                         int32_t K, size_t* ws_bytes_host);
 sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float* ws_host, float bs,
@@ -161,7 +172,8 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
                                       const float* wf_host, float bf, int32_t act_f, double p,
                                       double alpha, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
                                       const float* x0_or_null, float* x_out, double* stats_or_null,
-                                      void* ws, size_t ws_bytes, void* stream);
+                                      const sfseg_binarize* bin_or_null, void* ws, size_t ws_bytes,
+                                      void* stream);
 
 /* Hard threshold ("simply obtained by thresholding"): uint8 mask.
  * Mode per sfseg_thr_mode; strict '>' in fp32 against tau*max; a frame (or

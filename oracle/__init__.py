@@ -27,5 +27,6 @@ from .sfseg_oracle import (  # noqa: F401
     DegenerateError, gaussian_taps, combine, correlate_axis, gaussian_filter,
     apply_M, normalize_l2, power_iterate, threshold, power_iterate_backward,
 )
-from .full import full_step, combine_full, power_iterate_full  # noqa: F401,E402
+from .full import full_step, combine_full, power_iterate_full, soft_binarize  # noqa: F401,E402
 from .dense import dense_M_taylor  # noqa: F401,E402
+from .online import window_starts, power_iterate_online  # noqa: F401,E402

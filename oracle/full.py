@@ -50,9 +50,26 @@ def combine_full(s_ch, ws, bs, act_s, f_ch, wf, bf, act_f, p: float):
     return S, U, F
 
 
-def power_iterate_full(S: np.ndarray, U: np.ndarray, F: np.ndarray, alpha: float, g_t, g_s, K: int, x0=None):
+def soft_binarize(x: np.ndarray, kappa: float) -> np.ndarray:
+    """Alg.1 STEP 3: X_m <- sigma(X_m), "a sigmoid function (controlled by a
+    parameter)".  Reading A21: sigma(kappa (x - theta)) with
+    theta = mean of the strictly positive entries of x (0 if there are none)."""
+    x = np.asarray(x, np.float64)
+    pos = x[x > 0]
+    theta = float(pos.mean()) if pos.size else 0.0
+    with np.errstate(over="ignore"):
+        return 1.0 / (1.0 + np.exp(-kappa * (x - theta)))
+
+
+def power_iterate_full(S: np.ndarray, U: np.ndarray, F: np.ndarray, alpha: float, g_t, g_s, K: int, x0=None,
+                       binarize=None):
     """K iterations of Eq.7 + Eq.8 per volume from x_0 = S (Alg.1 line 3) or x0.
 
+    binarize = (n_cont, kappa0, growth): Alg.1 STEP 3 -- after the normalisation of
+    iteration k > n_cont the iterate is soft-binarised with kappa_k = kappa0 *
+    growth^(k - n_cont - 1) (reading A21, SPEC's geometric schedule); the result is
+    then the next iterate as is (not renormalised) and, after the last iteration,
+    the output (values in (0, 1)).
     Returns (x_K [B][T][H][W], stats) with stats["nu"][b, k] = ||X_crt_k||,
     stats["gain"][b, k] = nu_k / ||x_{k-1}||, stats["rho"][b, k] = Rayleigh quotient.
     """
@@ -73,5 +90,7 @@ def power_iterate_full(S: np.ndarray, U: np.ndarray, F: np.ndarray, alpha: float
             gains[b, k] = nu / math.sqrt(xx)
             rhos[b, k] = float(np.sum(x * y)) / xx
             x = y / nu
+            if binarize is not None and k + 1 > binarize[0]:
+                x = soft_binarize(x, binarize[1] * binarize[2] ** (k - binarize[0]))
         xs[b] = x
     return xs, {"nu": nus, "gain": gains, "rho": rhos}

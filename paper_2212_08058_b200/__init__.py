@@ -92,7 +92,7 @@ _SIGS = {
     "sfseg_workspace_bytes_full": (C.c_int, [Shape, C.c_int32, C.c_int32, GaussC, C.c_int32, _P]),
     "sfseg_power_iterate_full": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, _P, C.c_int32, _P, C.c_float,
                                            C.c_int32, C.c_double, C.c_double, Shape, GaussC, C.c_int32, _P, _P,
-                                           _P, _P, C.c_size_t, _P]),
+                                           _P, _P, _P, C.c_size_t, _P]),
     "sfseg_slabs_workspace_bytes": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
     "sfseg_power_iterate_slabs": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                             C.c_int32, _P, _P, _P, C.c_int32, _P, C.c_size_t, _P]),
@@ -387,6 +387,10 @@ class HostStream:
         self.solver.sync(s_cmp)
 
 
+class BinarizeC(C.Structure):
+    _fields_ = [("n_cont", C.c_int32), ("kappa0", C.c_float), ("growth", C.c_float)]
+
+
 class FullSolver:
     """The full SFSeg / SFSeg++ operator (Eq.7 / Eq.10 with
     unary exponent p, pairwise map F and alpha) through sfseg_power_iterate_full."""
@@ -404,7 +408,9 @@ class FullSolver:
 
     def forward(self, s_ch: torch.Tensor, ws, f_ch: torch.Tensor, wf, p: float, alpha: float,
                 bs: float = 0.0, act_s: int = ACT_IDENTITY, bf: float = 0.0, act_f: int = ACT_IDENTITY,
-                x0=None, x_out: Optional[torch.Tensor] = None, stream=None, check: bool = True) -> torch.Tensor:
+                x0=None, x_out: Optional[torch.Tensor] = None, binarize=None, stream=None,
+                check: bool = True) -> torch.Tensor:
+        """binarize = (n_cont, kappa0, growth): Alg.1 STEP 3 soft-binarisation (row f2)."""
         _require(s_ch, "s_ch", 5)
         _require(f_ch, "f_ch", 5)
         if x_out is None:
@@ -413,6 +419,8 @@ class FullSolver:
             _ptr(s_ch), self.Cs, _weights(ws, self.Cs), float(bs), int(act_s),
             _ptr(f_ch), self.Cf, _weights(wf, self.Cf), float(bf), int(act_f), float(p), float(alpha),
             Shape(*self.shape), self.gauss.c(), self.K, _ptr(x0), _ptr(x_out), _ptr(self.stats),
+            None if binarize is None else C.byref(BinarizeC(int(binarize[0]), float(binarize[1]),
+                                                            float(binarize[2]))),
             _ptr(self.ws), self.ws_bytes, _stream(stream))
         _check(st, "sfseg_power_iterate_full")
         if check:

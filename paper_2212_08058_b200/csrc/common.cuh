@@ -32,6 +32,7 @@ enum ScalSlot : int {
   SC_INV_NU = 3,       // backward: 1 / nu_k
   SC_INV_NU_PREV = 4,  // backward: 1 / nu_{k-1}
   SC_NU = 5,           // last nu
+  SC_THETA = 6,        // soft-binarisation: mean of the positive entries of y_k (y units)
 };
 
 enum ErrBits : unsigned { ERR_DEGENERATE = 1u, ERR_NONFINITE = 2u };

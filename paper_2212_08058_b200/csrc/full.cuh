@@ -145,4 +145,89 @@ __global__ void __launch_bounds__(kEwThreads) full_epilogue_kernel(const __grid_
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
+// ------------------------------------------------------------------ soft-binarisation (row f2)
+// Alg.1 STEP 3, reading A21: x_k <- sigma(kappa (y_k/nu_k - theta)),
+// theta = mean of the positive entries of y_k/nu_k.  Two streaming passes after the
+// iteration's norm finalize: pos_stats (sum and count of the positive y, fp64 fixed
+// order) and binarize (the sigmoid, the next stored iterate a = U x or the dense
+// output, and ||x|| for the next gain).
+struct BinParams {
+  const float* y;       // pitched y_k (unnormalised)
+  const float* U;       // pitched S^p (multiplier of the next stored iterate) or null
+  float* a;             // pitched: U * x_k (next iterate), or null
+  float* x_dense;       // dense output (last iteration) or null
+  double* sc;
+  double* partials;     // [2][B][T*gx]
+  unsigned* counter;
+  unsigned* err;
+  int B, T, H, W, Wp, gx;
+  float kappa;
+};
+
+__global__ void __launch_bounds__(kEwThreads) pos_stats_kernel(const __grid_constant__ BinParams P) {
+  __shared__ double red[kEwThreads / 32];
+  __shared__ int flag;
+  const int bt = blockIdx.y;
+  const int b = bt / P.T, t = bt - b * P.T;
+  const long HWp = (long)P.H * P.Wp;
+  double s = 0.0, n = 0.0;
+  for (int y = blockIdx.x; y < P.H; y += P.gx)
+    for (int x = threadIdx.x; x < P.W; x += kEwThreads) {
+      const float v = P.y[(long)bt * HWp + (long)y * P.Wp + x];
+      if (v > 0.f) {
+        s += (double)v;
+        n += 1.0;
+      }
+    }
+  const double ss = block_sum<kEwThreads>(s, red);
+  const double nn = block_sum<kEwThreads>(n, red);
+  const long nper = (long)P.T * P.gx;
+  if (threadIdx.x == 0) {
+    P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = ss;
+    P.partials[(long)(P.B + b) * nper + (long)t * P.gx + blockIdx.x] = nn;
+  }
+  if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
+  for (int v = 0; v < P.B; ++v) {
+    const double tot = block_sum_array<kEwThreads>(P.partials + (long)v * nper, nper, 1, red);
+    const double cnt = block_sum_array<kEwThreads>(P.partials + (long)(P.B + v) * nper, nper, 1, red);
+    if (threadIdx.x == 0) P.sc[v * kScal + SC_THETA] = cnt > 0.0 ? tot / cnt : 0.0;
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+__global__ void __launch_bounds__(kEwThreads) binarize_kernel(const __grid_constant__ BinParams P) {
+  __shared__ double red[kEwThreads / 32];
+  __shared__ int flag;
+  const int bt = blockIdx.y;
+  const int b = bt / P.T, t = bt - b * P.T;
+  const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
+  const double nu = P.sc[b * kScal + SC_NU];
+  const float inv_nu = (float)(1.0 / nu);
+  const float theta = (float)(P.sc[b * kScal + SC_THETA] / nu);
+  double acc = 0.0;
+  for (int y = blockIdx.x; y < P.H; y += P.gx)
+    for (int x = threadIdx.x; x < P.Wp; x += kEwThreads) {
+      const long po = (long)bt * HWp + (long)y * P.Wp + x;
+      float xv = 0.f;
+      if (x < P.W) {
+        xv = 1.f / (1.f + expf(-P.kappa * (P.y[po] * inv_nu - theta)));
+        acc += (double)xv * (double)xv;
+        if (P.x_dense) P.x_dense[(long)bt * HW + (long)y * P.W + x] = xv;
+      }
+      if (P.a) P.a[po] = P.U ? P.U[po] * xv : xv;
+    }
+  const double s = block_sum<kEwThreads>(acc, red);
+  const long nper = (long)P.T * P.gx;
+  if (threadIdx.x == 0) P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = s;
+  if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
+  for (int v = 0; v < P.B; ++v) {
+    const double tot = block_sum_array<kEwThreads>(P.partials + (long)v * nper, nper, 1, red);
+    if (threadIdx.x == 0) {
+      P.sc[v * kScal + SC_XNORM] = sqrt(tot);  // ||x_k|| for the next gain
+      P.sc[v * kScal + SC_S] = 1.0;            // x_k is the iterate itself (no pending normaliser)
+    }
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
 }  // namespace sfseg

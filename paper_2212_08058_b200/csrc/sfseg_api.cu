@@ -275,7 +275,7 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->NCC = (int)((P->H * P->Wp / 4 + 128 * P->NCOLS - 1) / (128 * P->NCOLS));
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
   size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max((size_t)P->G * kSpassPartSlots, (size_t)P->G3 * kF3dCW),
-                                   (size_t)P->BT * P->gx);
+                                   2 * (size_t)P->BT * P->gx);
   n_part = std::max<size_t>(n_part, (size_t)4 * num_sms() * (kMaxC + 1));
   P->n_part = n_part;
   size_t off = align_up(sizeof(WsHeader));
@@ -1070,9 +1070,12 @@ sfseg_status sfseg_workspace_bytes_full(sfseg_shape sh, int32_t Cs, int32_t Cf, 
 sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float* ws_host, float bs, int32_t act_s,
                                       const float* f_ch, int32_t Cf, const float* wf_host, float bf, int32_t act_f,
                                       double p, double alpha, sfseg_shape sh, sfseg_gauss gauss, int32_t K,
-                                      const float* x0, float* x_out, double* stats, void* ws, size_t ws_bytes,
-                                      void* stream) {
+                                      const float* x0, float* x_out, double* stats, const sfseg_binarize* bin,
+                                      void* ws, size_t ws_bytes, void* stream) {
   if (!s_ch || !f_ch || !ws_host || !wf_host || !x_out || !validate_act(act_s) || !validate_act(act_f))
+    return SFSEG_ERR_INVALID_ARGUMENT;
+  if (bin && (bin->n_cont < 0 || !(bin->kappa0 > 0.f) || !std::isfinite(bin->kappa0) || !(bin->growth > 0.f) ||
+              !std::isfinite(bin->growth)))
     return SFSEG_ERR_INVALID_ARGUMENT;
   sfseg_status s = full_check(Cs, Cf, p, alpha);
   if (s != SFSEG_OK) return s;
@@ -1173,11 +1176,36 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
         SF_CUDA(after_launch("spass_plain", st));
       }
     }
+    const bool bink = bin && k > bin->n_cont;  // Alg.1 STEP 3 after this iteration
     ep.k = k;
-    ep.last = (k == K) ? 1 : 0;
+    ep.last = (k == K || bink) ? 1 : 0;       // store y_k itself when it is binarised next
     full_epilogue_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ep);
     SF_CUDA(after_launch("full_epilogue", st));
+    if (bink) {
+      BinParams bp;
+      std::memset(&bp, 0, sizeof(bp));
+      bp.y = a;
+      bp.U = U;
+      bp.a = (k == K) ? nullptr : a;   // in place: each element of y_k becomes U x_k
+      bp.x_dense = (k == K) ? x_out : nullptr;
+      bp.sc = at<double>(ws, P.off_sc);
+      bp.partials = at<double>(ws, P.off_part);
+      bp.counter = &at<WsHeader>(ws, 0)->counter[1];
+      bp.err = &at<WsHeader>(ws, 0)->err;
+      bp.B = (int)P.B;
+      bp.T = (int)P.T;
+      bp.H = (int)P.H;
+      bp.W = (int)P.W;
+      bp.Wp = (int)P.Wp;
+      bp.gx = P.gx;
+      bp.kappa = (float)(bin->kappa0 * std::pow((double)bin->growth, (double)(k - bin->n_cont - 1)));
+      pos_stats_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(bp);
+      SF_CUDA(after_launch("pos_stats", st));
+      binarize_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(bp);
+      SF_CUDA(after_launch("binarize", st));
+    }
   }
+  if (bin && K > bin->n_cont) return SFSEG_OK;  // x_out = the last binarised iterate (values in (0,1))
   dim3 grid((unsigned)P.gx, (unsigned)P.BT);
   final_scale_kernel<<<grid, kEwThreads, 0, st>>>(a, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H, (int)P.W,
                                                   (int)P.Wp, (int)P.T, 0);

@@ -57,9 +57,11 @@ __host__ __device__ constexpr size_t spass_smem_for(int R, int stages) {
          8 * 8 + 16;
 }
 constexpr size_t kSmemPerSM = 227 * 1024;
-// TMA stages: double-buffered unless a single stage is what lets 3 CTAs share an SM.
+// TMA stages: double-buffered when 3 CTAs still share an SM (measured at c2, profiles/q11
+// vs q12: 3 CTAs x 2 stages 161 us, 4 CTAs x 1 stage 166 us -- occupancy is not the limit).
+__host__ __device__ constexpr int spass_fit_n(size_t smem) { return (int)(kSmemPerSM / (smem + 1024)); }
 __host__ __device__ constexpr int spass_stages(int R) {
-  return (3 * (spass_smem_for(R, 2) + 1024) <= kSmemPerSM) ? 2 : ((3 * (spass_smem_for(R, 1) + 1024) <= kSmemPerSM) ? 1 : 2);
+  return spass_fit_n(spass_smem_for(R, 2)) >= 3 ? 2 : 1;
 }
 __host__ __device__ constexpr size_t spass_smem_bytes(int R) { return spass_smem_for(R, spass_stages(R)); }
 __host__ __device__ constexpr int spass_ctas_per_sm(int R) {
@@ -397,7 +399,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_constant__ SpassParams P) {
+__global__ void __launch_bounds__(kSpassThreads, 4) spass_kernel(const __grid_constant__ SpassParams P) {
   using Geo = SpassGeom<R>;
   constexpr int BOXW = Geo::BOXW;
   constexpr int RING_ROWS = spass_nslot(R) * kM;

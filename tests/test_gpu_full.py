@@ -105,3 +105,34 @@ def test_full_invalid_arguments(sf):
     for p, alpha in ((0.0, 1.0), (-1.0, 1.0), (1.0, 0.0), (float("nan"), 1.0)):
         with pytest.raises(RuntimeError):
             solver.forward(s, [1.0], s, [1.0], p, alpha)
+
+
+# --------------------------------------------------------------------------- row f2
+@pytest.mark.parametrize("n_cont,K", [(3, 6), (0, 3), (5, 5)])
+def test_full_soft_binarisation(sf, n_cont, K):
+    """Alg.1 STEP 3: soft-binarisation after n_cont continuous iterations (reading A21).
+    Output values in (0,1) when K > n_cont; per-iteration norms and gains (the gain after a
+    binarised iteration uses ||x_k|| of the binarised iterate) match the oracle."""
+    rng = np.random.default_rng(13 + n_cont)
+    B, T, H, W = 2, 6, 40, 90
+    s_ch = (rng.random((B, 1, T, H, W)) * 0.9 + 0.05).astype(np.float32)
+    f_ch = rng.random((B, 1, T, H, W)).astype(np.float32)
+    dev = torch.device("cuda")
+    g = sf.Gauss(1.0, 3.0, 3, 9)
+    solver = sf.FullSolver((B, T, H, W), 1, 1, g, K)
+    xg = solver.forward(torch.from_numpy(s_ch).to(dev), [1.0], torch.from_numpy(f_ch).to(dev), [1.0], 0.5, 1.0,
+                        binarize=(n_cont, 4.0, 2.0)).cpu().numpy()
+    S, U, F = O.combine_full(s_ch, [1.0], 0.0, 0, f_ch, [1.0], 0.0, 0, 0.5)
+    xo, sto = O.power_iterate_full(S, U, F, 1.0, O.gaussian_taps(1.0, 3), O.gaussian_taps(3.0, 9), K,
+                                   binarize=(n_cont, 4.0, 2.0))
+    for b in range(B):
+        assert _rel(xg[b], xo[b]) <= X_TOL, f"volume {b}: rel err {_rel(xg[b], xo[b]):.3e}"
+    stg = solver.stats.cpu().numpy()
+    np.testing.assert_allclose(stg[..., 0], sto["nu"], rtol=NU_TOL)
+    np.testing.assert_allclose(stg[..., 1], sto["gain"], rtol=NU_TOL)
+    if K > n_cont:
+        assert xg.min() > 0.0 and xg.max() < 1.0
+        mask = sf.threshold(torch.from_numpy(xg).to(dev), 0.5, sf.THR_ABSOLUTE).cpu().numpy()
+        ref = O.threshold(xo, 0.5, O.THR_ABSOLUTE)
+        band = np.abs(xo - 0.5) > 1e-4
+        assert (mask[band] == ref[band]).all()

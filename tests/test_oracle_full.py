@@ -103,3 +103,35 @@ def test_combine_full_maps_and_power():
     assert abs(S.max() - 1.0 / (1.0 + math.exp(-1.5))) <= 1e-15
     assert abs(F.max() - 0.5) <= 1e-15
     assert np.allclose(U, np.sqrt(S), rtol=0, atol=1e-15)
+
+
+# --------------------------------------------------------------------------- row f2
+def test_soft_binarize_spec_values():
+    """S:215-218: x = theta -> 0.5; kappa 4, x - theta = 0.25 -> sigma(1); saturation to {0, 1};
+    the map is monotone (order preserving)."""
+    x = np.array([0.25, 0.75])          # theta = mean of positives = 0.5
+    y = O.soft_binarize(x, 4.0)
+    assert abs(y[1] - 1.0 / (1.0 + math.exp(-1.0))) <= 1e-15
+    assert abs(O.soft_binarize(np.array([0.5, 0.5]), 7.0)[0] - 0.5) <= 1e-15
+    z = O.soft_binarize(np.array([0.1, 0.9]), 1e4)
+    assert abs(z[0]) <= 1e-6 and abs(z[1] - 1.0) <= 1e-6
+    r = np.random.default_rng(0).random(50)
+    assert (np.argsort(O.soft_binarize(r, 3.0), kind="stable") == np.argsort(r, kind="stable")).all()
+
+
+def test_binarized_iteration_follows_alg1():
+    """With binarize=(n_cont, k0, g): iterations <= n_cont are the plain Eq.7/8 steps; after each
+    later iteration the normalised iterate is soft-binarised with the geometric kappa."""
+    rng = np.random.default_rng(5)
+    S, F = rng.random((1, 3, 6, 7)), rng.random((1, 3, 6, 7))
+    gt, gs = _taps(1, 2)
+    U = np.power(S, 0.5)
+    xb, stb = O.power_iterate_full(S, U, F, 1.0, gt, gs, 5, binarize=(3, 4.0, 2.0))
+    x = S[0].copy()
+    for k in range(5):
+        y = O.full_step(U[0], F[0], 1.0, x, gt, gs, gs)
+        x = y / np.linalg.norm(y)
+        if k + 1 > 3:
+            x = O.soft_binarize(x, 4.0 * 2.0 ** (k - 3))
+    assert np.abs(xb[0] - x).max() <= 1e-14
+    assert 0.0 < xb.min() and xb.max() < 1.0
