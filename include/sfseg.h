@@ -175,6 +175,25 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
                                       const sfseg_binarize* bin_or_null, void* ws, size_t ws_bytes,
                                       void* stream);
 
+/* ---- online / sub-window mode ----
+ * PAPER.md:367-387 (Fig. offline_online): the power iteration runs on
+ * q-frame sub-windows sliding by `stride` frames (starts 0, stride, ... while
+ * start + q < T, then T - q; q >= T is the offline solve), each window the
+ * offline iteration of sfseg_power_iterate (zero padding at the window ends,
+ * normalisation per window), warm-started on the frames it shares with the
+ * previous window from that window's solution, rescaled per volume to the L2
+ * norm of F on those frames (reading A20), and from F elsewhere (Alg.1 line 3).
+ * x_out [B][T][H][W]: per frame the result of the LAST window covering it (each
+ * window's result is unit-norm over that window).  Combine as
+ * sfseg_power_iterate; device errors via sfseg_sync_status(ws, stream).
+ * ws: >= sfseg_workspace_bytes_online(...).  Asynchronous. */
+sfseg_status sfseg_workspace_bytes_online(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K,
+                                          int32_t q, size_t* ws_bytes_host);
+sfseg_status sfseg_power_iterate_online(const float* ch, int32_t C, const float* w_host, float b,
+                                        int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
+                                        int32_t q, int32_t stride, float* x_out, void* ws,
+                                        size_t ws_bytes, void* stream);
+
 /* Hard threshold ("simply obtained by thresholding"): uint8 mask.
  * Mode per sfseg_thr_mode; strict '>' in fp32 against tau*max; a frame (or
  * volume) whose max is <= 0 yields zeros.  ws: >= sfseg_threshold_ws_bytes. */

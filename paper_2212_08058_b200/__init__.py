@@ -89,6 +89,9 @@ _SIGS = {
     "sfseg_profile_enable": (C.c_int, [C.c_int32]),
     "sfseg_profile_read": (C.c_int, [_P, _P]),
     "sfseg_set_algorithm": (C.c_int, [C.c_int32]),
+    "sfseg_workspace_bytes_online": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
+    "sfseg_power_iterate_online": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
+                                             C.c_int32, C.c_int32, _P, _P, C.c_size_t, _P]),
     "sfseg_workspace_bytes_full": (C.c_int, [Shape, C.c_int32, C.c_int32, GaussC, C.c_int32, _P]),
     "sfseg_power_iterate_full": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, _P, C.c_int32, _P, C.c_float,
                                            C.c_int32, C.c_double, C.c_double, Shape, GaussC, C.c_int32, _P, _P,
@@ -426,3 +429,21 @@ class FullSolver:
         if check:
             _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate_full (device)")
         return x_out
+
+
+def power_iterate_online(ch: torch.Tensor, w, gauss: Gauss, K: int, q: int, stride: int, b: float = 0.0,
+                         act: int = ACT_IDENTITY, stream=None) -> torch.Tensor:
+    """Online / sub-window mode via sfseg_power_iterate_online."""
+    _require(ch, "ch", 5)
+    B, Cn, T, H, W = ch.shape
+    shp = Shape(B, T, H, W)
+    n = C.c_size_t(0)
+    _check(lib().sfseg_workspace_bytes_online(shp, Cn, gauss.c(), int(K), int(q), C.byref(n)),
+           "sfseg_workspace_bytes_online")
+    ws = _alloc_bytes(n.value, ch.device)
+    x = torch.empty((B, T, H, W), dtype=torch.float32, device=ch.device)
+    _check(lib().sfseg_power_iterate_online(_ptr(ch), Cn, _weights(w, Cn), float(b), int(act), shp, gauss.c(),
+                                            int(K), int(q), int(stride), _ptr(x), _ptr(ws), n.value,
+                                            _stream(stream)), "sfseg_power_iterate_online")
+    _check(lib().sfseg_sync_status(_ptr(ws), _stream(stream)), "sfseg_power_iterate_online (device)")
+    return x

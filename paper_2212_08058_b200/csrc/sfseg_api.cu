@@ -21,6 +21,7 @@
 #include "tpass.cuh"
 #include "comm.cuh"
 #include "full.cuh"
+#include "online.cuh"
 #include "launch.h"
 
 using namespace sfseg;
@@ -1210,6 +1211,121 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   final_scale_kernel<<<grid, kEwThreads, 0, st>>>(a, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H, (int)P.W,
                                                   (int)P.Wp, (int)P.T, 0);
   SF_CUDA(after_launch("final_scale", st));
+  return SFSEG_OK;
+}
+
+// ====================================================================== online / sub-window mode (§8(f) f3)
+namespace {
+struct OnlineLayout {
+  size_t inner, off_F, off_Fw, off_x0, off_xa, off_xb, off_fac, total;
+};
+sfseg_status online_layout(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, int32_t q, OnlineLayout* L) {
+  if (q < 1) return SFSEG_ERR_INVALID_ARGUMENT;
+  const int64_t qq = std::min<int64_t>(q, sh.T);
+  Plan P;
+  sfseg_status s = make_plan(sfseg_shape{sh.B, qq, sh.H, sh.W}, 1, g, K, &P);
+  if (s != SFSEG_OK) return s;
+  Plan Pc;
+  if ((s = make_plan(sh, C, g, K, &Pc)) != SFSEG_OK) return s;  // validates C
+  L->inner = align_up(P.ws_fwd + sfseg_threshold_ws_bytes(sfseg_shape{sh.B, qq, sh.H, sh.W}));
+  const size_t full = align_up(sizeof(float) * (size_t)(sh.B * sh.T * sh.H * sh.W));
+  const size_t win = align_up(sizeof(float) * (size_t)(sh.B * qq * sh.H * sh.W));
+  size_t off = L->inner;
+  L->off_F = off;
+  off += full;
+  L->off_Fw = off;
+  off += win;
+  L->off_x0 = off;
+  off += win;
+  L->off_xa = off;
+  off += win;
+  L->off_xb = off;
+  off += win;
+  L->off_fac = off;
+  off += align_up(sizeof(double) * (size_t)sh.B);
+  L->total = off;
+  return SFSEG_OK;
+}
+// window starts: 0, stride, 2 stride, ... while start + q < T, then T - q (oracle/online.py)
+std::vector<int64_t> window_starts(int64_t T, int64_t q, int64_t stride) {
+  std::vector<int64_t> st;
+  if (q >= T) return {0};
+  for (int64_t s = 0; s + q < T; s += stride) st.push_back(s);
+  if (st.empty() || st.back() + q < T) st.push_back(T - q);
+  return st;
+}
+// copy frames [t0, t0 + n) of every volume between a [B][Ta][HW] and a [B][Tb][HW] buffer
+cudaError_t copy_frames(float* dst, int64_t Td, int64_t td0, const float* src, int64_t Ts, int64_t ts0, int64_t n,
+                        int64_t B, int64_t HW, cudaStream_t st) {
+  return cudaMemcpy2DAsync(dst + td0 * HW, sizeof(float) * Td * HW, src + ts0 * HW, sizeof(float) * Ts * HW,
+                           sizeof(float) * n * HW, B, cudaMemcpyDeviceToDevice, st);
+}
+}  // namespace
+
+sfseg_status sfseg_workspace_bytes_online(sfseg_shape sh, int32_t C, sfseg_gauss gauss, int32_t K, int32_t q,
+                                          size_t* ws_bytes_host) {
+  if (!ws_bytes_host) return SFSEG_ERR_INVALID_ARGUMENT;
+  OnlineLayout L;
+  sfseg_status s = online_layout(sh, C, gauss, K, q, &L);
+  if (s != SFSEG_OK) return s;
+  *ws_bytes_host = L.total;
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_power_iterate_online(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
+                                        sfseg_shape sh, sfseg_gauss gauss, int32_t K, int32_t q, int32_t stride,
+                                        float* x_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!ch || !w_host || !x_out || !validate_act(act) || stride < 1) return SFSEG_ERR_INVALID_ARGUMENT;
+  OnlineLayout L;
+  sfseg_status s = online_layout(sh, C, gauss, K, q, &L);
+  if (s != SFSEG_OK) return s;
+  if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
+  if ((s = check_ws(ws, ws_bytes, L.total)) != SFSEG_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t T = sh.T, B = sh.B, HW = sh.H * sh.W, qq = std::min<int64_t>(q, T);
+  char* base = static_cast<char*>(ws);
+  float* Ffull = reinterpret_cast<float*>(base + L.off_F);
+  float* Fw = reinterpret_cast<float*>(base + L.off_Fw);
+  float* x0 = reinterpret_cast<float*>(base + L.off_x0);
+  float* xcur = reinterpret_cast<float*>(base + L.off_xa);
+  float* xprev = reinterpret_cast<float*>(base + L.off_xb);
+  double* fac = reinterpret_cast<double*>(base + L.off_fac);
+  // F once for the whole video (Eq.9); every window then solves with C = 1, identity
+  if ((s = sfseg_combine_channels(ch, C, sh, w_host, b, act, Ffull, stream)) != SFSEG_OK) return s;
+  const float one = 1.0f;
+  const sfseg_shape ws_shape{B, qq, sh.H, sh.W};
+  int64_t prev = -1;
+  for (const int64_t s0 : window_starts(T, qq, stride)) {
+    SF_CUDA(copy_frames(Fw, qq, 0, Ffull, T, s0, qq, B, HW, st));
+    SF_CUDA(cudaMemcpyAsync(x0, Fw, sizeof(float) * (size_t)(B * qq * HW), cudaMemcpyDeviceToDevice, st));
+    if (prev >= 0 && prev + qq > s0) {  // overlap frames [s0, prev + qq): warm start (reading A20)
+      OnlineParams op;
+      op.xprev = xprev;
+      op.Fw = Fw;
+      op.x0 = x0;
+      op.factor = fac;
+      op.counter = &at<WsHeader>(ws, 0)->counter[2];
+      op.HW = HW;
+      op.B = (int)B;
+      op.q = (int)qq;
+      op.nov = (int)(prev + qq - s0);
+      op.po = (int)(s0 - prev);
+      Plan P;  // the inner solve's partials region holds >= 2 * B * q * gx doubles
+      make_plan(ws_shape, 1, gauss, K, &P);
+      op.gx = P.gx;
+      op.partials = at<double>(ws, P.off_part);
+      online_norms_kernel<<<dim3(op.gx, (unsigned)(B * op.nov)), kEwThreads, 0, st>>>(op);
+      SF_CUDA(after_launch("online_norms", st));
+      online_warm_kernel<<<dim3(op.gx, (unsigned)(B * op.nov)), kEwThreads, 0, st>>>(op);
+      SF_CUDA(after_launch("online_warm", st));
+    }
+    s = sfseg_power_iterate(Fw, 1, &one, 0.f, SFSEG_ACT_IDENTITY, ws_shape, gauss, K, x0, xcur, nullptr, nullptr, 0,
+                            nullptr, ws, L.inner, nullptr, stream);
+    if (s != SFSEG_OK) return s;
+    SF_CUDA(copy_frames(x_out, T, s0, xcur, qq, 0, qq, B, HW, st));
+    std::swap(xcur, xprev);
+    prev = s0;
+  }
   return SFSEG_OK;
 }
 
