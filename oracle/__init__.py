@@ -30,3 +30,4 @@ from .sfseg_oracle import (  # noqa: F401
 from .full import full_step, combine_full, power_iterate_full, soft_binarize  # noqa: F401,E402
 from .dense import dense_M_taylor  # noqa: F401,E402
 from .online import window_starts, power_iterate_online  # noqa: F401,E402
+from .learn import AdamW, mse_loss_grad, train  # noqa: F401,E402

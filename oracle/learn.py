@@ -1,0 +1,75 @@
+"""Learning loop -- TEST INFRASTRUCTURE ONLY.
+
+PAPER.md:210-232 (§3.4): the channel weights w (and bias b) of Eq.9 are learned
+by minimising a loss of the final segmentation, with the gradient propagated
+"through the full spectral algorithm", using AdamW (Eq.13) --
+"an AdamW optimizer with AMSGrad".  Readings:
+A13 -- the loss is the mean squared error between x_K and the unit-normalised
+clean mask (the paper's Focal-Dice loss, Eq.12, needs the soft-binarised output,
+whose backward is not part of this build); A22 -- AdamW with AMSGrad in
+PyTorch's form (decoupled weight decay w <- w - lr*wd*w, bias-corrected moments,
+running max of the second moment).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .sfseg_oracle import combine, power_iterate, power_iterate_backward
+
+
+def mse_loss_grad(x: np.ndarray, mask: np.ndarray):
+    """Reading A13: L = mean (x_K - m_hat)^2, m_hat = m / ||m|| (per volume); returns (L, dL/dx)."""
+    x = np.asarray(x, np.float64)
+    m = np.asarray(mask, np.float64)
+    mh = np.empty_like(m)
+    for b in range(m.shape[0]):
+        n = np.linalg.norm(m[b])
+        mh[b] = m[b] / n if n > 0 else m[b]
+    d = x - mh
+    return float(np.mean(d * d)), 2.0 * d / x.size
+
+
+class AdamW:
+    """Eq.13 with AMSGrad, PyTorch's update order (reading A22)."""
+
+    def __init__(self, n: int, lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
+                 amsgrad: bool = True):
+        self.lr, self.b1, self.b2, self.eps, self.wd, self.ams = lr, betas[0], betas[1], eps, weight_decay, amsgrad
+        self.m = np.zeros(n)
+        self.v = np.zeros(n)
+        self.vmax = np.zeros(n)
+        self.t = 0
+
+    def step(self, params: np.ndarray, grad: np.ndarray) -> np.ndarray:
+        self.t += 1
+        p = np.asarray(params, np.float64) * (1.0 - self.lr * self.wd)   # decoupled weight decay
+        g = np.asarray(grad, np.float64)
+        self.m = self.b1 * self.m + (1.0 - self.b1) * g
+        self.v = self.b2 * self.v + (1.0 - self.b2) * g * g
+        bc1 = 1.0 - self.b1 ** self.t
+        bc2 = 1.0 - self.b2 ** self.t
+        if self.ams:
+            self.vmax = np.maximum(self.vmax, self.v)
+            denom = np.sqrt(self.vmax) / math.sqrt(bc2) + self.eps
+        else:
+            denom = np.sqrt(self.v) / math.sqrt(bc2) + self.eps
+        return p - (self.lr / bc1) * self.m / denom
+
+
+def train(ch, mask, w0, b0: float, act: int, g_t, g_s, K: int, steps: int, lr: float, weight_decay: float = 0.0):
+    """`steps` AdamW steps on (w, b) of Eq.9 for the MSE loss of x_K; returns (w, b, losses)."""
+    w = np.asarray(w0, np.float64).copy()
+    b = float(b0)
+    opt = AdamW(w.size + 1, lr, weight_decay=weight_decay)
+    losses = []
+    for _ in range(steps):
+        F, _ = combine(ch, w, b, act)
+        x, _ = power_iterate(F, g_t, g_s, K)
+        L, g = mse_loss_grad(x, mask)
+        losses.append(L)
+        dw, db = power_iterate_backward(ch, w, b, act, g_t, g_s, K, g)
+        pb = opt.step(np.concatenate([w, [b]]), np.concatenate([dw, [db]]))
+        w, b = pb[:-1], float(pb[-1])
+    return w, b, losses

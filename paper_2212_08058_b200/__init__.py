@@ -447,3 +447,63 @@ def power_iterate_online(ch: torch.Tensor, w, gauss: Gauss, K: int, q: int, stri
                                             _stream(stream)), "sfseg_power_iterate_online")
     _check(lib().sfseg_sync_status(_ptr(ws), _stream(stream)), "sfseg_power_iterate_online (device)")
     return x
+
+
+class AdamW:
+    """AdamW with AMSGrad (Eq.13, PAPER.md:224-229; "AdamW optimizer with AMSGrad", P:603) over
+    the handful of combine parameters (w, b) of Eq.9 -- host-side, like any optimizer state of
+    a C+1-parameter model (reading A22: PyTorch's update order)."""
+
+    def __init__(self, n: int, lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
+                 amsgrad: bool = True):
+        import numpy as np
+        self.np = np
+        self.lr, self.b1, self.b2, self.eps, self.wd, self.ams = lr, betas[0], betas[1], eps, weight_decay, amsgrad
+        self.m = np.zeros(n)
+        self.v = np.zeros(n)
+        self.vmax = np.zeros(n)
+        self.t = 0
+
+    def step(self, params, grad):
+        np = self.np
+        self.t += 1
+        p = np.asarray(params, np.float64) * (1.0 - self.lr * self.wd)
+        g = np.asarray(grad, np.float64)
+        self.m = self.b1 * self.m + (1.0 - self.b1) * g
+        self.v = self.b2 * self.v + (1.0 - self.b2) * g * g
+        bc1, bc2 = 1.0 - self.b1 ** self.t, 1.0 - self.b2 ** self.t
+        if self.ams:
+            self.vmax = np.maximum(self.vmax, self.v)
+            denom = np.sqrt(self.vmax) / bc2 ** 0.5 + self.eps
+        else:
+            denom = np.sqrt(self.v) / bc2 ** 0.5 + self.eps
+        return p - (self.lr / bc1) * self.m / denom
+
+
+def train_weights(ch: torch.Tensor, mask: torch.Tensor, w0, b0: float, act: int, gauss: Gauss, K: int, steps: int,
+                  lr: float, weight_decay: float = 0.0):
+    """Learn the Eq.9 weights end to end: each step runs
+    sfseg_power_iterate with a tape, the MSE loss of reading A13 against the
+    unit-normalised mask (harness-side elementwise gradient), then
+    sfseg_power_iterate_backward for dL/dw, dL/db, and an AdamW/AMSGrad update.
+    Returns (w, b, losses)."""
+    import numpy as np
+    _require(ch, "ch", 5)
+    B, Cn, T, H, W = ch.shape
+    solver = Solver((B, T, H, W), Cn, gauss, K, device=ch.device, want_tape=True)
+    m = mask.to(torch.float32)
+    mn = torch.linalg.vector_norm(m.reshape(B, -1).double(), dim=1).float().clamp_min(1e-30)
+    mh = m / mn.view(B, 1, 1, 1)
+    w = np.asarray(w0, np.float64).copy()
+    b = float(b0)
+    opt = AdamW(w.size + 1, lr, weight_decay=weight_decay)
+    losses = []
+    for _ in range(steps):
+        x = solver.forward(ch, w.astype(np.float32), float(b), act)
+        d = x - mh
+        losses.append(float((d.double() ** 2).mean()))
+        g = (2.0 / x.numel()) * d
+        dw, db = solver.backward(ch, w.astype(np.float32), g.contiguous(), float(b), act)
+        pb = opt.step(np.concatenate([w, [b]]), np.concatenate([dw, [db]]))
+        w, b = pb[:-1], float(pb[-1])
+    return w, b, losses

@@ -67,6 +67,7 @@ struct F3dParams {
   long U;                  // total units = B * TY * TX * T
   int B, T, H, W, Wp, TX, TY, G;
   int K, k, last, rayleigh;
+  unsigned long long* trace;    // debug (SFSEG_F3D_TRACE): per CTA {smid, t_start, t_compute_end, t_end} or null
   float gt[2 * kF3dMaxRT + 1];  // temporal taps g_t[o + RT]
   float gs[kF3dMaxR + 1];       // spatial taps g_s[|d|]
 };
@@ -119,6 +120,8 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
     return s;
   };
 
+  unsigned long long tr_start = 0;
+  if (P.trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
@@ -298,13 +301,31 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
 
   // ---------------------------------------------------------------- last CTA: fixed-order fp64 finalize
   f3d_compute_bar();
+  if (P.trace && tid == 0 && false) {
+    unsigned long long t1, smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    smid = sm;
+    P.trace[blockIdx.x * 4 + 0] = smid;
+    P.trace[blockIdx.x * 4 + 1] = tr_start;
+    P.trace[blockIdx.x * 4 + 2] = t1;
+    P.trace[blockIdx.x * 4 + 3] = (unsigned long long)(u_end - u_begin);
+  }
   if (tid == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(P.counter, 1u);
     *flag = (prev == (unsigned)P.G - 1) ? 1 : 0;
   }
   f3d_compute_bar();
-  if (*flag == 0) return;
+  if (*flag == 0) {
+    if (P.trace && tid == 0) {
+      unsigned long long t2;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+      P.trace[blockIdx.x * 4 + 3] = t2;
+    }
+    return;
+  }
   __threadfence();
   const long per_vol = P.U / P.B;
   for (int b = warp; b < P.B; b += kF3dCW) {
@@ -326,6 +347,11 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
     if (lane == 0) fwd_finalize(P.sc + b * kScal, P.stats, P.tape_nu, P.err, P.K, P.k, P.rayleigh != 0, b, s0, s1);
   }
   if (tid == 0) *P.counter = 0u;
+  if (P.trace && tid == 0) {
+    unsigned long long t2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+    P.trace[blockIdx.x * 4 + 3] = t2;
+  }
 }
 
 }  // namespace sfseg

@@ -769,6 +769,8 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     for (int i = 0; i < 2 * P.RT + 1; ++i) fp.gt[i] = P.gt[i];
     for (int d = 0; d <= P.RS; ++d) fp.gs[d] = P.gs[P.RS + d];
     float* last_out = p;
+    const char* f3d_trace = std::getenv("SFSEG_F3D_TRACE");  // debug: per-CTA timing of the last launch
+    if (f3d_trace && *f3d_trace) SF_CUDA(cudaMalloc(&fp.trace, sizeof(unsigned long long) * 4 * P.G3));
     for (int k = 1; k <= K; ++k) {
       const bool odd = (k & 1) != 0;
       fp.tmap = odd ? map_p : map_v;
@@ -780,6 +782,18 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
       SF_CUDA(launch_f3d(P.RT, P.RS, fp, P.G3, st));
       SF_CUDA(after_launch("f3d", st));
       last_out = fp.out;
+    }
+    if (fp.trace) {
+      std::vector<unsigned long long> h((size_t)4 * P.G3);
+      SF_CUDA(cudaMemcpyAsync(h.data(), fp.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+      SF_CUDA(cudaStreamSynchronize(st));
+      cudaFree(fp.trace);
+      if (FILE* f = std::fopen(f3d_trace, "w")) {
+        std::fprintf(f, "cta,sm,t_start,t_bar,t_exit\n");
+        for (int i = 0; i < P.G3; ++i)
+          std::fprintf(f, "%d,%llu,%llu,%llu,%llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+        std::fclose(f);
+      }
     }
     dim3 grid((unsigned)P.gx, (unsigned)P.BT);
     final_scale_kernel<<<grid, kEwThreads, 0, st>>>(last_out, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H,
