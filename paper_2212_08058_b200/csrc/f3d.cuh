@@ -43,7 +43,7 @@ __host__ __device__ constexpr int f3d_th(int R) { return ((32 - 2 * R) / 4) * 4;
 __host__ __device__ constexpr int f3d_stages(int RT) { return 2 * RT + 1 + kF3dNPF; }
 __host__ __device__ constexpr size_t f3d_smem_bytes(int RT, int R) {
   return sizeof(float) * ((size_t)f3d_stages(RT) * (kM * f3d_boxw(R) + f3d_th(R) * kF3dTW) + (size_t)kF3dCW * kM * kF3dQS) +
-         2 * 8 * f3d_stages(RT) + 16;
+         2 * 8 * f3d_stages(RT) + 16 + 8 * kF3dCW;
 }
 __host__ __device__ constexpr int f3d_fit(size_t smem) {
   return (int)((227 * 1024) / (smem + 1024)) < 4 ? (int)((227 * 1024) / (smem + 1024)) : 4;
@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
   uint64_t* full = reinterpret_cast<uint64_t*>(qbuf + kF3dCW * kM * kF3dQS);
   uint64_t* empty = full + NS;
   int* flag = reinterpret_cast<int*>(empty + NS);
+  double* red = reinterpret_cast<double*>(flag + 4);  // kF3dCW doubles (finalize)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = P.T, H = P.H, W = P.W, Wp = P.Wp;
@@ -301,20 +302,17 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
 
   // ---------------------------------------------------------------- last CTA: fixed-order fp64 finalize
   f3d_compute_bar();
-  if (P.trace && tid == 0 && false) {
-    unsigned long long t1, smid;
+  if (P.trace && tid == 0) {  // debug: {smid, entry, all compute warps done, exit}
+    unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     unsigned sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    smid = sm;
-    P.trace[blockIdx.x * 4 + 0] = smid;
+    P.trace[blockIdx.x * 4 + 0] = sm;
     P.trace[blockIdx.x * 4 + 1] = tr_start;
     P.trace[blockIdx.x * 4 + 2] = t1;
-    P.trace[blockIdx.x * 4 + 3] = (unsigned long long)(u_end - u_begin);
   }
   if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(P.counter, 1u);
+    const unsigned prev = atomic_add_acq_rel(P.counter, 1u);  // the warps' partials: ordered by the barrier
     *flag = (prev == (unsigned)P.G - 1) ? 1 : 0;
   }
   f3d_compute_bar();
@@ -326,25 +324,21 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
     }
     return;
   }
-  __threadfence();
   const long per_vol = P.U / P.B;
-  for (int b = warp; b < P.B; b += kF3dCW) {
-    const long vs = (long)b * per_vol, ve = vs + per_vol;
-    double s0 = 0.0, s1 = 0.0;
-    for (long c = lane; c < nslots; c += 32) {
-      const long g = c / kF3dCW;
-      const long cs = g * P.U / P.G, ce = (g + 1) * P.U / P.G;
-      if (cs < ve && ce > vs) {
-        s0 += P.partials[(long)b * nslots + c];
-        s1 += P.partials[(long)(P.B + b) * nslots + c];
-      }
+  const bool wide = P.B < kF3dCW;  // few volumes: whole compute group per volume; many: a warp each
+  for (int b = wide ? 0 : warp; b < P.B; b += wide ? 1 : kF3dCW) {
+    long lo, hi;
+    vol_cta_range(b, per_vol, P.U, P.G, lo, hi);
+    double s0, s1;
+    if (wide) {
+      s0 = block_sum_range<kF3dCW * 32, 1>(P.partials + (long)b * nslots, lo * kF3dCW, hi * kF3dCW, 1, red);
+      s1 = block_sum_range<kF3dCW * 32, 1>(P.partials + (long)(P.B + b) * nslots, lo * kF3dCW, hi * kF3dCW, 1, red);
+    } else {
+      s0 = warp_sum_range(P.partials + (long)b * nslots, lo * kF3dCW, hi * kF3dCW);
+      s1 = warp_sum_range(P.partials + (long)(P.B + b) * nslots, lo * kF3dCW, hi * kF3dCW);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    }
-    if (lane == 0) fwd_finalize(P.sc + b * kScal, P.stats, P.tape_nu, P.err, P.K, P.k, P.rayleigh != 0, b, s0, s1);
+    if ((wide && tid == 0) || (!wide && lane == 0))
+      fwd_finalize(P.sc + b * kScal, P.stats, P.tape_nu, P.err, P.K, P.k, P.rayleigh != 0, b, s0, s1);
   }
   if (tid == 0) *P.counter = 0u;
   if (P.trace && tid == 0) {

@@ -437,22 +437,20 @@ __global__ void __launch_bounds__(kSpassThreads, 4) spass_kernel(const __grid_co
   // ---------------------------------------------------------------- last CTA: fixed-order fp64 finalize
   if (!last_block_arrive(P.counter, (unsigned)P.G, flag)) return;
   const long per_vol = P.U / P.B;  // units per volume
-  for (int b = warp; b < P.B; b += kSpassWarps) {
-    const long vs = (long)b * per_vol, ve = vs + per_vol;
-    double s0 = 0.0, s1 = 0.0;
-    for (int c = lane; c < P.G; c += 32) {
-      const long cs = (long)c * P.U / P.G, ce = (long)(c + 1) * P.U / P.G;
-      if (cs < ve && ce > vs) {
-        s0 += P.partials[(long)b * P.G + c];
-        s1 += P.partials[(long)(P.B + b) * P.G + c];
-      }
+  // few volumes: the whole CTA sums each volume's partials; many volumes: one warp each
+  const bool wide = P.B < kSpassWarps;
+  for (int b = wide ? 0 : warp; b < P.B; b += wide ? 1 : kSpassWarps) {
+    long lo, hi;
+    vol_cta_range(b, per_vol, P.U, P.G, lo, hi);
+    double s0, s1;
+    if (wide) {
+      s0 = block_sum_range<kSpassThreads>(P.partials + (long)b * P.G, lo, hi, 1, red);
+      s1 = block_sum_range<kSpassThreads>(P.partials + (long)(P.B + b) * P.G, lo, hi, 1, red);
+    } else {
+      s0 = warp_sum_range(P.partials + (long)b * P.G, lo, hi);
+      s1 = warp_sum_range(P.partials + (long)(P.B + b) * P.G, lo, hi);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    }
-    if (lane == 0) {
+    if ((wide && tid == 0) || (!wide && lane == 0)) {
       if (P.loc) {
         P.loc[2 * b] = s0;
         P.loc[2 * b + 1] = s1;
