@@ -1,24 +1,26 @@
 // Fused spatial pass of G_3D (x then y) + elementwise F multiplies
 // + per-iteration norm partials (Eq.8) -- the FP32-FMA-bound kernel of the path.
 //
-// Persistent, statically balanced: the work is the list of "row units"
-// (bt, strip, y) ordered bt-major, split into G equal contiguous ranges, one
-// per CTA.  A range decomposes into column segments (bt, strip, ya..yb); each
-// segment streams rows through:
+// Persistent, statically balanced: the work is the list of "block units"
+// (bt, 64-column strip, 32-row block) ordered bt-major, split into G equal
+// contiguous ranges, one per CTA.  A range decomposes into column segments
+// (bt, strip, ya..yb); each segment streams 32-row x-blocks through:
 //   TMA (cp.async.bulk.tensor.3d, OOB zero fill = zero padding in x and y)
-//     -> stage[2][32 rows][BOXW] (double-buffered, mbarrier complete_tx)
-//   x-pass: lane = row, 8 consecutive outputs per thread, (2R+1) taps from the
-//     kernel-parameter constant bank -> q rows written twice into a ring
-//     (duplicated so every y window is contiguous: immediate-offset LDS.128)
-//   y-pass: lane = column quad, warp = row quad, 4x4 outputs per thread
+//     -> stage[NST][32 rows][BOXW] (mbarrier complete_tx; thread 0 produces)
+//   x-pass: lane = row, 16 consecutive outputs per thread (warp w: columns
+//     16w..16w+15, skipped when beyond the image width), (2R+1) taps from the
+//     kernel-parameter bank (uniform registers) -> q rows written into a ring,
+//     the rows a y window can reach past the wrap written twice (every window
+//     contiguous: immediate-offset LDS.128)
+//   y-pass: lane = column quad, warp = two row quads, 4x4 outputs per thread
 //   epilogue: forward  y = F u ; store p = F y (or y on the last iteration);
 //             tape u; partials of ||y||^2 and <p_{k-1}, u> (Rayleigh)
 //             backward (Appendix A): x_bar_{k-1} = F v, F_bar += y_bar u_{k-1} + x_{k-1} v,
 //             partials of <x_{k-1}, x_bar_{k-1}>
-// No x- or y-pass FMA is repeated except the 2R-row warm-up per segment
-// (about 1-3 % at the configs' sizes).  The last CTA to finish reduces the
-// per-CTA partials in fixed order in fp64 (deterministic) and writes the
-// per-volume norm / scale for the next launch.
+// No x- or y-pass FMA is repeated except one 32-row x-block on each side of a
+// mid-column range cut.  The last CTA to finish reduces the per-CTA partials of
+// each volume (a contiguous CTA range) in fixed order in fp64 (deterministic)
+// and writes the per-volume norm / scale for the next launch.
 #pragma once
 #include "common.cuh"
 
@@ -233,12 +235,13 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
 
     // ---------------------------------------------------------------- y-pass + epilogue
     // thread: column quad cq (4 columns), row quad rq (4 rows) of the 32-row block
-    // y-pass: warp w owns the 16 columns its own x-pass produced (w*16 .. w*16+15):
-    // lane -> rows 4rq..4rq+3 x columns 4cq..4cq+3 (conflict-free LDS.128 on the stride-68 ring)
-    const int cq = lane & 3;
-    const int rq = lane >> 2;
-    const int x = sg.s * kTW + 16 * warp + 4 * cq;
-    const bool wlive = sg.s * kTW + 16 * warp < W;  // warp-uniform: ragged last strip
+    // y-pass: lane -> columns 4cq..4cq+3 (16 quads span the strip), warp -> two row quads
+    // (conflict-free LDS.128 on the stride-68 ring).  Measured faster than giving each warp
+    // its own 16 columns (which would let the ragged strip skip y work too): 157 vs 163 us.
+    const int cq = lane & 15;
+    const int rq = warp * 2 + (lane >> 4);
+    const int x = sg.s * kTW + 4 * cq;
+    const bool wlive = sg.s * kTW + 16 * warp < W;  // x-pass: this warp's 16 columns exist (ragged strip)
     const bool xok = x < W;
     const bool xfull = x + 4 <= W;
     const float4 msk = make_float4(1.f, (x + 1 < W) ? 1.f : 0.f, (x + 2 < W) ? 1.f : 0.f, (x + 3 < W) ? 1.f : 0.f);
@@ -264,7 +267,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
       }
     };
     auto ypass = [&](int m, const Pre& pr) {
-      const float* wb = ring + ((m % NSLOT) * kM + OFF + 4 * rq) * kRingStride + 16 * warp + 4 * cq;
+      const float* wb = ring + ((m % NSLOT) * kM + OFF + 4 * rq) * kRingStride + 4 * cq;
       float4 a[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -332,7 +335,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
     };
 
     for (int n = 0; n < nxb; ++n) {
-      const bool do_y = wlive && n >= PRO;
+      const bool do_y = n >= PRO;
       Pre pre;
       if (do_y) prefetch(n - PRO, pre);
       const int row0 = gs + n * kM;
@@ -399,7 +402,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kSpassThreads, 4) spass_kernel(const __grid_constant__ SpassParams P) {
+__global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_constant__ SpassParams P) {
   using Geo = SpassGeom<R>;
   constexpr int BOXW = Geo::BOXW;
   constexpr int RING_ROWS = spass_nslot(R) * kM;
