@@ -36,7 +36,7 @@ struct CombineParams {
 // columns (coalesced 128-byte rows for dense and pitched layouts alike); kRows
 // rows x kCols column chunks are unrolled so every thread keeps kRows*kCols
 // independent loads in flight (HBM latency hiding without any index division).
-constexpr int kRows = 2;
+constexpr int kRows = 4;
 constexpr int kCols = 4;
 
 __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_constant__ CombineParams P) {

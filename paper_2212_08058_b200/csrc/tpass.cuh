@@ -40,7 +40,7 @@ constexpr int kTpThreads = 128;
 // float4 columns) 6 x 128 threads per SM hold every column in ONE wave.
 __host__ __device__ constexpr int tpass_min_blocks(int RT) { return RT <= 6 ? 6 : (RT <= 9 ? 4 : 2); }
 // cp.async stages per input stream (frames prefetched ahead of the ring).
-__host__ __device__ constexpr int tpass_stages(int MODE) { return MODE == TP_FWD ? 8 : (MODE == TP_FWDF ? 6 : 4); }
+__host__ __device__ constexpr int tpass_stages(int MODE) { return MODE == TP_FWD ? 12 : (MODE == TP_FWDF ? 6 : 4); }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
