@@ -293,17 +293,31 @@ __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_const
   const int bt = blockIdx.y;
   const int b = bt / P.T, t = bt - b * P.T;
   const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
+  const float* gf = P.g + ((long)b * P.T + t) * HW;
   double acc = 0.0;
-  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < HWp; e += (long)P.gx * kEwThreads) {
-    const int y = (int)(e / P.Wp), x = (int)(e - (long)y * P.Wp);
-    const long po = (long)bt * HWp + e;
-    float gv = 0.f;
-    if (x < P.W) {
-      gv = P.g[((long)b * P.T + t) * HW + (long)y * P.W + x];
-      acc += (double)gv * (double)P.F[po] * (double)P.uK1[po];
+  // row-parallel (see combine_kernel): no per-element index division
+  for (int y = blockIdx.x; y < P.H; y += P.gx) {
+    for (int c0 = 0; c0 < P.Wp; c0 += kEwThreads * kCols) {
+      float gv[kCols], fv[kCols], uv[kCols];
+#pragma unroll
+      for (int i = 0; i < kCols; ++i) {  // all loads of the kCols columns first (memory parallelism)
+        const int x = c0 + i * kEwThreads + threadIdx.x;
+        const long po = (long)bt * HWp + (long)y * P.Wp + x;
+        const bool in = x < P.W;
+        gv[i] = in ? __ldcs(gf + (long)y * P.W + x) : 0.f;
+        fv[i] = in ? P.F[po] : 0.f;
+        uv[i] = in ? __ldcs(P.uK1 + po) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < kCols; ++i) {
+        const int x = c0 + i * kEwThreads + threadIdx.x;
+        if (x >= P.Wp) continue;
+        const long po = (long)bt * HWp + (long)y * P.Wp + x;
+        acc += (double)gv[i] * (double)fv[i] * (double)uv[i];
+        P.xbar[po] = gv[i];
+        P.Fbar[po] = 0.f;
+      }
     }
-    P.xbar[po] = gv;
-    P.Fbar[po] = 0.f;
   }
   const double s = block_sum<kEwThreads>(acc, red);
   const long nper = (long)P.T * P.gx;
@@ -335,6 +349,7 @@ struct ContractParams {
   float w[kMaxC];
 };
 
+// grid (gx, B*T), row-parallel; partials [(bt * gx + bx)][CMAX + 1]
 template <int CMAX>
 __global__ void __launch_bounds__(kEwThreads) contract_kernel(const __grid_constant__ ContractParams P) {
   __shared__ double red[kEwThreads / 32];
@@ -342,41 +357,45 @@ __global__ void __launch_bounds__(kEwThreads) contract_kernel(const __grid_const
   double acc[CMAX + 1];
 #pragma unroll
   for (int c = 0; c <= CMAX; ++c) acc[c] = 0.0;
-  const long HW = (long)P.H * P.W, vol = (long)P.T * HW;
-  const long N = (long)P.B * vol;
-  for (long i = (long)blockIdx.x * kEwThreads + threadIdx.x; i < N; i += (long)gridDim.x * kEwThreads) {
-    const long b = i / vol, r = i - b * vol;
-    const long t = r / HW, rr = r - t * HW;
-    const long y = rr / P.W, x = rr - y * P.W;
-    const long po = ((b * P.T + t) * P.H + y) * P.Wp + x;
-    float fb = P.Fbar[po];
-    if (P.xbar0) fb += P.xbar0[po];
-    const float* chb = P.ch + b * P.C * vol + r;
-    float cv[CMAX];
-    float z = P.bias;
+  const int bt = blockIdx.y;
+  const int b = bt / P.T, t = bt - b * P.T;
+  const long HW = (long)P.H * P.W, vol = (long)P.T * HW, HWp = (long)P.H * P.Wp;
+  const float* chf = P.ch + (long)b * P.C * vol + (long)t * HW;
+  for (int y = blockIdx.x; y < P.H; y += gridDim.x) {
+#pragma unroll 2
+    for (int x = threadIdx.x; x < P.W; x += kEwThreads) {
+      const long po = (long)bt * HWp + (long)y * P.Wp + x;
+      const long d = (long)y * P.W + x;
+      float fb = __ldcs(P.Fbar + po);
+      if (P.xbar0) fb += __ldcs(P.xbar0 + po);
+      float cv[CMAX];
+      float z = P.bias;
 #pragma unroll
-    for (int c = 0; c < CMAX; ++c) {
-      cv[c] = (c < P.C) ? __ldg(chb + (long)c * vol) : 0.f;
-      z = fmaf(P.w[c], cv[c], z);  // w[c] == 0 for c >= C (host zero-fills)
-    }
-    float dphi = 1.f;
-    if (P.act == 1) {
-      const float s = 1.f / (1.f + expf(-z));
-      dphi = s * (1.f - s);
-    }
-    const double zb = (double)fb * (double)dphi;
+      for (int c = 0; c < CMAX; ++c) {
+        cv[c] = (c < P.C) ? __ldcs(chf + (long)c * vol + d) : 0.f;
+        z = fmaf(P.w[c], cv[c], z);  // w[c] == 0 for c >= C (host zero-fills)
+      }
+      float dphi = 1.f;
+      if (P.act == 1) {
+        const float sg = 1.f / (1.f + expf(-z));
+        dphi = sg * (1.f - sg);
+      }
+      const double zb = (double)fb * (double)dphi;
 #pragma unroll
-    for (int c = 0; c < CMAX; ++c) acc[c] += zb * (double)cv[c];
-    acc[CMAX] += zb;
+      for (int c = 0; c < CMAX; ++c) acc[c] += zb * (double)cv[c];
+      acc[CMAX] += zb;
+    }
   }
+  const long slot = (long)bt * gridDim.x + blockIdx.x;
 #pragma unroll
   for (int c = 0; c <= CMAX; ++c) {
     const double s = block_sum<kEwThreads>(acc[c], red);
-    if (threadIdx.x == 0) P.partials[(long)blockIdx.x * (CMAX + 1) + c] = s;
+    if (threadIdx.x == 0) P.partials[slot * (CMAX + 1) + c] = s;
   }
-  if (!last_block_arrive(P.counter, gridDim.x, &flag)) return;
+  if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
+  const long nslot = (long)gridDim.x * gridDim.y;
   for (int c = 0; c <= CMAX; ++c) {
-    const double tot = block_sum_array<kEwThreads>(P.partials + c, gridDim.x, CMAX + 1, red);
+    const double tot = block_sum_array<kEwThreads>(P.partials + c, nslot, CMAX + 1, red);
     if (threadIdx.x == 0) {
       if (c < P.C) P.out[c] = tot;
       if (c == CMAX) P.out[P.C] = tot;

@@ -277,7 +277,10 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
   size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max((size_t)P->G * kSpassPartSlots, (size_t)P->G3 * kF3dCW),
                                    2 * (size_t)P->BT * P->gx);
-  n_part = std::max<size_t>(n_part, (size_t)4 * num_sms() * (kMaxC + 1));
+  {  // backward contraction: one (C_pad + 1)-vector per (frame, block)
+    const int cpad = C <= 1 ? 1 : C <= 2 ? 2 : C <= 4 ? 4 : C <= 8 ? 8 : C <= 16 ? 16 : kMaxC;
+    n_part = std::max<size_t>(n_part, (size_t)P->BT * P->gx * (cpad + 1));
+  }
   P->n_part = n_part;
   size_t off = align_up(sizeof(WsHeader));
   P->off_sc = off;
@@ -1021,7 +1024,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
   cc.act = act;
   cc.bias = b;
   for (int c = 0; c < C; ++c) cc.w[c] = w_host[c];
-  const int G2 = 4 * num_sms();
+  const dim3 G2((unsigned)P.gx, (unsigned)P.BT);  // partials: BT * gx * (C+1) <= n_part (checked in make_plan)
   if (C <= 1) contract_kernel<1><<<G2, kEwThreads, 0, st>>>(cc);
   else if (C <= 2) contract_kernel<2><<<G2, kEwThreads, 0, st>>>(cc);
   else if (C <= 4) contract_kernel<4><<<G2, kEwThreads, 0, st>>>(cc);

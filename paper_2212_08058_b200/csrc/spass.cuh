@@ -246,7 +246,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
     const bool xfull = x + 4 <= W;
     const float4 msk = make_float4(1.f, (x + 1 < W) ? 1.f : 0.f, (x + 2 < W) ? 1.f : 0.f, (x + 3 < W) ? 1.f : 0.f);
     struct Pre {
-      float4 f[4], a[4], c[4];
+      float4 f[4], a[4], c[4], d[4], e[4];  // BWD: a = x_bar, c = u_{k-1}, d = u_{k-2} or x_0, e = F_bar
     };
     // issue the epilogue's global loads early so their latency overlaps the FMAs
     auto prefetch = [&](int m, Pre& pr) {
@@ -262,6 +262,9 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
           } else {
             pr.a[i] = *reinterpret_cast<const float4*>(out_ + off);
             pr.c[i] = *reinterpret_cast<const float4*>(P.u1 + off);
+            if (P.u2) pr.d[i] = *reinterpret_cast<const float4*>(P.u2 + off);
+            else if (P.x0p) pr.d[i] = *reinterpret_cast<const float4*>(P.x0p + off);
+            pr.e[i] = *reinterpret_cast<const float4*>(P.Fbar + off);
           }
         }
       }
@@ -311,15 +314,15 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
           const float4 xb = pr.a[i];
           const float4 u1 = pr.c[i];
           float4 xp;
-          if (P.u2) xp = f4_scale(f4_mul(f, *reinterpret_cast<const float4*>(P.u2 + off)), inv_nu_prev);
-          else if (P.x0p) xp = f4_mul(*reinterpret_cast<const float4*>(P.x0p + off), msk);
+          if (P.u2) xp = f4_scale(f4_mul(f, pr.d[i]), inv_nu_prev);
+          else if (P.x0p) xp = f4_mul(pr.d[i], msk);
           else xp = f;
           float4 yb;
           yb.x = (xb.x - f.x * u1.x * cn) * inv_nu;
           yb.y = (xb.y - f.y * u1.y * cn) * inv_nu;
           yb.z = (xb.z - f.z * u1.z * cn) * inv_nu;
           yb.w = (xb.w - f.w * u1.w * cn) * inv_nu;
-          float4 fb = *reinterpret_cast<const float4*>(P.Fbar + off);
+          float4 fb = pr.e[i];
           fb.x += yb.x * u1.x + xp.x * uu.x;
           fb.y += yb.y * u1.y + xp.y * uu.y;
           fb.z += yb.z * u1.z + xp.z * uu.z;
@@ -337,7 +340,9 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
     for (int n = 0; n < nxb; ++n) {
       const bool do_y = n >= PRO;
       Pre pre;
-      if (do_y) prefetch(n - PRO, pre);
+      // forward: the epilogue's loads before the x-pass; backward (five operands): after it,
+      // when the x-pass registers are free (the y-pass still covers their latency)
+      if (MODE == SP_FWD && do_y) prefetch(n - PRO, pre);
       const int row0 = gs + n * kM;
       const bool live = (row0 + kM > 0) && (row0 < H);
       const int sl = n % NSLOT;
@@ -383,6 +388,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
           if (dup) *reinterpret_cast<float4*>(r1 + Geo::XO * warp + 4 * q) = z;
         }
       }
+      if (MODE == SP_BWD && do_y) prefetch(n - PRO, pre);
       __syncthreads();  // stage consumed; ring slot visible
       if (live) {
         ++cseq;

@@ -84,3 +84,21 @@ def test_null_pointers_rejected_before_launch(lib):
     assert lib.sfseg_power_iterate_backward(None, 1, w, 0.0, 0, shp, g, 2, None, None, None, None, None,
                                             None, 0, None, None) == 1
     assert lib.sfseg_sync_status(None, None) == 1
+
+
+def test_full_and_online_workspace_validation(lib):
+    """Host-only validation of the §8(f) entry points (no device work)."""
+    g = sf.Gauss(2.0, 8.0)
+    shp = sf.Shape(1, 10, 32, 40)
+    n = C.c_size_t(0)
+    assert lib.sfseg_workspace_bytes_full(shp, 1, 2, g.c(), 5, C.byref(n)) == 0 and n.value > 0
+    full = n.value
+    assert lib.sfseg_workspace_bytes_full(shp, 0, 2, g.c(), 5, C.byref(n)) == 1   # Cs < 1
+    assert lib.sfseg_workspace_bytes_full(shp, 1, 200, g.c(), 5, C.byref(n)) == 8  # Cf > compiled max
+    assert lib.sfseg_workspace_bytes_full(shp, 1, 1, g.c(), 5, None) == 1
+    assert lib.sfseg_workspace_bytes_online(shp, 1, g.c(), 5, 4, C.byref(n)) == 0 and n.value > 0
+    assert lib.sfseg_workspace_bytes_online(shp, 1, g.c(), 5, 0, C.byref(n)) == 1  # q < 1
+    # the full operator needs 7 pitched volumes (U, F, a, v, ua, ub, uc)
+    assert full >= 7 * 10 * 32 * 40 * 4
+    assert lib.sfseg_set_algorithm(7) == 1
+    assert lib.sfseg_set_algorithm(0) == 0
