@@ -249,7 +249,6 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    sf.profile_enable(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -257,14 +256,24 @@ def run_ours(args):
         step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    sf.profile_enable(False)
-    prof = sf.profile_read()
     solver.sync()
     if world > 1:
         dist.barrier()
     time.sleep(0.1)
     clocks.stop()
     ms = e0.elapsed_time(e1)
+    # per-kernel durations for the roofline: a few extra steps with every pass launch bracketed
+    # by CUDA events on its stream (kept out of the timed region: events between launches
+    # defeat the programmatic dependent launch that overlaps a kernel's prologue with the
+    # previous kernel's tail)
+    prof_steps = max(1, min(3, args.steps))
+    sf.profile_enable(True)
+    for _ in range(prof_steps):
+        step()
+    torch.cuda.synchronize(dev)
+    sf.profile_enable(False)
+    prof = sf.profile_read()
+    prof = {k: (v[0] * args.steps / prof_steps, int(round(v[1] * args.steps / prof_steps))) for k, v in prof.items()}
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
