@@ -43,7 +43,7 @@ __host__ __device__ constexpr int f3d_th(int R) { return ((32 - 2 * R) / 4) * 4;
 __host__ __device__ constexpr int f3d_stages(int RT) { return 2 * RT + 1 + kF3dNPF; }
 __host__ __device__ constexpr size_t f3d_smem_bytes(int RT, int R) {
   return sizeof(float) * ((size_t)f3d_stages(RT) * (kM * f3d_boxw(R) + f3d_th(R) * kF3dTW) + (size_t)kF3dCW * kM * kF3dQS) +
-         2 * 8 * f3d_stages(RT) + 16 + 8 * kF3dCW;
+         2 * 8 * f3d_stages(RT) + 16 + 16 * kF3dCW;
 }
 __host__ __device__ constexpr int f3d_fit(size_t smem) {
   return (int)((227 * 1024) / (smem + 1024)) < 4 ? (int)((227 * 1024) / (smem + 1024)) : 4;
@@ -59,7 +59,7 @@ struct F3dParams {
   float* out;              // p_k (or y_k when last), pitched; must not alias the tmap source
   float* tape_u;           // record u (nullable)
   double* sc;              // per-volume scalars [B][kScal]  (SC_S = s_{k-1} read; finalize writes s_k)
-  double* partials;        // [2][B][G * kF3dCW]
+  double* partials;        // [2][B][G] (one slot per CTA)
   unsigned* counter;
   unsigned* err;
   double* stats;           // [B][K][3] (nullable)
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
   uint64_t* full = reinterpret_cast<uint64_t*>(qbuf + kF3dCW * kM * kF3dQS);
   uint64_t* empty = full + NS;
   int* flag = reinterpret_cast<int*>(empty + NS);
-  double* red = reinterpret_cast<double*>(flag + 4);  // kF3dCW doubles (finalize)
+  double* red = reinterpret_cast<double*>(flag + 4);  // 2 * kF3dCW doubles (partial fold, finalize)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = P.T, H = P.H, W = P.W, Wp = P.Wp;
@@ -164,16 +164,29 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
   double acc0 = 0.0, acc1 = 0.0;
   int cur_vol = -1;
   float s = 1.f;
-  const long nslots = (long)P.G * kF3dCW;
+  const long nslots = (long)P.G;  // partial slots per volume (one per CTA)
+  // one partial per CTA and volume (the last CTA then sums G, not G*4, values): the four
+  // compute warps reach the same volume boundaries, so the fold is a named-barrier step
   auto flush = [&](int vol) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
       acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
     }
+    f3d_compute_bar();  // red[] free (previous fold done)
     if (lane == 0) {
-      P.partials[(long)vol * nslots + (long)blockIdx.x * kF3dCW + warp] = acc0;
-      P.partials[(long)(P.B + vol) * nslots + (long)blockIdx.x * kF3dCW + warp] = acc1;
+      red[2 * warp] = acc0;
+      red[2 * warp + 1] = acc1;
+    }
+    f3d_compute_bar();
+    if (tid == 0) {
+      double t0 = 0.0, t1 = 0.0;
+      for (int w = 0; w < kF3dCW; ++w) {
+        t0 += red[2 * w];
+        t1 += red[2 * w + 1];
+      }
+      P.partials[(long)vol * nslots + blockIdx.x] = t0;
+      P.partials[(long)(P.B + vol) * nslots + blockIdx.x] = t1;
     }
     acc0 = acc1 = 0.0;
   };
@@ -331,11 +344,11 @@ __global__ void __launch_bounds__(kF3dThreads, f3d_ctas_per_sm(RT, R)) f3d_kerne
     vol_cta_range(b, per_vol, P.U, P.G, lo, hi);
     double s0, s1;
     if (wide) {
-      s0 = block_sum_range<kF3dCW * 32, 1>(P.partials + (long)b * nslots, lo * kF3dCW, hi * kF3dCW, 1, red);
-      s1 = block_sum_range<kF3dCW * 32, 1>(P.partials + (long)(P.B + b) * nslots, lo * kF3dCW, hi * kF3dCW, 1, red);
+      s0 = block_sum_range<kF3dCW * 32, 1>(P.partials + (long)b * nslots, lo, hi, 1, red);
+      s1 = block_sum_range<kF3dCW * 32, 1>(P.partials + (long)(P.B + b) * nslots, lo, hi, 1, red);
     } else {
-      s0 = warp_sum_range(P.partials + (long)b * nslots, lo * kF3dCW, hi * kF3dCW);
-      s1 = warp_sum_range(P.partials + (long)(P.B + b) * nslots, lo * kF3dCW, hi * kF3dCW);
+      s0 = warp_sum_range(P.partials + (long)b * nslots, lo, hi);
+      s1 = warp_sum_range(P.partials + (long)(P.B + b) * nslots, lo, hi);
     }
     if ((wide && tid == 0) || (!wide && lane == 0))
       fwd_finalize(P.sc + b * kScal, P.stats, P.tape_nu, P.err, P.K, P.k, P.rayleigh != 0, b, s0, s1);
