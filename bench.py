@@ -240,6 +240,23 @@ def run_ours(args):
         step()
     (fsolver.forward(ch, wl.w, f_ch, wl.extra["wf"], wl.extra["p"], wl.extra["alpha"], x_out=x) if full
      else solver.sync())   # raises on a device-detected error
+    timed_step = step
+    graph = None
+    if args.graph and not slab and not train:
+        # the whole step (every kernel of combine, K iterations, final scale, threshold) captured
+        # once into a CUDA graph and replayed: one launch per step from the host
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                step()
+        stream.wait_stream(cap)
+        torch.cuda.synchronize(dev)
+        timed_step = graph.replay
+        for _ in range(2):
+            timed_step()
+        torch.cuda.synchronize(dev)
 
     clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
                           if os.environ.get("CUDA_VISIBLE_DEVICES", "").isdigit() else local)
@@ -253,7 +270,7 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        step()
+        timed_step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     solver.sync()
@@ -421,7 +438,8 @@ def run_ours(args):
                        "iters": K, "tau": cfg.tau,
                        "parallelism": (f"time-slab x{world} (NCCL halo r_t frames + fp64 norm allreduce / iter)"
                                        if slab else f"dp{world} (one volume per GPU)"),
-                       "l2": "inputs > L2 (ch 115 MB + F/p/v 344 MB vs 126 MB L2); no flush"},
+                       "l2": "inputs > L2 (ch 115 MB + F/p/v 344 MB vs 126 MB L2); no flush",
+                       "launch": "one CUDA graph per step" if graph is not None else "stream launches"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": n_launch + (int(prof["backward"][1]) + 2 * args.steps if train else 0),
             "clocks": {k: ck[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
@@ -453,6 +471,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", type=int, default=0, help="1: replay the step as one captured CUDA graph")
     ap.add_argument("--shard", default="volume", choices=["volume", "slab"],
                     help="N>1: one volume per GPU (weak scaling) or time slabs of one volume with NCCL halos (strong)")
     args = ap.parse_args()
