@@ -33,6 +33,10 @@ METRIC = "voxel-iterations/sec (T*H*W*iters/s)"
 UNIT = "voxel-iterations/s"
 ALU_PEAK_FMA_PER_CLK_PER_SM = 128     # FP32 lanes per SM (B200_PROFILING.md / blackwell guide)
 SM_COUNT = 148
+# legacy warp-level HMMA (mma.sync m16n8k16 bf16, fp32 accumulate) full-chip rate measured by
+# tools/mma_microbench.cu on this pool's B200 (profiles/mma/mma.log): the ceiling of the
+# tensor-core spatial pass's instruction choice (a third of the tcgen05 dense bf16 peak)
+MMA_SYNC_BF16_TFLOPS = 555.6
 
 
 def _peaks():
@@ -213,6 +217,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     # the per-frame threshold (a9) is frame-local: each rank thresholds its own slab
+    path_info = sf.forward_path((B, T, H, W), gauss)
+    path_tc = path_info[0] == sf.PATH_TWO_PASS_TC
     thr_solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev) if slab else solver
 
     train = args.config == "c3" and not slab
@@ -365,6 +371,43 @@ def run_ours(args):
             "peak_source": f"{peaks_src} hbm_gbs (MEASURED_PEAKS.json)",
             "algorithmic_bytes_per_launch": f3_bytes, "launch_ms": f3_avg_s * 1e3, "launches": f3_n,
             "share_of_step": f3_ms / ms if ms > 0 else None,
+            "path_hbm_frac_algorithmic_12B": 12.0 * value / world / 1e9 / hbm_peak,
+        }
+    elif path_tc:
+        # tensor-core spatial pass: bound by HBM at speed of light (12 B/voxel: read v and F,
+        # write p = 53 us at c2) rather than by the tensor pipe (its banded bf16x3 products
+        # take 13.5 us at the measured dense bf16 peak); both reported
+        RSc = path_info[2]
+        ra = (RSc + 3) // 4 * 4
+        nkx, nky = (16 + ra + RSc + 15) // 16, (16 + 2 * RSc + 15) // 16
+        S_, NB_ = -(-W // 64), -(-H // 32)
+        tc_flops = float(B * T * S_ * NB_) * 48 * (nkx + nky) * 4096   # HMMA m16n8k16 = 4096 flop
+        # read v (+ F unless the full operator's plain pass), write p (+ the tape u for training)
+        sp_bytes = (8.0 + (0.0 if full else 4.0) + (4.0 if args.config == "c3" else 0.0)) * vox
+        bf16_peak = float(peaks.get("bf16_tflops", 2250.0))
+        try:
+            tc_traffic = json.load(open(tfile)).get(args.config, {}).get("spass_tc", {}).get("dram_bytes_per_launch")
+        except Exception:
+            tc_traffic = None
+        roofline = {
+            "kernel": f"spass_tc_kernel<R={RSc}> (x/y Gaussian as banded bf16x3 Toeplitz products on the "
+                      f"tensor pipe + F multiplies + norm)",
+            "bound": "hbm", "achieved": sp_bytes / sp_avg_s / 1e9 if sp_n else None, "peak": hbm_peak,
+            "unit": "GB/s", "frac": (sp_bytes / sp_avg_s / 1e9 / hbm_peak) if sp_n else None,
+            "traffic": tc_traffic,
+            "peak_source": f"{peaks_src} hbm_gbs (MEASURED_PEAKS.json)",
+            "algorithmic_bytes_per_launch": sp_bytes,
+            "launch_ms": sp_avg_s * 1e3, "launches": sp_n,
+            "share_of_step": sp_ms / ms if ms > 0 else None,
+            "tensor": {"hmma_flops_per_launch": tc_flops,
+                       "achieved_TFLOPs": tc_flops / sp_avg_s / 1e12 if sp_n else None,
+                       "peak_bf16_TFLOPs": bf16_peak, "peak_source": f"{peaks_src} bf16_tflops",
+                       "frac": (tc_flops / sp_avg_s / 1e12 / bf16_peak) if sp_n else None,
+                       "mma_sync_ceiling_TFLOPs": MMA_SYNC_BF16_TFLOPS,
+                       "useful_fp32_TFLOPs": flops_per_launch / sp_avg_s / 1e12 if sp_n else None},
+            "tpass": {"launch_ms": tp_avg_s * 1e3, "launches": tp_n,
+                      "achieved_GBps": tp_bytes / tp_avg_s / 1e9 if tp_n else None, "peak_GBps": hbm_peak,
+                      "bound": "hbm"},
             "path_hbm_frac_algorithmic_12B": 12.0 * value / world / 1e9 / hbm_peak,
         }
     else:

@@ -233,6 +233,10 @@ sfseg_status sfseg_profile_read(double* ms_host /*[6]*/, int64_t* count_host /*[
  * such a case), otherwise one temporal pass + one fused spatial pass per
  * iteration.
  * SFSEG_ALGO_TWO_PASS: always the two-pass iteration.
+ * The forward spatial pass of the two-pass iteration runs on the bf16 tensor
+ * pipe (3-product split, ~1e-5 relative, reading A23) for compiled
+ * spatial radii 8..48; SFSEG_ALGO_TWO_PASS_FP32 forces the two-pass iteration
+ * with the FP32-FMA spatial pass (the A/B and parity reference of that choice).
  * SFSEG_ALGO_MEGAKERNEL: for (r_s, r_t) in {(24,6), (18,5), (36,9)} without a
  * tape, all K iterations as one persistent wavefront kernel (temporal and
  * spatial work items overlapped, lagged normalisation); else as AUTO.  Measured
@@ -242,7 +246,20 @@ sfseg_status sfseg_profile_read(double* ms_host /*[6]*/, int64_t* count_host /*[
 #define SFSEG_ALGO_AUTO 0
 #define SFSEG_ALGO_TWO_PASS 1
 #define SFSEG_ALGO_MEGAKERNEL 2
+#define SFSEG_ALGO_TWO_PASS_FP32 3
 sfseg_status sfseg_set_algorithm(int32_t algo);
+
+/* ---- plan introspection ----
+ * The forward path sfseg_power_iterate takes for this shape and Gaussian on one
+ * GPU without a tape, under the current sfseg_set_algorithm (a tape forces the
+ * two-pass iteration): info_host[0] = SFSEG_PATH_*, [1] = compiled temporal
+ * radius, [2] = compiled spatial radius.  Host only, no device work.
+ * Errors: SFSEG_ERR_INVALID_ARGUMENT / SFSEG_ERR_SHAPE as sfseg_workspace_bytes. */
+#define SFSEG_PATH_TWO_PASS_FP32 0
+#define SFSEG_PATH_TWO_PASS_TC 1
+#define SFSEG_PATH_FUSED_3D 2
+#define SFSEG_PATH_MEGAKERNEL 3
+sfseg_status sfseg_forward_path(sfseg_shape shape, sfseg_gauss gauss, int32_t* info_host /*[3]*/);
 
 /* ---- multi-GPU communicator (NCCL, loaded at run time with dlopen) ---- */
 /* Multi-GPU solve: call sfseg_power_iterate with dist_or_null = {comm, T_global,

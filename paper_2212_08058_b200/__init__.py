@@ -89,6 +89,7 @@ _SIGS = {
     "sfseg_profile_enable": (C.c_int, [C.c_int32]),
     "sfseg_profile_read": (C.c_int, [_P, _P]),
     "sfseg_set_algorithm": (C.c_int, [C.c_int32]),
+    "sfseg_forward_path": (C.c_int, [Shape, GaussC, C.POINTER(C.c_int32)]),
     "sfseg_workspace_bytes_online": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
     "sfseg_power_iterate_online": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                              C.c_int32, C.c_int32, _P, _P, C.c_size_t, _P]),
@@ -172,12 +173,29 @@ def profile_read():
 ALGO_AUTO = 0
 ALGO_TWO_PASS = 1
 ALGO_MEGAKERNEL = 2
+ALGO_TWO_PASS_FP32 = 3
+
+
+PATH_TWO_PASS_FP32 = 0
+PATH_TWO_PASS_TC = 1
+PATH_FUSED_3D = 2
+PATH_MEGAKERNEL = 3
+
+
+def forward_path(shape, gauss) -> tuple:
+    """(path, compiled r_t, compiled r_s) of the single-GPU forward without a tape under
+    the current set_algorithm: path is one of PATH_* (host-side plan, no device work)."""
+    info = (C.c_int32 * 3)()
+    _check(lib().sfseg_forward_path(Shape(*shape), gauss.c(), info), "sfseg_forward_path")
+    return int(info[0]), int(info[1]), int(info[2])
 
 
 def set_algorithm(algo: int) -> None:
     """Forward-path selection: ALGO_AUTO (fused single-pass 3D kernel for small
     radii, else two-pass), ALGO_TWO_PASS (always temporal + spatial pass) or
-    ALGO_MEGAKERNEL (all iterations in one persistent launch, large radii)."""
+    ALGO_MEGAKERNEL (all iterations in one persistent launch, large radii) or
+    ALGO_TWO_PASS_FP32 (two-pass with the FP32-FMA spatial pass instead of the
+    tensor-core one)."""
     _check(lib().sfseg_set_algorithm(int(algo)), "sfseg_set_algorithm")
 
 

@@ -57,6 +57,19 @@ __device__ __forceinline__ float f4_dot(float4 a, float4 b) {
   return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
 }
 
+// (a, b) -> hi = bf16x2(a, b), lo = bf16x2 of the residuals (a in the low half):
+// a = hi + lo to 2^-18 relative (two F2FP, one shift + one LOP3 to widen hi, two FADD).
+// The operand split of the tensor-core spatial pass (spass_tc.cuh, A23).
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  uint32_t h;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+  const float ha = __uint_as_float(h << 16), hb = __uint_as_float(h & 0xffff0000u);
+  uint32_t l;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(b - hb), "f"(a - ha));
+  hi = h;
+  lo = l;
+}
+
 // Deterministic block sum of per-thread doubles (fixed tree).  All threads get the
 // result.  BAR = 0: the whole CTA (__syncthreads); BAR > 0: the named barrier BAR over
 // the first NT threads only (kernels whose producer warp has already exited).

@@ -14,6 +14,10 @@ cudaError_t launch_spass_bwd(int R, const SpassParams& P, int grid, cudaStream_t
 cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_fwdf(int RT, const TpassParams& P, int B, cudaStream_t st);
+bool spass_tc_supported(int R);
+int spass_tc_occupancy(int R);
+int spass_tc_boxw(int R);
+cudaError_t launch_spass_tc(int R, const SpassParams& P, int grid, cudaStream_t st);
 bool f3d_supported(int RT, int R);
 int f3d_occupancy(int RT, int R);
 cudaError_t launch_f3d(int RT, int R, const F3dParams& P, int grid, cudaStream_t st);

@@ -221,6 +221,8 @@ struct Plan {
   int NB;             // 32-row blocks per column
   int64_t U;          // spass block units
   int G;              // spass grid
+  bool tc;            // forward spatial pass on the tensor cores (spass_tc_kernel)
+  int Gtc;            // its grid
   int gx;             // elementwise grid.x per frame
   bool f3d;           // single-pass fused 3D kernel (small radii) for the single-GPU forward
   int TX, TY;         // f3d tiles per frame (64 columns x f3d_th(RS) rows)
@@ -264,7 +266,9 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   const int64_t cap = (int64_t)num_sms() * spass_occupancy(P->RS);
   P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 4));
   P->gx = ew_gx(P->H, P->BT);
-  P->f3d = g_algorithm != SFSEG_ALGO_TWO_PASS && f3d_supported(P->RT, P->RS);
+  P->tc = g_algorithm != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
+  P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * spass_tc_occupancy(P->RS), P->U / 4));
+  P->f3d = (g_algorithm == SFSEG_ALGO_AUTO || g_algorithm == SFSEG_ALGO_MEGAKERNEL) && f3d_supported(P->RT, P->RS);
   P->TX = (int)((sh.W + kF3dTW - 1) / kF3dTW);
   P->TY = (int)((sh.H + f3d_th(std::min(P->RS, kF3dMaxR)) - 1) / f3d_th(std::min(P->RS, kF3dMaxR)));
   P->U3 = P->B * P->TY * P->TX * P->T;
@@ -275,7 +279,7 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->NCOLS = 4;
   P->NCC = (int)((P->H * P->Wp / 4 + 128 * P->NCOLS - 1) / (128 * P->NCOLS));
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
-  size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max((size_t)P->G * kSpassPartSlots, (size_t)P->G3 * kF3dCW),
+  size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max({(size_t)P->G * kSpassPartSlots, (size_t)P->Gtc, (size_t)P->G3 * kF3dCW}),
                                    2 * (size_t)P->BT * P->gx);
   {  // backward contraction: one (C_pad + 1)-vector per (frame, block)
     const int cpad = C <= 1 ? 1 : C <= 2 ? 2 : C <= 4 ? 4 : C <= 8 ? 8 : C <= 16 ? 16 : kMaxC;
@@ -380,6 +384,20 @@ void fill_spass_common(SpassParams& sp, const Plan& P, void* ws) {
   for (int d = 0; d <= P.RS; ++d) sp.g[d] = P.gs[P.RS + d];
 }
 
+// Forward spatial pass: the tensor-core kernel when the plan selected it, else the FP32 one.
+// Input descriptor of the forward spatial pass over v (box width of the selected kernel).
+bool make_spass_fwd_tmap(CUtensorMap* map, const Plan& P, const float* v) {
+  return make_volume_tmap(map, v, P.W, P.H, P.BT, P.Wp, P.tc ? spass_tc_boxw(P.RS) : spass_boxw(P.RS));
+}
+cudaError_t launch_spass_forward(const Plan& P, SpassParams& sp, cudaStream_t st) {
+  if (P.tc) {
+    sp.G = P.Gtc;
+    return launch_spass_tc(P.RS, sp, P.Gtc, st);
+  }
+  sp.G = P.G;
+  return launch_spass_fwd(P.RS, sp, P.G, st);
+}
+
 void fill_tpass_common(TpassParams& tp, const Plan& P, void* ws) {
   tp.sc = at<double>(ws, P.off_sc);
   tp.frame4 = P.H * P.Wp / 4;
@@ -455,7 +473,7 @@ sfseg_status rank_setup(Rank& r, cudaStream_t st) {
   r.glob = at<double>(r.ws, r.so.off_glob);
   SF_CUDA(cudaMemsetAsync(r.ws, 0, P.off_part, st));
   std::memset(&r.sp, 0, sizeof(r.sp));
-  if (!make_volume_tmap(&r.sp.tmap, r.v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+  if (!make_spass_fwd_tmap(&r.sp.tmap, P, r.v)) return SFSEG_ERR_CUDA;
   fill_spass_common(r.sp, P, r.ws);
   r.sp.stats = r.stats;
   r.sp.loc = r.loc;
@@ -511,7 +529,7 @@ sfseg_status ph_S(Rank& r, int k, cudaStream_t st) {
   r.sp.k = k;
   r.sp.last = (k == r.P.K) ? 1 : 0;
   ProfScope ps(st, PC_SPASS);
-  SF_CUDA(launch_spass_fwd(r.P.RS, r.sp, r.P.G, st));
+  SF_CUDA(launch_spass_forward(r.P, r.sp, st));
   SF_CUDA(after_launch("spass(slab)", st));
   return SFSEG_OK;
 }
@@ -654,8 +672,21 @@ int32_t sfseg_abi_version(void) { return SFSEG_ABI_VERSION; }
 
 const char* sfseg_last_cuda_error(void) { return cudaGetErrorString(last_cuda_error()); }
 
+sfseg_status sfseg_forward_path(sfseg_shape sh, sfseg_gauss g, int32_t* info) {
+  if (!info) return SFSEG_ERR_INVALID_ARGUMENT;
+  Plan P;
+  sfseg_status s = make_plan(sh, 1, g, 1, &P);
+  if (s != SFSEG_OK) return s;
+  info[0] = P.f3d ? SFSEG_PATH_FUSED_3D : P.mk ? SFSEG_PATH_MEGAKERNEL : P.tc ? SFSEG_PATH_TWO_PASS_TC
+                                                                            : SFSEG_PATH_TWO_PASS_FP32;
+  info[1] = P.RT;
+  info[2] = P.RS;
+  return SFSEG_OK;
+}
+
 sfseg_status sfseg_set_algorithm(int32_t algo) {
-  if (algo != SFSEG_ALGO_AUTO && algo != SFSEG_ALGO_TWO_PASS && algo != SFSEG_ALGO_MEGAKERNEL)
+  if (algo != SFSEG_ALGO_AUTO && algo != SFSEG_ALGO_TWO_PASS && algo != SFSEG_ALGO_MEGAKERNEL &&
+      algo != SFSEG_ALGO_TWO_PASS_FP32)
     return SFSEG_ERR_INVALID_ARGUMENT;
   g_algorithm = algo;
   return SFSEG_OK;
@@ -881,7 +912,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
 
   SpassParams sp;
   std::memset(&sp, 0, sizeof(sp));
-  if (!make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+  if (!make_spass_fwd_tmap(&sp.tmap, P, v)) return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.stats = stats;
   sp.tape_nu = tape_nu;
@@ -906,7 +937,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     sp.last = (k == K) ? 1 : 0;
     {
       ProfScope ps(st, PC_SPASS);
-      SF_CUDA(launch_spass_fwd(P.RS, sp, P.G, st));
+      SF_CUDA(launch_spass_forward(P, sp, st));
       SF_CUDA(after_launch("spass_fwd", st));
     }
   }
@@ -1143,7 +1174,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
 
   SpassParams sp;
   std::memset(&sp, 0, sizeof(sp));
-  if (!make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+  if (!make_spass_fwd_tmap(&sp.tmap, P, v)) return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.plain = 1;
   TpassParams tp;
@@ -1190,7 +1221,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
       sp.k = k;
       {
         ProfScope ps(st, PC_SPASS);
-        SF_CUDA(launch_spass_fwd(P.RS, sp, P.G, st));
+        SF_CUDA(launch_spass_forward(P, sp, st));
         SF_CUDA(after_launch("spass_plain", st));
       }
     }

@@ -126,6 +126,41 @@ __device__ __forceinline__ void bwd_finalize(double* sc, const double* tape_nu, 
   }
 }
 
+// Last CTA of a spatial-pass launch: fixed-order fp64 reduction of the per-CTA
+// partials of each volume (a contiguous CTA range) and the per-volume finalize.
+template <int MODE, int NT>
+__device__ __forceinline__ void spass_finalize(const SpassParams& P, double* red, int* flag) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!last_block_arrive(P.counter, (unsigned)P.G, flag)) return;
+  const long per_vol = P.U / P.B;  // units per volume
+  // few volumes: the whole CTA sums each volume's partials; many volumes: one warp each
+  const bool wide = P.B < NW;
+  for (int b = wide ? 0 : warp; b < P.B; b += wide ? 1 : NW) {
+    long lo, hi;
+    vol_cta_range(b, per_vol, P.U, P.G, lo, hi);
+    double s0, s1;
+    if (wide) {
+      s0 = block_sum_range<NT>(P.partials + (long)b * P.G, lo, hi, 1, red);
+      s1 = block_sum_range<NT>(P.partials + (long)(P.B + b) * P.G, lo, hi, 1, red);
+    } else {
+      s0 = warp_sum_range(P.partials + (long)b * P.G, lo, hi);
+      s1 = warp_sum_range(P.partials + (long)(P.B + b) * P.G, lo, hi);
+    }
+    if ((wide && tid == 0) || (!wide && lane == 0)) {
+      if (P.loc) {
+        P.loc[2 * b] = s0;
+        P.loc[2 * b + 1] = s1;
+      } else if (MODE == SP_FWD) {
+        fwd_finalize(P.sc + b * kScal, P.stats, P.tape_nu, P.err, P.K, P.k, P.pprev != nullptr, b, s0, s1);
+      } else {
+        bwd_finalize(P.sc + b * kScal, P.tape_nu, P.K, P.k, b, s0);
+      }
+    }
+  }
+  if (tid == 0) *P.counter = 0u;
+}
+
 template <int R>
 struct SpassGeom {
   static constexpr int BOXW = spass_boxw(R);
@@ -421,7 +456,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
   double* red = reinterpret_cast<double*>(bars + 2);
   int* flag = reinterpret_cast<int*>(red + 8);
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const long u_begin = (long)blockIdx.x * P.U / P.G;
   const long u_end = (long)(blockIdx.x + 1) * P.U / P.G;
 
@@ -443,34 +478,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_kernel(const __grid_co
   }, P.out, P.pprev, P.tape_u, P.last);
 
   if (P.plain) return;  // no norm in the plain (full-operator) mode
-  // ---------------------------------------------------------------- last CTA: fixed-order fp64 finalize
-  if (!last_block_arrive(P.counter, (unsigned)P.G, flag)) return;
-  const long per_vol = P.U / P.B;  // units per volume
-  // few volumes: the whole CTA sums each volume's partials; many volumes: one warp each
-  const bool wide = P.B < kSpassWarps;
-  for (int b = wide ? 0 : warp; b < P.B; b += wide ? 1 : kSpassWarps) {
-    long lo, hi;
-    vol_cta_range(b, per_vol, P.U, P.G, lo, hi);
-    double s0, s1;
-    if (wide) {
-      s0 = block_sum_range<kSpassThreads>(P.partials + (long)b * P.G, lo, hi, 1, red);
-      s1 = block_sum_range<kSpassThreads>(P.partials + (long)(P.B + b) * P.G, lo, hi, 1, red);
-    } else {
-      s0 = warp_sum_range(P.partials + (long)b * P.G, lo, hi);
-      s1 = warp_sum_range(P.partials + (long)(P.B + b) * P.G, lo, hi);
-    }
-    if ((wide && tid == 0) || (!wide && lane == 0)) {
-      if (P.loc) {
-        P.loc[2 * b] = s0;
-        P.loc[2 * b + 1] = s1;
-      } else if (MODE == SP_FWD) {
-        fwd_finalize(P.sc + b * kScal, P.stats, P.tape_nu, P.err, P.K, P.k, P.pprev != nullptr, b, s0, s1);
-      } else {
-        bwd_finalize(P.sc + b * kScal, P.tape_nu, P.K, P.k, b, s0);
-      }
-    }
-  }
-  if (tid == 0) *P.counter = 0u;
+  spass_finalize<MODE, kSpassThreads>(P, red, flag);
 }
 
 }  // namespace sfseg

@@ -1,0 +1,66 @@
+// Tensor-core forward spatial-pass instantiations (spass_tc.cuh).
+#include "launch.h"
+#include "spass_tc.cuh"
+
+namespace sfseg {
+namespace {
+template <int R>
+cudaError_t launch_tc_one(const SpassParams& P, int grid, cudaStream_t st) {
+  const size_t smem = sptc_smem_bytes(R);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(spass_tc_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  spass_tc_kernel<R><<<grid, kSpassThreads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+}  // namespace
+
+#define SPTC_RADII(X) X(8) X(9) X(12) X(16) X(18) X(24) X(32) X(36) X(48)
+
+bool spass_tc_supported(int R) {
+  switch (R) {
+#define TC_SUP(r) case r:
+    SPTC_RADII(TC_SUP)
+#undef TC_SUP
+    return true;
+    default:
+      return false;
+  }
+}
+int spass_tc_occupancy(int R) {
+  switch (R) {
+#define TC_OCC(r) \
+  case r:         \
+    return sptc_ctas_per_sm(r);
+    SPTC_RADII(TC_OCC)
+#undef TC_OCC
+    default:
+      return 1;
+  }
+}
+int spass_tc_boxw(int R) {
+  switch (R) {
+#define TC_BW(r) \
+  case r:        \
+    return sptc_boxw(r);
+    SPTC_RADII(TC_BW)
+#undef TC_BW
+    default:
+      return 0;
+  }
+}
+cudaError_t launch_spass_tc(int R, const SpassParams& P, int grid, cudaStream_t st) {
+  switch (R) {
+#define TC_CASE(r) \
+  case r:          \
+    return launch_tc_one<r>(P, grid, st);
+    SPTC_RADII(TC_CASE)
+#undef TC_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+}  // namespace sfseg

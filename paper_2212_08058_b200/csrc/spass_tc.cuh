@@ -1,0 +1,393 @@
+// Tensor-core spatial pass (forward): the x and y Gaussians of G_3D
+// as banded Toeplitz products on the warp-level bf16 tensor pipe (mma.sync
+// m16n8k16 -> HMMA), fused with the F multiplies and the norm partials (Eq.8)
+// exactly like spass_kernel, which stays the FP32-FMA path (backward, megakernel,
+// and SFSEG_ALGO_TWO_PASS_FP32).
+//
+// Why: at radius 24 the FP32 pass does 98 FMA per voxel and is ALU-bound (49 % of
+// the FP32 peak, profiles/r01_final); the tensor pipe does the same contraction
+// with 3 bf16 products per tap (measured mma.sync bf16 rate 555 TFLOP/s, 7.5x the
+// FP32 peak; tools/mma_microbench.cu, profiles/mma).
+//
+// Precision (reading A23): every operand a is split a = a_hi + a_lo with
+// a_hi = bf16(a), a_lo = bf16(a - a_hi) (|a - a_hi - a_lo| <= 2^-18 |a|), the same for
+// the taps g; each product is a_hi g_hi + a_lo g_hi + a_hi g_lo (the dropped
+// a_lo g_lo <= 2^-18), accumulated in fp32 by the tensor core: relative error per
+// output ~1e-5 worst case, far inside the 1e-4 x_K tolerance.
+//
+// Tiling.  Same work list, segments, TMA producer, ring streaming and finalize as
+// spass_kernel (spass.cuh header), with:
+//   x-pass: D[16 rows x 8 cols] += A[16 rows x 16 box cols] * Tx[16 x 8]; the
+//     Toeplitz slice Tx depends only on the output tile's parity (8-column shift
+//     inside a 16-column k block) and the k step, so its bf16 fragments live in
+//     registers for the whole kernel; warp w: rows 16 (w & 1).., columns 32 (w >> 1)..
+//   ring: x-pass output as two bf16 planes (hi, lo), row-major, row stride 72
+//     (conflict-free u32 stores and ldmatrix); the x-block grid starts R rows above
+//     the segment so every y window of a 16-row output tile is 16-aligned and never
+//     straddles a 32-row slot: no duplicated rows.
+//   y-pass: D[16 out rows x 8 cols] += Ty[16 x 16 ring rows] * Ring[16 x 8]; Ty
+//     fragments (shift invariant) in shared memory, Ring fragments by
+//     ldmatrix.x4.trans.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "spass.cuh"
+
+namespace sfseg {
+
+constexpr int kTcRingStride = 72;  // bf16 per ring row (64 + 8: conflict-free)
+
+__host__ __device__ constexpr int sptc_nkx(int R) { return (16 + spass_ra(R) + R + 15) / 16; }
+__host__ __device__ constexpr int sptc_nky(int R) { return (16 + 2 * R + 15) / 16; }
+__host__ __device__ constexpr int sptc_boxw(int R) { return 16 * (3 + sptc_nkx(R)) + 8; }  // == 8 or 24 mod 32
+__host__ __device__ constexpr int sptc_pro(int R) { return (31 + 2 * R) / 32; }
+__host__ __device__ constexpr int sptc_nslot(int R) { return sptc_pro(R) + 1; }
+__host__ __device__ constexpr size_t sptc_smem_for(int R, int stages) {
+  return sizeof(float) * (size_t)stages * kM * sptc_boxw(R)                       // TMA stages
+         + 2 * sizeof(uint16_t) * (size_t)sptc_nslot(R) * kM * kTcRingStride  // ring (hi, lo)
+         + (size_t)sptc_nky(R) * 2 * 32 * 16                                   // Ty fragments
+         + 2 * 8 + 8 * 8 + 16;
+}
+__host__ __device__ constexpr int sptc_stages(int R) { return spass_fit_n(sptc_smem_for(R, 2)) >= 2 ? 2 : 1; }
+__host__ __device__ constexpr size_t sptc_smem_bytes(int R) { return sptc_smem_for(R, sptc_stages(R)); }
+__host__ __device__ constexpr int sptc_ctas_per_sm(int R) {
+  return spass_fit_n(sptc_smem_bytes(R)) < 3 ? spass_fit_n(sptc_smem_bytes(R)) : 3;
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                              uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// weight of spatial offset d (zero outside the support)
+__device__ __forceinline__ float sptc_w(const SpassParams& P, int d, int R) {
+  const int a = d < 0 ? -d : d;
+  return a <= R ? P.g[a] : 0.f;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid_constant__ SpassParams P) {
+  constexpr int BOXW = sptc_boxw(R);
+  constexpr int RA = spass_ra(R);
+  constexpr int NKX = sptc_nkx(R);
+  constexpr int NKY = sptc_nky(R);
+  constexpr int PRO = sptc_pro(R);
+  constexpr int NSLOT = sptc_nslot(R);
+  constexpr int NST = sptc_stages(R);
+  constexpr int RSW = kTcRingStride / 2;  // ring row stride in u32 words
+  constexpr int PLANE = NSLOT * kM * RSW;  // words per ring plane
+  constexpr unsigned STAGE_BYTES = kM * BOXW * sizeof(float);
+  static_assert(BOXW <= 256, "TMA box width limit");
+  static_assert(16 * NKY <= 16 + 32 * PRO, "y windows stay inside the live ring slots");
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* stage = reinterpret_cast<float*>(smem);                          // [NST][32][BOXW]
+  uint32_t* ring = reinterpret_cast<uint32_t*>(stage + NST * kM * BOXW);  // [2 planes][NSLOT*32][RSW]
+  uint4* tyf = reinterpret_cast<uint4*>(ring + 2 * PLANE);                 // [NKY][2][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tyf + NKY * 2 * 32);
+  double* red = reinterpret_cast<double*>(bars + 2);
+  int* flag = reinterpret_cast<int*>(red + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mt = warp & 1;  // 16-row half of the 32-row block
+  const int hh = warp >> 1; // 32-column half of the 64-column strip
+  const int H = P.H, W = P.W, Wp = P.Wp, S = P.S, T = P.T, NB = P.NB;
+  const long u_begin = (long)blockIdx.x * P.U / P.G;
+  const long u_end = (long)(blockIdx.x + 1) * P.U / P.G;
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+    prefetch_tmap(&P.tmap);
+  }
+  // Ty fragments (A operand of the y-pass): A[i][kk] = w(16 s + kk - i - R)
+  for (int idx = tid; idx < NKY * 2 * 32; idx += kSpassThreads) {
+    const int s = idx / 64, pl = (idx >> 5) & 1, l = idx & 31;
+    const int gi = l >> 2, ti = l & 3;
+    uint32_t v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = gi + 8 * (j & 1);
+      const int kk = 16 * s + 2 * ti + 8 * (j >> 1);
+      uint32_t hi, lo;
+      split_bf16x2(sptc_w(P, kk - i - R, R), sptc_w(P, kk + 1 - i - R, R), hi, lo);
+      v[j] = pl ? lo : hi;
+    }
+    tyf[idx] = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  // Tx fragments (B operand of the x-pass), registers: B[kk][jj] = w(16 s + kk - jj - 8 par - RA)
+  uint32_t bxh[2][NKX][2], bxl[2][NKX][2];
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int s = 0; s < NKX; ++s)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int d = 16 * s + 2 * t + 8 * j - g - 8 * par - RA;
+        split_bf16x2(sptc_w(P, d, R), sptc_w(P, d + 1, R), bxh[par][s][j], bxl[par][s][j]);
+      }
+  __syncthreads();
+
+  // ---- producer (thread 0): the x-block sequence of the CTA's unit range
+  long pu = u_begin;
+  Seg pseg{};
+  int pn = 0, pnx = 0, pgs = 0;
+  unsigned pseq = 0;
+  auto producer_next = [&]() {
+    while (pu < u_end) {
+      if (pn == 0) {
+        pseg = seg_decode(pu, u_end, NB, S);
+        pnx = (pseg.yb1 - pseg.yb0) + PRO;
+        pgs = pseg.yb0 * kM - R;
+      }
+      const int row0 = pgs + pn * kM;
+      if (++pn == pnx) {
+        pn = 0;
+        pu += pseg.yb1 - pseg.yb0;
+      }
+      if (row0 + kM > 0 && row0 < H) {
+        const int st = (NST == 2) ? (pseq & 1) : 0;
+        ++pseq;
+        mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
+        tma_load_3d(stage + st * kM * BOXW, &P.tmap, &bars[st], pseg.s * kTW - RA, row0, pseg.bt);
+        return;
+      }
+    }
+  };
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) producer_next();
+  }
+
+  const bool plain = P.plain != 0;
+  float* const out = P.out;
+  const float* const pprev = P.pprev;
+  float* const tape = P.tape_u;
+  const int last = P.last;
+  double acc0 = 0.0, acc1 = 0.0;
+  int cur_vol = -1;
+  auto flush = [&](int vol) {
+    const double s0 = block_sum<kSpassThreads>(acc0, red);
+    const double s1 = block_sum<kSpassThreads>(acc1, red);
+    if (tid == 0) {
+      P.partials[(long)vol * P.G + blockIdx.x] = s0;
+      P.partials[(long)(P.B + vol) * P.G + blockIdx.x] = s1;
+    }
+    acc0 = acc1 = 0.0;
+  };
+  // ldmatrix lane address parts: matrix mi = lane >> 3 (k half = mi & 1, n tile = mi >> 1)
+  const int lm_row = (lane & 7) + 8 * ((lane >> 3) & 1);
+  const int lm_nt = lane >> 4;
+  const uint32_t ring_s = smem_u32(ring);
+
+  unsigned cseq = 0;
+  long u = u_begin;
+  while (u < u_end) {
+    const Seg sg = seg_decode(u, u_end, NB, S);
+    const int nyb = sg.yb1 - sg.yb0;
+    const int nxb = nyb + PRO;
+    const int gs = sg.yb0 * kM - R;
+    const int yend = min(sg.yb1 * kM, H);
+    const int vol = sg.bt / T;
+    if (vol != cur_vol) {
+      if (cur_vol >= 0) flush(cur_vol);
+      cur_vol = vol;
+    }
+    const int c0 = sg.s * kTW;
+    const bool wlive = c0 + 32 * hh < W;  // this warp's 32 columns exist (ragged strip)
+
+    // epilogue geometry: thread element (nl, i) = row 16 mt + g + 8 i, column c0 + 32 hh + 8 nl + 2 t
+    const int xt = c0 + 32 * hh + 2 * t;
+    float2 cmask[4];  // columns < W (pad columns and beyond: 0)
+    bool cst[4];      // pair inside the pitched row (store allowed)
+#pragma unroll
+    for (int nl = 0; nl < 4; ++nl) {
+      const int x = xt + 8 * nl;
+      cst[nl] = x < Wp;
+      cmask[nl] = make_float2(x < W ? 1.f : 0.f, x + 1 < W ? 1.f : 0.f);
+    }
+    struct Pre {
+      float2 f[4][2], a[4][2];
+    };
+    auto row_base = [&](int m) -> long { return ((long)sg.bt * H + (sg.yb0 + m) * kM + 16 * mt + g) * Wp + xt; };
+    auto prefetch = [&](int m, Pre& pr) {
+      const int yb = (sg.yb0 + m) * kM + 16 * mt + g;
+      const long base = row_base(m);
+      const float* fb = P.F + base;
+      const float* ab = pprev + base;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const bool rok = yb + 8 * i < yend;
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl) {
+          pr.f[nl][i] = pr.a[nl][i] = make_float2(0.f, 0.f);
+          if (rok && cst[nl]) {
+            pr.f[nl][i] = *reinterpret_cast<const float2*>(fb + (long)8 * i * Wp + 8 * nl);
+            if (pprev) pr.a[nl][i] = __ldcg(reinterpret_cast<const float2*>(ab + (long)8 * i * Wp + 8 * nl));
+          }
+        }
+      }
+    };
+    auto ypass = [&](int m, const Pre& pr) {
+      float acc[4][4];
+#pragma unroll
+      for (int nl = 0; nl < 4; ++nl)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[nl][i] = 0.f;
+      // ring slot of each x-block of this y window (x-blocks m .. m + PRO)
+      uint32_t slot_addr[PRO + 1];
+      {
+        const int sm = m % NSLOT;
+#pragma unroll
+        for (int j = 0; j <= PRO; ++j) {
+          const int sj = sm + j < NSLOT ? sm + j : sm + j - NSLOT;
+          slot_addr[j] = ring_s + 4u * (uint32_t)((sj * kM + lm_row) * RSW + 4 * (4 * hh + lm_nt));
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < NKY; ++s) {
+        const uint4 ah = tyf[(2 * s) * 32 + lane];
+        const uint4 al = tyf[(2 * s + 1) * 32 + lane];
+        // window rows 16 mt + 16 s ..: x-block (16 mt + 16 s) >> 5 of the window, mt runtime
+        const uint32_t sa = (mt ? slot_addr[(16 + 16 * s) >> 5] + 4u * (uint32_t)(((16 + 16 * s) & 31) * RSW)
+                                : slot_addr[(16 * s) >> 5] + 4u * (uint32_t)(((16 * s) & 31) * RSW));
+        uint32_t bh[8], bl[8];  // B fragments of the four n tiles (2 regs each), hi and lo planes
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {
+          const uint32_t addr = sa + 4u * (uint32_t)(8 * pp);
+          ldsm_x4_trans(addr, bh[4 * pp], bh[4 * pp + 1], bh[4 * pp + 2], bh[4 * pp + 3]);
+          ldsm_x4_trans(addr + 4u * PLANE, bl[4 * pp], bl[4 * pp + 1], bl[4 * pp + 2], bl[4 * pp + 3]);
+        }
+        // product-major order: consecutive HMMAs write different accumulators
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl) mma16816(acc[nl], ah.x, ah.y, ah.z, ah.w, bh[2 * nl], bh[2 * nl + 1]);
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl) mma16816(acc[nl], ah.x, ah.y, ah.z, ah.w, bl[2 * nl], bl[2 * nl + 1]);
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl) mma16816(acc[nl], al.x, al.y, al.z, al.w, bh[2 * nl], bh[2 * nl + 1]);
+      }
+      // epilogue
+      float s0 = 0.f, s1 = 0.f;
+      const int yb = (sg.yb0 + m) * kM + 16 * mt + g;
+      const long base = row_base(m);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const bool rok = yb + 8 * i < yend;
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl) {
+          if (!(rok && cst[nl])) continue;
+          const long off = base + (long)8 * i * Wp + 8 * nl;
+          const float2 uu = make_float2(acc[nl][2 * i] * cmask[nl].x, acc[nl][2 * i + 1] * cmask[nl].y);
+          if (plain) {
+            *reinterpret_cast<float2*>(out + off) = uu;
+            continue;
+          }
+          const float2 f = pr.f[nl][i];
+          const float2 yv = make_float2(f.x * uu.x, f.y * uu.y);
+          s0 = fmaf(yv.x, yv.x, fmaf(yv.y, yv.y, s0));
+          if (pprev) s1 = fmaf(pr.a[nl][i].x, uu.x, fmaf(pr.a[nl][i].y, uu.y, s1));
+          if (tape) *reinterpret_cast<float2*>(tape + off) = uu;
+          *reinterpret_cast<float2*>(out + off) = last ? yv : make_float2(f.x * yv.x, f.y * yv.y);
+        }
+      }
+      acc0 += (double)s0;
+      acc1 += (double)s1;
+    };
+
+    for (int n = 0; n < nxb; ++n) {
+      const bool do_y = n >= PRO;
+      Pre pre;
+      if (do_y && wlive) prefetch(n - PRO, pre);
+      const int row0 = gs + n * kM;
+      const bool live = (row0 + kM > 0) && (row0 < H);
+      const int slot_row = (n % NSLOT) * kM + 16 * mt + g;
+      if (wlive) {
+        float acc[4][4];
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[nl][i] = 0.f;
+        if (live) {
+          const int st = (NST == 2) ? (cseq & 1) : 0;
+          mbar_wait(&bars[st], (NST == 2) ? ((cseq >> 1) & 1) : (cseq & 1));
+          // ------------------------------------------------------------ x-pass (tensor cores)
+          const float* sb = stage + st * kM * BOXW + (16 * mt + g) * BOXW + 2 * t;
+          // k block kb = 2 hh + j (j = 0 .. NKX) feeds n tiles 2q, 2q + 1 of the pairs
+          // q = 2 hh + qq with step s = j - qq: each block is loaded and split once
+#pragma unroll
+          for (int j = 0; j <= NKX; ++j) {
+            const float* p0 = sb + 16 * (2 * hh + j);
+            const float2 v00 = *reinterpret_cast<const float2*>(p0);
+            const float2 v10 = *reinterpret_cast<const float2*>(p0 + 8 * BOXW);
+            const float2 v01 = *reinterpret_cast<const float2*>(p0 + 8);
+            const float2 v11 = *reinterpret_cast<const float2*>(p0 + 8 * BOXW + 8);
+            uint32_t ah[4], al[4];
+            split_bf16x2(v00.x, v00.y, ah[0], al[0]);
+            split_bf16x2(v10.x, v10.y, ah[1], al[1]);
+            split_bf16x2(v01.x, v01.y, ah[2], al[2]);
+            split_bf16x2(v11.x, v11.y, ah[3], al[3]);
+            // product-major order: consecutive HMMAs write different accumulators
+#pragma unroll
+            for (int pr3 = 0; pr3 < 3; ++pr3)
+#pragma unroll
+              for (int qq = 0; qq < 2; ++qq) {
+                const int s = j - qq;
+                if (s < 0 || s >= NKX) continue;
+#pragma unroll
+                for (int par = 0; par < 2; ++par) {
+                  float(&d)[4] = acc[2 * qq + par];
+                  const uint32_t* a = pr3 == 1 ? al : ah;
+                  const uint32_t* bb = pr3 == 2 ? bxl[par][s] : bxh[par][s];
+                  mma16816(d, a[0], a[1], a[2], a[3], bb[0], bb[1]);
+                }
+              }
+          }
+        }
+        // x-pass output (or the zero padding of a block outside rows [0, H)) -> ring planes
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl) {
+          const int w0 = slot_row * RSW + 4 * (4 * hh + nl) + t;
+          uint32_t hi, lo;
+          split_bf16x2(acc[nl][0], acc[nl][1], hi, lo);
+          ring[w0] = hi;
+          ring[PLANE + w0] = lo;
+          split_bf16x2(acc[nl][2], acc[nl][3], hi, lo);
+          ring[w0 + 8 * RSW] = hi;
+          ring[PLANE + w0 + 8 * RSW] = lo;
+        }
+      }
+      __syncthreads();  // stage consumed; ring slot visible
+      if (live) {
+        ++cseq;
+        if (tid == 0) {
+          fence_proxy_async();
+          producer_next();
+        }
+      }
+      if (do_y && wlive) ypass(n - PRO, pre);
+      __syncthreads();  // ring slot (n + 1) % NSLOT may be overwritten next
+    }
+    u += nyb;
+  }
+  if (cur_vol >= 0) flush(cur_vol);
+
+  if (plain) return;
+  spass_finalize<SP_FWD, kSpassThreads>(P, red, flag);
+}
+
+}  // namespace sfseg

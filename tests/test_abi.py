@@ -102,3 +102,27 @@ def test_full_and_online_workspace_validation(lib):
     assert full >= 7 * 10 * 32 * 40 * 4
     assert lib.sfseg_set_algorithm(7) == 1
     assert lib.sfseg_set_algorithm(0) == 0
+
+
+def test_forward_path_selection(lib):
+    """Host-side plan introspection: which forward kernels a problem runs on."""
+    import paper_2212_08058_b200 as m
+    shp = (1, 70, 480, 854)
+    try:
+        m.set_algorithm(m.ALGO_AUTO)
+        assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24)) == (m.PATH_TWO_PASS_TC, 6, 24)
+        assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3)) == (m.PATH_FUSED_3D, 1, 3)
+        # spatial radii below the tensor-core kernel's smallest compiled radius: FP32 pass
+        assert m.forward_path(shp, m.Gauss(2.0, 2.0, 6, 6))[0] == m.PATH_TWO_PASS_FP32
+        # requested radii round up to compiled ones (extra taps are zero)
+        assert m.forward_path(shp, m.Gauss(1.5, 6.0, 5, 17))[1:] == (5, 18)
+        m.set_algorithm(m.ALGO_TWO_PASS)
+        assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3))[0] == m.PATH_TWO_PASS_FP32
+        m.set_algorithm(m.ALGO_TWO_PASS_FP32)
+        assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24))[0] == m.PATH_TWO_PASS_FP32
+        m.set_algorithm(m.ALGO_MEGAKERNEL)
+        assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24))[0] == m.PATH_MEGAKERNEL
+    finally:
+        m.set_algorithm(m.ALGO_AUTO)
+    with pytest.raises(m.SfsegError):
+        m.forward_path((0, 1, 1, 1), m.Gauss(1.0, 1.0))

@@ -134,6 +134,56 @@ def test_two_pass_path(sf, case):
         sf.set_algorithm(sf.ALGO_AUTO)
 
 
+@pytest.mark.parametrize("case", ["c2", "c4", "c5", "edge"])
+def test_fp32_spatial_pass_path(sf, case):
+    """ALGO_TWO_PASS_FP32: the two-pass iteration with the FP32-FMA spatial pass
+    (the default two-pass forward runs the spatial pass on the bf16 tensor pipe)."""
+    sf.set_algorithm(sf.ALGO_TWO_PASS_FP32)
+    try:
+        if case == "c2":
+            wl = WL.generate("c2", cfg=WL.get_config("c2", T=16, H=150, W=300))
+            _check_forward(sf, wl.ch, wl.w, 2.0, 8.0, 6, 24, 15)
+        elif case == "c4":
+            wl = WL.generate("c4", cfg=WL.get_config("c4", B=3, T=12, H=64, W=96))
+            _check_forward(sf, wl.ch, wl.w, 1.5, 6.0, 5, 18, 10)
+        elif case == "c5":
+            wl = WL.generate("c5", cfg=WL.get_config("c5", T=24, H=90, W=260))
+            _check_forward(sf, wl.ch, wl.w, 3.0, 12.0, 9, 36, 6)
+        else:
+            rng = np.random.default_rng(12)
+            ch = (rng.random((2, 1, 7, 45, 150)) * 0.8 + 0.1).astype(np.float32)
+            _check_forward(sf, ch, [1.0], 1.0, 4.0, 3, 12, 4)
+    finally:
+        sf.set_algorithm(sf.ALGO_AUTO)
+
+
+@pytest.mark.parametrize("r_s,shape", [
+    (8, (2, 5, 70, 200)),      # NKX = 2, one-slot prologue
+    (9, (1, 6, 33, 130)),      # radius not a multiple of 4: box offset D = 3
+    (12, (1, 4, 97, 71)),      # W < 2 strips, ragged 32-row blocks
+    (16, (1, 3, 64, 129)),     # one live column in the last strip
+    (32, (1, 3, 50, 300)),     # four-slot ring
+    (48, (1, 2, 130, 190)),    # largest compiled radius (box 168 columns)
+])
+def test_tensor_core_spatial_radii(sf, r_s, shape):
+    """Every compiled radius of the tensor-core spatial pass, on ragged shapes,
+    against the oracle (x_K 1e-4, gains 1e-5) and against the FP32 spatial pass."""
+    B, T, H, W = shape
+    rng = np.random.default_rng(r_s)
+    ch = (rng.random((B, 1, T, H, W)) * 0.8 + 0.1).astype(np.float32)
+    sig_s = r_s / 3.0
+    xg, xo, _ = _check_forward(sf, ch, [1.0], 1.0, sig_s, 2, r_s, 5)
+    sf.set_algorithm(sf.ALGO_TWO_PASS_FP32)
+    try:
+        x32, _, _ = _gpu_solve(sf, ch, [1.0], sf.Gauss(1.0, sig_s, 2, r_s), 5)
+    finally:
+        sf.set_algorithm(sf.ALGO_AUTO)
+    for bb in range(B):
+        # both within ~1e-5 of the oracle; bf16x3 products vs fp32 FMAs
+        assert _rel(xg[bb], x32[bb]) <= 2e-5
+        assert _rel(x32[bb], xo[bb]) <= 1e-5
+
+
 @pytest.fixture
 def mega(sf):
     sf.set_algorithm(sf.ALGO_MEGAKERNEL)
