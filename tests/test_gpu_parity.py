@@ -369,8 +369,22 @@ def _mse_grad(x, mask):
     return 2.0 * (x - mh) / x.size
 
 
-@pytest.mark.parametrize("act,b", [(0, 0.0), (1, 0.2)])
-def test_backward_c3_recipe(sf, act, b):
+@pytest.mark.parametrize("act,b,algo", [(0, 0.0, "auto"), (1, 0.2, "auto"), (1, 0.2, "fp32")])
+def test_backward_c3_recipe(sf, act, b, algo):
+    """dL/dw through the unrolled iterations; "auto" records the tape with the
+    tensor-core forward spatial pass, "fp32" with the FP32-FMA one (the backward
+    passes are FP32 in both)."""
+    if algo == "fp32":
+        sf.set_algorithm(sf.ALGO_TWO_PASS_FP32)
+        try:
+            _backward_c3_case(sf, act, b)
+        finally:
+            sf.set_algorithm(sf.ALGO_AUTO)
+    else:
+        _backward_c3_case(sf, act, b)
+
+
+def _backward_c3_case(sf, act, b):
     cfg = WL.get_config("c3", T=12, H=72, W=150)
     wl = WL.generate("c3", cfg=cfg)
     w = wl.w if act == 0 else np.array([0.5, -0.3, 0.8, 0.1, 0.6, -0.2], np.float32)
