@@ -12,7 +12,7 @@ timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 [ -x tools/stencil_microbench ] && timeout 120 tools/stencil_microbench > $OUT/stencil_microbench.log 2>&1
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
-for c in probe c4 c3 c2f; do
+for c in probe c4 c3 c2f c5; do
   timeout 900 python bench.py --config $c --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err
 done
 for c in c2 probe; do
@@ -23,6 +23,7 @@ done
 BC="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 $BC > $OUT/plain_full.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:spass -s 16 -c 1 -o $OUT/spass $BC > $OUT/ncu_spass.log 2>&1
+[ -x tools/mma_microbench ] && timeout 120 tools/mma_microbench > $OUT/mma_microbench.log 2>&1
 $BC > $OUT/plain_full2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:tpass -s 16 -c 1 -o $OUT/tpass $BC > $OUT/ncu_tpass.log 2>&1
 BP="python bench.py --config probe --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
