@@ -304,6 +304,45 @@ def test_deterministic_bitwise(sf):
     assert np.array_equal(a, b) and np.array_equal(sa, sb)
 
 
+@pytest.mark.parametrize("radii", [(6, 24), (1, 3)])
+def test_cuda_graph_capture_and_replay(sf, radii):
+    """The forward + threshold (every kernel, no host sync) captured into one CUDA graph
+    and replayed gives bitwise the stream-launched result (bench.py --graph 1)."""
+    r_t, r_s = radii
+    cfg = WL.get_config("c2", T=10, H=70, W=140)
+    wl = WL.generate("c2", cfg=cfg)
+    dev = torch.device("cuda")
+    B, C, T, H, W = wl.ch.shape
+    s = sf.Solver((B, T, H, W), C, sf.Gauss(r_t / 3.0, r_s / 3.0, r_t, r_s), 6)
+    ch = torch.from_numpy(wl.ch).to(dev)
+    x = torch.empty((B, T, H, W), dtype=torch.float32, device=dev)
+    m = torch.empty((B, T, H, W), dtype=torch.uint8, device=dev)
+
+    def step():
+        s.forward(ch, wl.w, 0.0, 0, x_out=x, check=False)
+        s.threshold(x, 0.5, sf.THR_PER_FRAME_MAX, mask=m)
+
+    step()
+    s.sync()
+    x_ref, m_ref = x.clone(), m.clone()
+    x.zero_()
+    m.zero_()
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(graph, stream=cap):
+            step()
+    torch.cuda.current_stream(dev).wait_stream(cap)
+    torch.cuda.synchronize(dev)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize(dev)
+    assert torch.equal(x, x_ref) and torch.equal(m, m_ref)
+    xo, _ = _oracle_solve(wl.ch, wl.w, (r_t / 3.0, r_s / 3.0, r_t, r_s), 6)
+    assert _rel(x.cpu().numpy(), xo) <= X_TOL
+
+
 # --------------------------------------------------------------------------- invariants
 def test_invariants_nonneg_monotone_mirror(sf):
     cfg = WL.get_config("c2", T=12, H=96, W=200)
