@@ -1,0 +1,85 @@
+// Backward step epilogue as a streaming kernel (Appendix A of SURVEY.md; the
+// operations of spass_kernel<R, SP_BWD>'s epilogue, split from the spatial pass):
+//   u = G_xy * v is produced by the tensor-core spatial pass in plain mode;
+//   y_bar_k = (x_bar_k - F u_{k-1} cn) / nu_k,  x_{k-1} = F u_{k-2} / nu_{k-1}
+//   (x_0 = F or the user's x_0 at k = 1),
+//   F_bar += y_bar_k u_{k-1} + x_{k-1} u,  x_bar_{k-1} = F u,
+//   c_{k-1} = <x_{k-1}, x_bar_{k-1}> (fixed-order fp64 partials; last block:
+//   bwd_finalize -> the next step's cn, 1/nu, 1/nu_prev).
+// One float4 per thread per row step, row-parallel like the other streaming kernels.
+#pragma once
+#include "misc.cuh"
+#include "spass.cuh"
+
+namespace sfseg {
+
+struct BwdEpiParams {
+  const float* u;    // pitched G_xy * v
+  const float* F;    // pitched
+  float* xbar;       // pitched, in: x_bar_k, out: x_bar_{k-1}
+  const float* u1;   // tape u_{k-1}
+  const float* u2;   // tape u_{k-2} (k >= 2) or null
+  const float* x0p;  // pitched user x_0 (k == 1) or null (x_0 = F)
+  float* Fbar;       // pitched, accumulated
+  double* sc;
+  const double* tape_nu;
+  double* partials;  // [B][T * gx]
+  unsigned* counter;
+  int B, T, H, W, Wp, gx, K, k;
+};
+
+__global__ void __launch_bounds__(kEwThreads) bwd_epi_kernel(const __grid_constant__ BwdEpiParams P) {
+  __shared__ double red[kEwThreads / 32];
+  __shared__ int flag;
+  const int bt = blockIdx.y;
+  const int b = bt / P.T, t = bt - b * P.T;
+  const long HWp = (long)P.H * P.Wp;
+  const long W4 = P.Wp / 4;
+  const float cn = (float)P.sc[b * kScal + SC_CN];
+  const float inv_nu = (float)P.sc[b * kScal + SC_INV_NU];
+  const float inv_nu_prev = (float)P.sc[b * kScal + SC_INV_NU_PREV];
+  double acc = 0.0;
+  for (int y = blockIdx.x; y < P.H; y += P.gx) {
+    for (long x4 = threadIdx.x; x4 < W4; x4 += kEwThreads) {
+      const long po = (long)bt * HWp + (long)y * P.Wp + 4 * x4;
+      const float4 u4 = __ldcs(reinterpret_cast<const float4*>(P.u + po));
+      const float4 f4 = *reinterpret_cast<const float4*>(P.F + po);
+      const float4 xb4 = *reinterpret_cast<const float4*>(P.xbar + po);
+      const float4 a4 = *reinterpret_cast<const float4*>(P.u1 + po);
+      float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (P.u2) d4 = *reinterpret_cast<const float4*>(P.u2 + po);
+      else if (P.x0p) d4 = *reinterpret_cast<const float4*>(P.x0p + po);
+      const float4 fb4 = *reinterpret_cast<const float4*>(P.Fbar + po);
+      const float uv[4] = {u4.x, u4.y, u4.z, u4.w}, fv[4] = {f4.x, f4.y, f4.z, f4.w};
+      const float xbv[4] = {xb4.x, xb4.y, xb4.z, xb4.w}, u1v[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, fbv[4] = {fb4.x, fb4.y, fb4.z, fb4.w};
+      float xo[4], fo[4];
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool in = 4 * x4 + i < P.W;
+        const float f = in ? fv[i] : 0.f;
+        const float uu = in ? uv[i] : 0.f;
+        const float xp = P.u2 ? f * dv[i] * inv_nu_prev : (P.x0p ? (in ? dv[i] : 0.f) : f);
+        const float yb = (xbv[i] - f * u1v[i] * cn) * inv_nu;
+        fo[i] = fbv[i] + (yb * u1v[i] + xp * uu);
+        xo[i] = f * uu;
+        s = fmaf(xp, xo[i], s);
+      }
+      *reinterpret_cast<float4*>(P.Fbar + po) = make_float4(fo[0], fo[1], fo[2], fo[3]);
+      *reinterpret_cast<float4*>(P.xbar + po) = make_float4(xo[0], xo[1], xo[2], xo[3]);
+      acc += (double)s;
+    }
+  }
+  const double s = block_sum<kEwThreads>(acc, red);
+  const long nper = (long)P.T * P.gx;
+  if (threadIdx.x == 0) P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = s;
+  if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
+  for (int v = 0; v < P.B; ++v) {
+    const double tot = block_sum_array<kEwThreads>(P.partials + (long)v * nper, nper, 1, red);
+    if (threadIdx.x == 0) bwd_finalize(P.sc + v * kScal, P.tape_nu, P.K, P.k, v, tot);
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+}  // namespace sfseg

@@ -22,6 +22,7 @@
 #include "comm.cuh"
 #include "full.cuh"
 #include "online.cuh"
+#include "bwd.cuh"
 #include "launch.h"
 
 using namespace sfseg;
@@ -1009,12 +1010,36 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
 
   SpassParams sp;
   std::memset(&sp, 0, sizeof(sp));
-  if (!make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
+  // spatial part of a backward step: on the tensor-core plan, u = G_xy * v by the
+  // tensor-core pass in plain mode into a scratch volume, then the streaming epilogue
+  // (bwd_epi_kernel); otherwise the FP32 pass with the fused epilogue (SP_BWD)
+  if (!(P.tc ? make_spass_fwd_tmap(&sp.tmap, P, v)
+             : make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))))
+    return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.tape_nu = const_cast<double*>(tape_nu);
   sp.out = xbar;
   sp.Fbar = Fbar;
   sp.x0p = x0p;
+  float* ubuf = at<float>(ws, P.off_p2);
+  BwdEpiParams be;
+  std::memset(&be, 0, sizeof(be));
+  be.u = ubuf;
+  be.F = F;
+  be.xbar = xbar;
+  be.x0p = x0p;
+  be.Fbar = Fbar;
+  be.sc = at<double>(ws, P.off_sc);
+  be.tape_nu = tape_nu;
+  be.partials = at<double>(ws, P.off_part);
+  be.counter = &at<WsHeader>(ws, 0)->counter[0];
+  be.B = (int)P.B;
+  be.T = (int)P.T;
+  be.H = (int)P.H;
+  be.W = (int)P.W;
+  be.Wp = (int)P.Wp;
+  be.gx = P.gx;
+  be.K = K;
   TpassParams tp;
   std::memset(&tp, 0, sizeof(tp));
   fill_tpass_common(tp, P, ws);
@@ -1031,7 +1056,24 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
     sp.u1 = tape_u(k - 1);
     sp.u2 = (k >= 2) ? tape_u(k - 2) : nullptr;
     sp.k = k;
-    {
+    if (P.tc) {
+      SpassParams pl = sp;
+      pl.plain = 1;
+      pl.out = ubuf;
+      {
+        ProfScope ps(st, PC_BWD);
+        SF_CUDA(launch_spass_forward(P, pl, st));
+        SF_CUDA(after_launch("spass_tc(plain, bwd)", st));
+      }
+      be.u1 = sp.u1;
+      be.u2 = sp.u2;
+      be.k = k;
+      {
+        ProfScope ps(st, PC_BWD);
+        bwd_epi_kernel<<<dim3((unsigned)P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(be);
+        SF_CUDA(after_launch("bwd_epi", st));
+      }
+    } else {
       ProfScope ps(st, PC_BWD);
       SF_CUDA(launch_spass_bwd(P.RS, sp, P.G, st));
       SF_CUDA(after_launch("spass_bwd", st));
