@@ -164,6 +164,9 @@ def test_fp32_spatial_pass_path(sf, case):
     (16, (1, 3, 64, 129)),     # one live column in the last strip
     (32, (1, 3, 50, 300)),     # four-slot ring
     (48, (1, 2, 130, 190)),    # largest compiled radius (box 168 columns)
+    (12, (1, 3, 5, 5)),        # W, H << radius: one partial strip, two dead warps, pure padding
+    (16, (2, 2, 1, 300)),      # H = 1: every window is zero padding but one row
+    (8, (1, 1, 40, 9)),        # T = 1, W = 9 (pitch 16)
 ])
 def test_tensor_core_spatial_radii(sf, r_s, shape):
     """Every compiled radius of the tensor-core spatial pass, on ragged shapes,
