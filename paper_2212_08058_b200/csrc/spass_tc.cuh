@@ -73,10 +73,12 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint3
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
-// weight of spatial offset d (zero outside the support)
-__device__ __forceinline__ float sptc_w(const SpassParams& P, int d, int R) {
+// weight of spatial offset d (zero outside the support), from the shared-memory copy of
+// the taps: indexing the kernel-parameter array with a runtime index made the fragment
+// setup take ~7 us of a 117 us launch (globaltimer trace, profiles/tc/trace_*)
+__device__ __forceinline__ float sptc_w(const float* gsm, int d, int R) {
   const int a = d < 0 ? -d : d;
-  return a <= R ? P.g[a] : 0.f;
+  return a <= R ? gsm[a] : 0.f;
 }
 
 template <int R>
@@ -110,12 +112,15 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
   const long u_begin = (long)blockIdx.x * P.U / P.G;
   const long u_end = (long)(blockIdx.x + 1) * P.U / P.G;
 
+  __shared__ float gsm[kMaxRS + 1];
+  if (tid <= R) gsm[tid] = P.g[tid];
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_barrier_init();
     prefetch_tmap(&P.tmap);
   }
+  __syncthreads();
   // Ty fragments (A operand of the y-pass): A[i][kk] = w(16 s + kk - i - R)
   for (int idx = tid; idx < NKY * 2 * 32; idx += kSpassThreads) {
     const int s = idx / 64, pl = (idx >> 5) & 1, l = idx & 31;
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
       const int i = gi + 8 * (j & 1);
       const int kk = 16 * s + 2 * ti + 8 * (j >> 1);
       uint32_t hi, lo;
-      split_bf16x2(sptc_w(P, kk - i - R, R), sptc_w(P, kk + 1 - i - R, R), hi, lo);
+      split_bf16x2(sptc_w(gsm, kk - i - R, R), sptc_w(gsm, kk + 1 - i - R, R), hi, lo);
       v[j] = pl ? lo : hi;
     }
     tyf[idx] = make_uint4(v[0], v[1], v[2], v[3]);
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int d = 16 * s + 2 * t + 8 * j - g - 8 * par - RA;
-        split_bf16x2(sptc_w(P, d, R), sptc_w(P, d + 1, R), bxh[par][s][j], bxl[par][s][j]);
+        split_bf16x2(sptc_w(gsm, d, R), sptc_w(gsm, d + 1, R), bxh[par][s][j], bxl[par][s][j]);
       }
   __syncthreads();
 
