@@ -4,17 +4,24 @@
 
 namespace sfseg {
 namespace {
-template <int R>
-cudaError_t launch_tc_one(const SpassParams& P, int grid, cudaStream_t st) {
+template <int R, int EPI>
+cudaError_t launch_tc_epi(const SpassParams& P, int grid, cudaStream_t st) {
   const size_t smem = sptc_smem_bytes(R);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(spass_tc_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(spass_tc_kernel<R, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  spass_tc_kernel<R><<<grid, kSpassThreads, smem, st>>>(P);
+  spass_tc_kernel<R, EPI><<<grid, kSpassThreads, smem, st>>>(P);
   return cudaGetLastError();
+}
+template <int R>
+cudaError_t launch_tc_one(const SpassParams& P, int grid, cudaStream_t st) {
+  if (P.plain) return launch_tc_epi<R, EPI_PLAIN>(P, grid, st);
+  if (P.tape_u || P.pprev) return launch_tc_epi<R, EPI_FWD_OPT>(P, grid, st);
+  return launch_tc_epi<R, EPI_FWD>(P, grid, st);
 }
 }  // namespace
 
