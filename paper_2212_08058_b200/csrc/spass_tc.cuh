@@ -301,7 +301,10 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
         for (int nl = 0; nl < 4; ++nl) {
           if (!(rok && cst[nl])) continue;
           const long off = base + (long)8 * i * Wp + 8 * nl;
-          const float2 uu = make_float2(acc[nl][2 * i] * cmask[nl].x, acc[nl][2 * i + 1] * cmask[nl].y);
+          // columns >= W: the forward's outputs are F * (...) and F is zero there (combine
+          // writes zero pad columns), so only the plain / tape / Rayleigh variants mask u
+          const float2 uu = EPI == EPI_FWD ? make_float2(acc[nl][2 * i], acc[nl][2 * i + 1])
+                                           : make_float2(acc[nl][2 * i] * cmask[nl].x, acc[nl][2 * i + 1] * cmask[nl].y);
           if (plain) {
             *reinterpret_cast<float2*>(out + off) = uu;
             continue;
