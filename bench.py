@@ -5,8 +5,10 @@
 
 A "step" is one pass of the whole hot path over one synthetic volume:
 fused channel combine + K_iter power iterations (temporal pass, fused spatial
-pass with F multiplies and norm) + final normalisation + per-frame threshold
-(SURVEY.md §8(a) rows a1-a9).  At N=1 the workload is BASELINE.json configs[1]
+pass with F multiplies and norm -- on the bf16 tensor pipe for r_s >= 8, or the
+fused single-pass 3D kernel for small radii) + final normalisation + per-frame
+threshold, captured once and replayed as one CUDA
+graph per step (--graph 0: stream launches).  At N=1 the workload is BASELINE.json configs[1]
 ("c2": 1x70x480x854, C=1, sigma_t=2, sigma_s=8, 15 iterations, tau=0.5).
 For N>1 (torchrun, one rank per GPU) every rank solves its own c2 volume
 (data-parallel over independent volumes, weak scaling, no data-path collective);
