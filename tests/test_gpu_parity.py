@@ -157,6 +157,24 @@ def test_fp32_spatial_pass_path(sf, case):
         sf.set_algorithm(sf.ALGO_AUTO)
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_tensor_core_random_shapes(sf, seed):
+    """Seeded random shapes / radii / weights through the default (tensor-core) path:
+    ragged strips and blocks, B > 1, sigmoid combine, both against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(1, 3))
+    T = int(rng.integers(1, 9))
+    H = int(rng.integers(1, 110))
+    W = int(rng.integers(1, 200))
+    C = int(rng.integers(1, 4))
+    r_s = int(rng.choice([8, 9, 12, 16, 18, 24]))
+    r_t = int(rng.integers(0, 7))
+    ch = (rng.random((B, C, T, H, W)) * 0.8 + 0.1).astype(np.float32)
+    w = (rng.random(C) + 0.2).astype(np.float32)
+    act = int(rng.integers(0, 2))
+    _check_forward(sf, ch, w, max(r_t, 1) / 3.0, r_s / 3.0, r_t, r_s, 4, b=0.1 * act, act=act)
+
+
 @pytest.mark.parametrize("r_s,shape", [
     (8, (2, 5, 70, 200)),      # NKX = 2, one-slot prologue
     (9, (1, 6, 33, 130)),      # radius not a multiple of 4: box offset D = 3
