@@ -4,17 +4,22 @@
 
 namespace sfseg {
 namespace {
-template <int RT, int R>
-cudaError_t f3d_launch_one(const F3dParams& P, int grid, cudaStream_t st) {
+template <int RT, int R, bool OPT>
+cudaError_t f3d_launch_opt(const F3dParams& P, int grid, cudaStream_t st) {
   const size_t smem = f3d_smem_bytes(RT, R);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(f3d_kernel<RT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(f3d_kernel<RT, R, OPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  f3d_kernel<RT, R><<<grid, kF3dThreads, smem, st>>>(P);
+  f3d_kernel<RT, R, OPT><<<grid, kF3dThreads, smem, st>>>(P);
   return cudaGetLastError();
+}
+template <int RT, int R>
+cudaError_t f3d_launch_one(const F3dParams& P, int grid, cudaStream_t st) {
+  return (P.tape_u || P.rayleigh) ? f3d_launch_opt<RT, R, true>(P, grid, st) : f3d_launch_opt<RT, R, false>(P, grid, st);
 }
 template <int RT>
 cudaError_t f3d_launch_rt(int R, const F3dParams& P, int grid, cudaStream_t st) {
