@@ -386,10 +386,9 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
       __syncthreads();  // stage consumed; ring slot visible
       if (live) {
         ++cseq;
-        if (tid == 0) {
-          fence_proxy_async();
-          producer_next();
-        }
+        // no proxy fence: the stage was only READ through the generic proxy, and every
+        // read completed before the barrier (write-after-read needs no cross-proxy fence)
+        if (tid == 0) producer_next();
       }
       if (do_y && wlive) ypass(n - PRO, pre);
       __syncthreads();  // ring slot (n + 1) % NSLOT may be overwritten next
