@@ -544,3 +544,40 @@ def test_c5_full_size_properties_and_crop(sf):
     cfg = WL.get_config("c5", T=24, H=120, W=300)
     crop = WL.generate("c5", cfg=cfg, with_mask=False)
     _check_forward(sf, crop.ch, crop.w, c.sigma_t, c.sigma_s, c.radius_t, c.radius_s, 6)
+
+
+@pytest.mark.parametrize("algo,radii,expect", [
+    ("auto", (6, 24), "tc"), ("auto", (1, 3), "f3d"), ("fp32", (6, 24), "fp32"), ("mega", (6, 24), "mk"),
+])
+def test_reported_path_is_the_launched_path(sf, algo, radii, expect):
+    """sfseg_forward_path's answer matches the kernels that actually run (per-category
+    launch counts of the library's event instrumentation)."""
+    r_t, r_s = radii
+    g = sf.Gauss(r_t / 3.0 if r_t > 1 else 0.5, r_s / 3.0, r_t, r_s)
+    shape = (1, 14, 64, 140)
+    sel = {"auto": sf.ALGO_AUTO, "fp32": sf.ALGO_TWO_PASS_FP32, "mega": sf.ALGO_MEGAKERNEL}[algo]
+    sf.set_algorithm(sel)
+    try:
+        path = sf.forward_path(shape, g)[0]
+        want = {"tc": sf.PATH_TWO_PASS_TC, "f3d": sf.PATH_FUSED_3D, "fp32": sf.PATH_TWO_PASS_FP32,
+                "mk": sf.PATH_MEGAKERNEL}[expect]
+        assert path == want
+        rng = np.random.default_rng(3)
+        ch = torch.from_numpy((rng.random((1, 1) + shape[1:]) * 0.8 + 0.1).astype(np.float32)).cuda()
+        s = sf.Solver(shape, 1, g, 3)
+        s.forward(ch, [1.0])
+        s.sync()
+        sf.profile_enable(True)
+        s.forward(ch, [1.0])
+        s.sync()
+        sf.profile_enable(False)
+        prof = sf.profile_read()
+    finally:
+        sf.set_algorithm(sf.ALGO_AUTO)
+    n = {k: v[1] for k, v in prof.items()}
+    if expect in ("tc", "fp32"):
+        assert n["tpass"] == 3 and n["spass"] == 3 and n["f3d"] == 0 and n["mk"] == 0
+    elif expect == "f3d":
+        assert n["f3d"] == 3 and n["spass"] == 0 and n["tpass"] == 0
+    else:
+        assert n["mk"] == 1 and n["spass"] == 0
