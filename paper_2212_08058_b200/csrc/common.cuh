@@ -70,6 +70,18 @@ __device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uin
   lo = l;
 }
 
+// L2 eviction-priority policy (createpolicy) and a hinted 16-byte global store.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_f4_hint(float4* ptr, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+
 // Deterministic block sum of per-thread doubles (fixed tree).  All threads get the
 // result.  BAR = 0: the whole CTA (__syncthreads); BAR > 0: the named barrier BAR over
 // the first NT threads only (kernels whose producer warp has already exited).

@@ -140,6 +140,8 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
     return val;
   };
 
+  // forward: keep v in L2 for the spatial pass that reads it next (and its halo re-reads)
+  const uint64_t pol = MODE == TP_FWD ? l2_policy_evict_last() : 0ull;
   float4 acc[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -165,7 +167,10 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
       }
       const int slot0 = (((d - 2 * RT) % NR) + NR) % NR;
       const int t = jp - 2 * RT;
-      if (active && t >= 0 && t < T) __stcg(out + (long)t * P.frame4, f4_scale(acc[slot0], scale));
+      if (active && t >= 0 && t < T) {
+        if (MODE == TP_FWD) st_f4_hint(out + (long)t * P.frame4, f4_scale(acc[slot0], scale), pol);
+        else __stcg(out + (long)t * P.frame4, f4_scale(acc[slot0], scale));
+      }
       acc[slot0] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
