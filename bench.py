@@ -289,7 +289,7 @@ def run_ours(args):
         timed_step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    solver.sync()
+    (fsolver if full else solver).sync()   # device errors of the timed steps (sticky error word)
     if world > 1:
         dist.barrier()
     time.sleep(0.1)
@@ -300,12 +300,18 @@ def run_ours(args):
     # defeat the programmatic dependent launch that overlaps a kernel's prologue with the
     # previous kernel's tail)
     prof_steps = max(1, min(3, args.steps))
-    sf.profile_enable(True)
+    profiler = sf.Profiler()   # caller-owned event timing passed in the solvers' options
+    for so in (solver, fsolver if full else None):
+        if so is not None:
+            so.profiler = profiler
     for _ in range(prof_steps):
         step()
     torch.cuda.synchronize(dev)
-    sf.profile_enable(False)
-    prof = sf.profile_read()
+    for so in (solver, fsolver if full else None):
+        if so is not None:
+            so.profiler = None
+    prof = profiler.read()
+    profiler.close()
     prof = {k: (v[0] * args.steps / prof_steps, int(round(v[1] * args.steps / prof_steps))) for k, v in prof.items()}
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -342,29 +348,7 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     tp_bytes = 8.0 * B * T * H * W
     f3_ms, f3_n = prof["f3d"]
-    mk_ms, mk_n = prof["mk"]
-    if mk_n:
-        # large radii: ONE persistent launch runs all K iterations (temporal + spatial work
-        # items): FP32-FMA-bound.  Algorithmic flops per launch = K * voxels * 2 *
-        # (x taps + y taps + t taps + 3 epilogue FMAs)
-        mk_avg_s = mk_ms / mk_n / 1e3
-        mk_flops = 2.0 * K * vox * (2 * (2 * r_s + 1) + (2 * r_t + 1) + 3)
-        mk_traffic = None
-        try:
-            mk_traffic = json.load(open(tfile)).get(args.config, {}).get("mk", {}).get("dram_bytes_per_launch")
-        except Exception:
-            pass
-        roofline = {
-            "kernel": f"mk_kernel<R={r_s}, RT={r_t}> (all {K} iterations: temporal + fused spatial work items)",
-            "bound": "alu", "achieved": mk_flops / mk_avg_s / 1e12, "peak": alu_peak_tflops, "unit": "TFLOP/s",
-            "frac": mk_flops / mk_avg_s / 1e12 / alu_peak_tflops, "traffic": mk_traffic,
-            "peak_source": f"derived: {SM_COUNT} SM x {ALU_PEAK_FMA_PER_CLK_PER_SM} FP32 FMA/clk x 2 x "
-                           f"{sm_max:.0f} MHz ({peaks_src} sm_max_mhz)",
-            "algorithmic_flops_per_launch": mk_flops, "launch_ms": mk_avg_s * 1e3, "launches": mk_n,
-            "share_of_step": mk_ms / ms if ms > 0 else None,
-            "path_hbm_frac_algorithmic_12B": 12.0 * value / world / 1e9 / hbm_peak,
-        }
-    elif f3_n:
+    if f3_n:
         # small radii: the fused single-pass 3D kernel is the whole iteration (HBM-bound):
         # algorithmic bytes = read p_{k-1} + read F + write p_k = 12 B per voxel
         f3_avg_s = f3_ms / f3_n / 1e3
@@ -437,7 +421,7 @@ def run_ours(args):
         }
     # our kernels launched in the timed region: the passes (counted by the library's
     # event instrumentation) + combine, final scale, frame max and threshold per step
-    n_launch = int(sp_n + tp_n + f3_n + 2 * mk_n + 4 * args.steps)   # mk: + its finalize kernel
+    n_launch = int(sp_n + tp_n + f3_n + 4 * args.steps)
     if full:
         n_launch += K * args.steps   # the full operator's per-iteration epilogue kernel
 

@@ -15,15 +15,21 @@
  *   - Every pointer is a DEVICE pointer unless its name ends in _host.
  *   - Dense layouts: channels [B][C][T][H][W] fp32, volumes [B][T][H][W] fp32,
  *     masks [B][T][H][W] uint8; W fastest, no padding, C order.
- *   - The caller owns all memory (PyTorch allocates); the library never
- *     allocates or frees device memory and keeps no hidden global state other
- *     than a per-process cache of TMA descriptors' driver entry point.
+ *   - The caller owns all memory (PyTorch allocates); the solve entry points
+ *     never allocate or free device memory and never synchronise unless stated.
+ *     No call changes process-wide behaviour: the path choice and the optional
+ *     event timing are per-call arguments (sfseg_options).  The only process-
+ *     wide state is read-only caches: the TMA-encode driver entry point, the SM
+ *     count per device and the shared-memory attribute per (kernel, device).
  *   - `stream` is a cudaStream_t passed as void*; all work is enqueued on it.
  *     Entry points do NOT synchronise unless stated ("syncs").
  *   - Validation first: every argument is checked before any launch; on a
  *     validation error nothing is written and nothing is launched.
  *   - Device-detected errors (zero norm, non-finite norm) are recorded in the
- *     workspace's error word and reported by sfseg_sync_status().
+ *     workspace's error word and reported by sfseg_sync_status().  The word is
+ *     STICKY: later calls on the same workspace do not clear it (the first error
+ *     wins); only sfseg_sync_status reads and clears it.  A freshly allocated
+ *     workspace must be reset once with sfseg_workspace_reset before its first use.
  *   - No C++ exception crosses the ABI.
  *   - Results are bitwise reproducible for a fixed (shape, build, GPU model):
  *     all reductions are fixed-order (fp32 within a CTA, fp64 across CTAs).
@@ -87,6 +93,40 @@ int32_t sfseg_abi_version(void);
 /* Text of the last CUDA error seen by this thread inside the library (for SFSEG_ERR_CUDA). */
 const char* sfseg_last_cuda_error(void);
 
+/* ---- per-call options (no process-global switches) ----
+ * algo selects the forward path (all compute the same operator, Eq.7 with p = 1,
+ * up to fp32 rounding order):
+ *   SFSEG_ALGO_AUTO: the fused single-pass 3D kernel (one HBM read of p_{k-1} and F,
+ *     one write of p_k per voxel-iteration) when the compiled radii allow it
+ *     (r_t <= 3, r_s <= 8; PAPER.md:319's 3x7x7 support is such a case), otherwise
+ *     one temporal pass + one fused spatial pass per iteration.
+ *   SFSEG_ALGO_TWO_PASS: always the two-pass iteration.  Its spatial pass runs on the
+ *     tensor pipe for compiled spatial radii 8..48: each operand and tap split into three
+ *     bf16 planes (the full fp32 significand) and six products per tap (A23),
+ *     fp32 accumulation: fp32-class arithmetic.
+ *   SFSEG_ALGO_TWO_PASS_FP32: the two-pass iteration with the FP32-FMA spatial pass.
+ * profiler: NULL, or a sfseg_profiler that records CUDA events around every pass launch
+ * (benchmark instrumentation). */
+#define SFSEG_ALGO_AUTO 0
+#define SFSEG_ALGO_TWO_PASS 1
+#define SFSEG_ALGO_TWO_PASS_FP32 3
+typedef struct sfseg_profiler sfseg_profiler;
+typedef struct {
+  int32_t algo;
+  sfseg_profiler* profiler;
+} sfseg_options;
+
+/* Per-kernel timing object (owned by the caller).  sfseg_profiler_read syncs the
+ * recorded events and returns, per category [0]=temporal pass, [1]=spatial pass,
+ * [2]=once-per-solve kernels, [3]=backward passes, [4]=fused single-pass 3D
+ * iteration, [5]=reserved, the summed milliseconds and launch counts, then resets. */
+sfseg_status sfseg_profiler_create(sfseg_profiler** out);
+sfseg_status sfseg_profiler_destroy(sfseg_profiler* p);
+sfseg_status sfseg_profiler_read(sfseg_profiler* p, double* ms_host /*[6]*/, int64_t* count_host /*[6]*/);
+
+/* Zero the header (error word, counters) of a freshly allocated workspace (async on stream). */
+sfseg_status sfseg_workspace_reset(void* ws, void* stream);
+
 /* Largest radii compiled into this build (spatial, temporal). */
 void sfseg_max_radii(int32_t* radius_s_max_host, int32_t* radius_t_max_host);
 
@@ -123,6 +163,16 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
                                  double* stats_or_null, int32_t want_rayleigh, void* tape_or_null,
                                  void* ws, size_t ws_bytes, const sfseg_dist* dist_or_null,
                                  void* stream);
+/* Same, with per-call options (NULL == {SFSEG_ALGO_AUTO, NULL}).  With dist_or_null the
+ * call validates its arguments on every rank and agrees on the outcome (one int
+ * allreduce, one stream sync) before the first data-path collective: a rank's invalid
+ * argument makes every rank return an error instead of blocking its peers. */
+sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_host, float b,
+                                    int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
+                                    const float* x0_or_null, float* x_out, float* F_out_or_null,
+                                    double* stats_or_null, int32_t want_rayleigh, void* tape_or_null,
+                                    void* ws, size_t ws_bytes, const sfseg_dist* dist_or_null,
+                                    const sfseg_options* opt_or_null, void* stream);
 
 /* Gradient of L(x_K) w.r.t. the channel weights and bias through the K
  * unrolled iterations ("through the full spectral algorithm", P:42, P:212-213,
@@ -138,6 +188,14 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
                                           const float* dL_dx, double* dL_dw_host,
                                           double* dL_db_host, void* ws, size_t ws_bytes,
                                           const sfseg_dist* dist_or_null, void* stream);
+sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const float* w_host,
+                                             float b, int32_t act, sfseg_shape shape,
+                                             sfseg_gauss gauss, int32_t K,
+                                             const float* x0_or_null, const void* tape,
+                                             const float* dL_dx, double* dL_dw_host,
+                                             double* dL_db_host, void* ws, size_t ws_bytes,
+                                             const sfseg_dist* dist_or_null,
+                                             const sfseg_options* opt_or_null, void* stream);
 
 /* ---- full SFSeg / SFSeg++ operator ----
  * The general power iteration of Eq.7 / Eq.10: a unary
@@ -173,7 +231,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
                                       double alpha, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
                                       const float* x0_or_null, float* x_out, double* stats_or_null,
                                       const sfseg_binarize* bin_or_null, void* ws, size_t ws_bytes,
-                                      void* stream);
+                                      const sfseg_options* opt_or_null, void* stream);
 
 /* ---- online / sub-window mode ----
  * PAPER.md:367-387 (Fig. offline_online): the power iteration runs on
@@ -185,7 +243,8 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
  * norm of F on those frames (reading A20), and from F elsewhere (Alg.1 line 3).
  * x_out [B][T][H][W]: per frame the result of the LAST window covering it (each
  * window's result is unit-norm over that window).  Combine as
- * sfseg_power_iterate; device errors via sfseg_sync_status(ws, stream).
+ * sfseg_power_iterate; device errors of every window via sfseg_sync_status(ws, stream).
+ * 1 <= stride <= q when q < T (else SFSEG_ERR_INVALID_ARGUMENT: frames would be skipped).
  * ws: >= sfseg_workspace_bytes_online(...).  Asynchronous. */
 sfseg_status sfseg_workspace_bytes_online(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K,
                                           int32_t q, size_t* ws_bytes_host);
@@ -216,50 +275,15 @@ sfseg_status sfseg_solve_host(const float* ch_host, int32_t C, const float* w_ho
                               uint8_t* d_mask, float* x_out_host, uint8_t* mask_out_host,
                               void* ws, size_t ws_bytes, void* stream);
 
-/* ---- optional per-kernel timing (benchmark instrumentation) ----
- * When enabled, every pass launch is bracketed by CUDA events recorded on the
- * launching stream.  sfseg_profile_read syncs those events and returns, per
- * category [0]=temporal pass, [1]=spatial pass, [2]=once-per-solve kernels,
- * [3]=backward passes, [4]=fused single-pass 3D iteration (small radii),
- * [5]=persistent all-iterations megakernel (large radii), the summed
- * milliseconds and launch counts, then resets. */
-sfseg_status sfseg_profile_enable(int32_t on);
-sfseg_status sfseg_profile_read(double* ms_host /*[6]*/, int64_t* count_host /*[6]*/);
-
-/* ---- forward-path selection (process-wide tuning knob) ----
- * SFSEG_ALGO_AUTO: the single-GPU forward uses the fused single-pass 3D kernel
- * (one HBM read of p_{k-1} and F, one write of p_k per voxel-iteration) when the
- * compiled radii allow it (r_t <= 3, r_s <= 8; PAPER.md:319's 3x7x7 support is
- * such a case), otherwise one temporal pass + one fused spatial pass per
- * iteration.
- * SFSEG_ALGO_TWO_PASS: always the two-pass iteration.
- * The forward spatial pass of the two-pass iteration runs on the bf16 tensor
- * pipe (3-product split, ~1e-5 relative, reading A23) for compiled
- * spatial radii 8..48; SFSEG_ALGO_TWO_PASS_FP32 forces the two-pass iteration
- * with the FP32-FMA spatial pass (the A/B and parity reference of that choice).
- * SFSEG_ALGO_MEGAKERNEL: for (r_s, r_t) in {(24,6), (18,5), (36,9)} without a
- * tape, all K iterations as one persistent wavefront kernel (temporal and
- * spatial work items overlapped, lagged normalisation); else as AUTO.  Measured
- * on par with the two-pass path at config 2, hence not the default.
- * All compute the same operator (Eq.7 with p = 1) up to fp32 rounding order.
- * Not thread-safe against concurrent solves; set it once, before solving. */
-#define SFSEG_ALGO_AUTO 0
-#define SFSEG_ALGO_TWO_PASS 1
-#define SFSEG_ALGO_MEGAKERNEL 2
-#define SFSEG_ALGO_TWO_PASS_FP32 3
-sfseg_status sfseg_set_algorithm(int32_t algo);
-
 /* ---- plan introspection ----
- * The forward path sfseg_power_iterate takes for this shape and Gaussian on one
- * GPU without a tape, under the current sfseg_set_algorithm (a tape forces the
- * two-pass iteration): info_host[0] = SFSEG_PATH_*, [1] = compiled temporal
- * radius, [2] = compiled spatial radius.  Host only, no device work.
- * Errors: SFSEG_ERR_INVALID_ARGUMENT / SFSEG_ERR_SHAPE as sfseg_workspace_bytes. */
+ * The forward path sfseg_power_iterate_ex takes for this shape, Gaussian and algo on
+ * one GPU without a tape (a tape forces the two-pass iteration): info_host[0] =
+ * SFSEG_PATH_*, [1] = compiled temporal radius, [2] = compiled spatial radius.  Host
+ * only, no device work.  Errors: SFSEG_ERR_INVALID_ARGUMENT / SFSEG_ERR_SHAPE. */
 #define SFSEG_PATH_TWO_PASS_FP32 0
 #define SFSEG_PATH_TWO_PASS_TC 1
 #define SFSEG_PATH_FUSED_3D 2
-#define SFSEG_PATH_MEGAKERNEL 3
-sfseg_status sfseg_forward_path(sfseg_shape shape, sfseg_gauss gauss, int32_t* info_host /*[3]*/);
+sfseg_status sfseg_forward_path(sfseg_shape shape, sfseg_gauss gauss, int32_t algo, int32_t* info_host /*[3]*/);
 
 /* ---- multi-GPU communicator (NCCL, loaded at run time with dlopen) ---- */
 /* Multi-GPU solve: call sfseg_power_iterate with dist_or_null = {comm, T_global,
@@ -287,10 +311,22 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
                                        int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
                                        int32_t nslabs, const float* x0_or_null, float* x_out,
                                        double* stats_or_null, int32_t want_rayleigh, void* ws,
-                                       size_t ws_bytes, void* stream);
+                                       size_t ws_bytes, const sfseg_options* opt_or_null, void* stream);
 /* Syncs `stream`; returns the first device-detected error of any slab. */
 sfseg_status sfseg_slabs_sync_status(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K,
                                      int32_t nslabs, void* ws, void* stream);
+
+/* ---- learning loop ----
+ * One optimizer step of Eq.13, AdamW, with AMSGrad ("AdamW optimizer
+ * with AMSGrad") when amsgrad != 0:
+ *   m_t = b1 m + (1 - b1) g;  v_t = b2 v + (1 - b2) g^2;  vmax_t = max(vmax, v_t)
+ *   w  <- w - lr ( m_t/(1 - b1^t) / (sqrt(vmax_t (or v_t))/sqrt(1 - b2^t) + eps) + weight_decay w )
+ * (alpha = 1, eta_t = lr: the decoupled weight decay of AdamW, reading A22).
+ * w [n], grad [n], state [3][n] (m, v, vmax; zero before step 1): DEVICE doubles, updated in
+ * place; t >= 1 is the step number.  Asynchronous on stream. */
+typedef struct { double lr, beta1, beta2, eps, weight_decay; int32_t amsgrad; } sfseg_adamw;
+sfseg_status sfseg_adamw_step(double* w, const double* grad, double* state, int32_t n, int64_t t,
+                              const sfseg_adamw* hp, void* stream);
 
 #ifdef __cplusplus
 }

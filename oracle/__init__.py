@@ -25,9 +25,10 @@ Parity status per function:
 from .sfseg_oracle import (  # noqa: F401
     ACT_IDENTITY, ACT_SIGMOID, THR_PER_FRAME_MAX, THR_GLOBAL_MAX, THR_ABSOLUTE,
     DegenerateError, gaussian_taps, combine, correlate_axis, gaussian_filter,
-    apply_M, normalize_l2, power_iterate, threshold, power_iterate_backward,
+    apply_M, normalize_l2, power_iterate, threshold, power_iterate_backward, soft_binarize,
+    binarize_kappa,
 )
-from .full import full_step, combine_full, power_iterate_full, soft_binarize  # noqa: F401,E402
+from .full import full_step, combine_full, power_iterate_full  # noqa: F401,E402
 from .dense import dense_M_taylor  # noqa: F401,E402
 from .online import window_starts, power_iterate_online  # noqa: F401,E402
-from .learn import AdamW, mse_loss_grad, train  # noqa: F401,E402
+from .learn import AdamW, mse_loss_grad, focal_dice_loss_grad, train  # noqa: F401,E402

@@ -26,7 +26,7 @@ import math
 
 import numpy as np
 
-from .sfseg_oracle import DegenerateError, combine, gaussian_filter
+from .sfseg_oracle import DegenerateError, binarize_kappa, combine, gaussian_filter, soft_binarize
 
 
 def full_step(U: np.ndarray, F: np.ndarray, alpha: float, x: np.ndarray, g_t, g_y, g_x) -> np.ndarray:
@@ -48,17 +48,6 @@ def combine_full(s_ch, ws, bs, act_s, f_ch, wf, bf, act_f, p: float):
         raise ValueError("S^p needs S >= 0 (reading A19)")
     U = np.power(S, float(p))
     return S, U, F
-
-
-def soft_binarize(x: np.ndarray, kappa: float) -> np.ndarray:
-    """Alg.1 STEP 3: X_m <- sigma(X_m), "a sigmoid function (controlled by a
-    parameter)".  Reading A21: sigma(kappa (x - theta)) with
-    theta = mean of the strictly positive entries of x (0 if there are none)."""
-    x = np.asarray(x, np.float64)
-    pos = x[x > 0]
-    theta = float(pos.mean()) if pos.size else 0.0
-    with np.errstate(over="ignore"):
-        return 1.0 / (1.0 + np.exp(-kappa * (x - theta)))
 
 
 def power_iterate_full(S: np.ndarray, U: np.ndarray, F: np.ndarray, alpha: float, g_t, g_s, K: int, x0=None,
@@ -90,7 +79,8 @@ def power_iterate_full(S: np.ndarray, U: np.ndarray, F: np.ndarray, alpha: float
             gains[b, k] = nu / math.sqrt(xx)
             rhos[b, k] = float(np.sum(x * y)) / xx
             x = y / nu
-            if binarize is not None and k + 1 > binarize[0]:
-                x = soft_binarize(x, binarize[1] * binarize[2] ** (k - binarize[0]))
+            kap = binarize_kappa(k + 1, binarize)
+            if kap > 0.0:
+                x = soft_binarize(x, kap)
         xs[b] = x
     return xs, {"nu": nus, "gain": gains, "rho": rhos}

@@ -121,9 +121,31 @@ def normalize_l2(y: np.ndarray) -> np.ndarray:
     return y / n
 
 
+# --------------------------------------------------------------------------- row f2
+def soft_binarize(x: np.ndarray, kappa: float) -> np.ndarray:
+    """Alg.1 STEP 3: X_m <- sigma(X_m), "a sigmoid function (controlled by a
+    parameter)".  Reading A21: sigma(kappa (x - theta)) with
+    theta = mean of the strictly positive entries of x (0 if there are none)."""
+    x = np.asarray(x, np.float64)
+    pos = x[x > 0]
+    theta = float(pos.mean()) if pos.size else 0.0
+    with np.errstate(over="ignore"):
+        return 1.0 / (1.0 + np.exp(-kappa * (x - theta)))
+
+
+def binarize_kappa(k: int, binarize) -> float:
+    """Steepness of iteration k (1-based) under binarize = (n_cont, kappa0, growth), or 0
+    when iteration k is not binarised: Alg.1 STEP 3 runs after the N_cont continuous
+    iterations ("gradually"); SPEC's geometric schedule (S:224,
+    S:251: start kappa0, times growth per iteration) -- reading A21."""
+    if binarize is None or k <= binarize[0]:
+        return 0.0
+    return float(binarize[1]) * float(binarize[2]) ** (k - binarize[0] - 1)
+
+
 # --------------------------------------------------------------------------- O3/O4
 def power_iterate(F: np.ndarray, g_t, g_s, K: int, x0=None, g_x=None,
-                  keep_iterates: bool = False):
+                  keep_iterates: bool = False, binarize=None):
     """K power iterations of Eq.4 in the filtering form of Eq.7/8.
 
     F: [B][T][H][W].  x_0 = F (Alg.1 line 3, "X_m <- S_m"; reading A10:
@@ -134,6 +156,10 @@ def power_iterate(F: np.ndarray, g_t, g_s, K: int, x0=None, g_x=None,
         rho_k = <x_{k-1}, y_k> / ||x_{k-1}||^2             (Rayleigh quotient, Eq.3)
         x_k   = y_k / nu_k                                  (Eq.8)
     ``g_s`` is used for both spatial axes unless ``g_x`` is given.
+    binarize = (n_cont, kappa0, growth): after the normalisation of every iteration
+    k > n_cont the iterate is soft-binarised, x_k <- soft_binarize(x_k, kappa_k)
+    (Alg.1 STEP 3; reading A21) and is the next iterate as is; the output is
+    then the last binarised iterate (values in (0, 1)).
     Returns (x_K float64 [B][T][H][W], stats) with stats arrays of shape [B][K].
     """
     F = np.asarray(F, dtype=np.float64)
@@ -160,6 +186,9 @@ def power_iterate(F: np.ndarray, g_t, g_s, K: int, x0=None, g_x=None,
             rhos[b, k] = float(np.sum(x * y)) / xx
             nus[b, k] = nu
             x = y / nu
+            kap = binarize_kappa(k + 1, binarize)
+            if kap > 0.0:
+                x = soft_binarize(x, kap)
             if keep_iterates:
                 it_b.append(x.copy())
         xs[b] = x
@@ -198,7 +227,7 @@ def threshold(x: np.ndarray, tau: float, mode: int = THR_PER_FRAME_MAX) -> np.nd
 
 
 # --------------------------------------------------------------------------- O6
-def power_iterate_backward(ch, w, b, act, g_t, g_s, K: int, dL_dx, x0=None):
+def power_iterate_backward(ch, w, b, act, g_t, g_s, K: int, dL_dx, x0=None, binarize=None):
     """Gradient of L(x_K) w.r.t. the channel weights w and bias b, through the
     K unrolled iterations ("gradient ... through the full spectral algorithm",
     P:42).  SURVEY.md Appendix A recursion, per volume:
@@ -213,6 +242,12 @@ def power_iterate_backward(ch, w, b, act, g_t, g_s, K: int, dL_dx, x0=None):
         F_bar += x_bar_0                (x_0 = F, Alg.1 line 3; skipped if x0 given)
         z_bar = F_bar * phi'(z);  dw_c = <z_bar, ch_c>;  db = sum z_bar   (Eq.9)
 
+    With binarize (row f2), iteration k > n_cont ends with b_k = sigma(kappa_k (x_k -
+    theta_k)), theta_k = mean of the positive entries of x_k (A21), and b_k is the next
+    iterate; its adjoint is first pulled back through the sigmoid and the centre:
+        g = kappa_k sigma'(z) b_bar ;  x_bar_k = g - [x_k > 0] sum(g) / n_pos
+    (d theta / d x_j = [x_j > 0] / n_pos), then through Eq.8 as above.
+
     Returns (dw float64 [C], db float64), summed over volumes.
     """
     ch = np.asarray(ch, np.float64)
@@ -224,7 +259,7 @@ def power_iterate_backward(ch, w, b, act, g_t, g_s, K: int, dL_dx, x0=None):
     for bb in range(B):
         Fb = F[bb]
         x = Fb.copy() if x0 is None else np.asarray(x0[bb], np.float64).copy()
-        xs, us, nus = [x], [], []
+        xs, xn, us, nus = [x], [None], [], []   # xs[k]: input of iteration k+1; xn[k]: y_k / nu_k
         for k in range(K):
             u = gaussian_filter(Fb * x, g_t, g_y, g_y)
             y = Fb * u
@@ -232,13 +267,23 @@ def power_iterate_backward(ch, w, b, act, g_t, g_s, K: int, dL_dx, x0=None):
             if nu == 0.0:
                 raise DegenerateError("zero norm")
             x = y / nu
+            xn.append(x)
+            kap = binarize_kappa(k + 1, binarize)
+            if kap > 0.0:
+                x = soft_binarize(x, kap)
             us.append(u)
             nus.append(nu)
             xs.append(x)
         xbar = dL_dx[bb].copy()
         for k in range(K, 0, -1):
-            c = float(np.sum(xs[k] * xbar))
-            ybar = (xbar - xs[k] * c) / nus[k - 1]
+            kap = binarize_kappa(k, binarize)
+            if kap > 0.0:   # xbar is the adjoint of b_k: pull it back to x_k = y_k / nu_k
+                s = xs[k] * (1.0 - xs[k])          # sigma'(z) = b (1 - b)
+                g = kap * s * xbar
+                pos = xn[k] > 0
+                xbar = g - pos * (float(np.sum(g)) / max(int(pos.sum()), 1))
+            c = float(np.sum(xn[k] * xbar))
+            ybar = (xbar - xn[k] * c) / nus[k - 1]
             v = gaussian_filter(Fb * ybar, g_t, g_y, g_y)
             F_bar[bb] += ybar * us[k - 1] + xs[k - 1] * v
             xbar = Fb * v

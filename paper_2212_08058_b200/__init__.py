@@ -9,7 +9,6 @@ to load, every entry point raises.
 from __future__ import annotations
 
 import ctypes as C
-import math
 import os
 from dataclasses import dataclass
 from typing import Optional
@@ -18,8 +17,9 @@ import torch
 
 __all__ = [
     "SfsegError", "Gauss", "lib", "workspace_bytes", "combine_channels", "power_iterate",
-    "power_iterate_backward", "threshold", "solve_host", "Solver",
+    "power_iterate_backward", "threshold", "solve_host", "Solver", "Profiler", "AdamWState",
     "ACT_IDENTITY", "ACT_SIGMOID", "THR_PER_FRAME_MAX", "THR_GLOBAL_MAX", "THR_ABSOLUTE",
+    "ALGO_AUTO", "ALGO_TWO_PASS", "ALGO_TWO_PASS_FP32",
 ]
 
 ACT_IDENTITY, ACT_SIGMOID = 0, 1
@@ -56,6 +56,15 @@ class DistC(C.Structure):
     _fields_ = [("comm", C.c_void_p), ("T_global", C.c_int64), ("t_offset", C.c_int64)]
 
 
+class OptionsC(C.Structure):
+    _fields_ = [("algo", C.c_int32), ("profiler", C.c_void_p)]
+
+
+class AdamwC(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double), ("amsgrad", C.c_int32)]
+
+
 @dataclass(frozen=True)
 class Gauss:
     sigma_t: float
@@ -79,27 +88,33 @@ _SIGS = {
     "sfseg_combine_channels": (C.c_int, [_P, C.c_int32, Shape, _P, C.c_float, C.c_int32, _P, _P]),
     "sfseg_power_iterate": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                       _P, _P, _P, _P, C.c_int32, _P, _P, C.c_size_t, _P, _P]),
+    "sfseg_power_iterate_ex": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
+                                         _P, _P, _P, _P, C.c_int32, _P, _P, C.c_size_t, _P, _P, _P]),
     "sfseg_power_iterate_backward": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC,
                                                C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t, _P, _P]),
+    "sfseg_power_iterate_backward_ex": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC,
+                                                  C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t, _P, _P, _P]),
+    "sfseg_workspace_reset": (C.c_int, [_P, _P]),
+    "sfseg_profiler_create": (C.c_int, [_P]),
+    "sfseg_profiler_destroy": (C.c_int, [_P]),
+    "sfseg_profiler_read": (C.c_int, [_P, _P, _P]),
+    "sfseg_adamw_step": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
     "sfseg_threshold_ws_bytes": (C.c_size_t, [Shape]),
     "sfseg_threshold": (C.c_int, [_P, Shape, C.c_float, C.c_int32, _P, _P, C.c_size_t, _P]),
     "sfseg_sync_status": (C.c_int, [_P, _P]),
     "sfseg_solve_host": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                    C.c_float, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
-    "sfseg_profile_enable": (C.c_int, [C.c_int32]),
-    "sfseg_profile_read": (C.c_int, [_P, _P]),
-    "sfseg_set_algorithm": (C.c_int, [C.c_int32]),
-    "sfseg_forward_path": (C.c_int, [Shape, GaussC, C.POINTER(C.c_int32)]),
+    "sfseg_forward_path": (C.c_int, [Shape, GaussC, C.c_int32, C.POINTER(C.c_int32)]),
     "sfseg_workspace_bytes_online": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
     "sfseg_power_iterate_online": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                              C.c_int32, C.c_int32, _P, _P, C.c_size_t, _P]),
     "sfseg_workspace_bytes_full": (C.c_int, [Shape, C.c_int32, C.c_int32, GaussC, C.c_int32, _P]),
     "sfseg_power_iterate_full": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, _P, C.c_int32, _P, C.c_float,
                                            C.c_int32, C.c_double, C.c_double, Shape, GaussC, C.c_int32, _P, _P,
-                                           _P, _P, _P, C.c_size_t, _P]),
+                                           _P, _P, _P, C.c_size_t, _P, _P]),
     "sfseg_slabs_workspace_bytes": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
     "sfseg_power_iterate_slabs": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
-                                            C.c_int32, _P, _P, _P, C.c_int32, _P, C.c_size_t, _P]),
+                                            C.c_int32, _P, _P, _P, C.c_int32, _P, C.c_size_t, _P, _P]),
     "sfseg_slabs_sync_status": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P, _P]),
     "sfseg_get_unique_id": (C.c_int, [_P]),
     "sfseg_comm_create": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P]),
@@ -142,11 +157,18 @@ def _shape(x: torch.Tensor) -> Shape:
     return Shape(B, T, H, W)
 
 
-def _require(t: torch.Tensor, name: str, ndim: int, dtype=torch.float32):
+def _require(t: torch.Tensor, name: str, ndim: int, dtype=torch.float32, shape=None, device=None):
+    """Every tensor handed to the library: CUDA, contiguous, the dtype, rank (and, when
+    given, exact shape and device) the C call expects -- a wrong buffer would be read or
+    written out of bounds by the kernels, so it is rejected here."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
     if t.dtype != dtype or t.dim() != ndim or not t.is_contiguous():
         raise ValueError(f"{name} must be a contiguous {dtype} tensor with {ndim} dims")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if device is not None and t.device != torch.device(device):
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
 
 
 def _weights(w, Cn: int):
@@ -156,47 +178,56 @@ def _weights(w, Cn: int):
     return (C.c_float * Cn)(*w)
 
 
-def profile_enable(on: bool = True) -> None:
-    """Bracket every pass launch with CUDA events (bench instrumentation)."""
-    _check(lib().sfseg_profile_enable(int(on)), "sfseg_profile_enable")
+class Profiler:
+    """Caller-owned per-kernel event timing (sfseg_profiler): pass ``profiler=`` to a solver."""
 
+    def __init__(self):
+        self._h = C.c_void_p()
+        _check(lib().sfseg_profiler_create(C.byref(self._h)), "sfseg_profiler_create")
 
-def profile_read():
-    """Sync the recorded events; returns {category: (total_ms, launches)} and resets."""
-    ms = (C.c_double * 6)()
-    n = (C.c_int64 * 6)()
-    _check(lib().sfseg_profile_read(ms, n), "sfseg_profile_read")
-    names = ("tpass", "spass", "once", "backward", "f3d", "mk")
-    return {names[i]: (ms[i], n[i]) for i in range(6)}
+    @property
+    def handle(self):
+        return self._h
+
+    def read(self):
+        """Sync the recorded events; returns {category: (total_ms, launches)} and resets."""
+        ms = (C.c_double * 6)()
+        n = (C.c_int64 * 6)()
+        _check(lib().sfseg_profiler_read(self._h, ms, n), "sfseg_profiler_read")
+        names = ("tpass", "spass", "once", "backward", "f3d", "reserved")
+        return {names[i]: (ms[i], n[i]) for i in range(6)}
+
+    def close(self):
+        if self._h:
+            _check(lib().sfseg_profiler_destroy(self._h), "sfseg_profiler_destroy")
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 ALGO_AUTO = 0
 ALGO_TWO_PASS = 1
-ALGO_MEGAKERNEL = 2
 ALGO_TWO_PASS_FP32 = 3
-
 
 PATH_TWO_PASS_FP32 = 0
 PATH_TWO_PASS_TC = 1
 PATH_FUSED_3D = 2
-PATH_MEGAKERNEL = 3
 
 
-def forward_path(shape, gauss) -> tuple:
-    """(path, compiled r_t, compiled r_s) of the single-GPU forward without a tape under
-    the current set_algorithm: path is one of PATH_* (host-side plan, no device work)."""
+def _options(algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None) -> OptionsC:
+    return OptionsC(int(algo), profiler.handle if profiler is not None else None)
+
+
+def forward_path(shape, gauss, algo: int = ALGO_AUTO) -> tuple:
+    """(path, compiled r_t, compiled r_s) of the single-GPU forward without a tape for this
+    algo: path is one of PATH_* (host-side plan, no device work)."""
     info = (C.c_int32 * 3)()
-    _check(lib().sfseg_forward_path(Shape(*shape), gauss.c(), info), "sfseg_forward_path")
+    _check(lib().sfseg_forward_path(Shape(*shape), gauss.c(), int(algo), info), "sfseg_forward_path")
     return int(info[0]), int(info[1]), int(info[2])
-
-
-def set_algorithm(algo: int) -> None:
-    """Forward-path selection: ALGO_AUTO (fused single-pass 3D kernel for small
-    radii, else two-pass), ALGO_TWO_PASS (always temporal + spatial pass) or
-    ALGO_MEGAKERNEL (all iterations in one persistent launch, large radii) or
-    ALGO_TWO_PASS_FP32 (two-pass with the FP32-FMA spatial pass instead of the
-    tensor-core one)."""
-    _check(lib().sfseg_set_algorithm(int(algo)), "sfseg_set_algorithm")
 
 
 def workspace_bytes(shape, C_: int, gauss: Gauss, K: int, want_tape: bool = False):
@@ -209,6 +240,15 @@ def workspace_bytes(shape, C_: int, gauss: Gauss, K: int, want_tape: bool = Fals
 def _alloc_bytes(n: int, device) -> torch.Tensor:
     # torch's caching allocator returns >= 512-byte aligned blocks
     return torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+
+
+def _alloc_ws(n: int, device) -> torch.Tensor:
+    """A solve workspace: allocated, then its header (sticky error word, counters) zeroed
+    once by sfseg_workspace_reset on the current stream."""
+    ws = _alloc_bytes(n, device)
+    with torch.cuda.device(ws.device):
+        _check(lib().sfseg_workspace_reset(_ptr(ws), _stream()), "sfseg_workspace_reset")
+    return ws
 
 
 def combine_channels(ch: torch.Tensor, w, b: float = 0.0, act: int = ACT_IDENTITY, stream=None) -> torch.Tensor:
@@ -224,38 +264,47 @@ def combine_channels(ch: torch.Tensor, w, b: float = 0.0, act: int = ACT_IDENTIT
 class Solver:
     """Holds the workspace (and optional tape) for one problem shape.
 
-    ``forward`` runs sfseg_power_iterate; ``backward`` runs
-    sfseg_power_iterate_backward on the tape of the last forward.
+    ``forward`` runs sfseg_power_iterate_ex; ``backward`` runs
+    sfseg_power_iterate_backward_ex on the tape of the last forward.  ``algo`` and
+    ``profiler`` are this solver's sfseg_options (no process-global switch).
     """
 
-    def __init__(self, shape, C_: int, gauss: Gauss, K: int, device="cuda", want_tape: bool = False):
+    def __init__(self, shape, C_: int, gauss: Gauss, K: int, device="cuda", want_tape: bool = False,
+                 algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None):
         self.shape = tuple(int(v) for v in shape)
         self.C, self.gauss, self.K = int(C_), gauss, int(K)
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.want_tape = bool(want_tape)
+        self.algo, self.profiler = int(algo), profiler
         ws, tape = workspace_bytes(self.shape, self.C, gauss, self.K, want_tape)
         thr = lib().sfseg_threshold_ws_bytes(Shape(*self.shape))
         self.ws_bytes = ws
-        self.ws = _alloc_bytes(ws + thr, self.device)
+        self.ws = _alloc_ws(ws + thr, self.device)
         self.thr_ws_bytes = thr
         self.tape = _alloc_bytes(tape, self.device) if want_tape else None
         self.stats = torch.zeros((self.shape[0], self.K, 3), dtype=torch.float64, device=self.device)
 
+    def _opt(self):
+        return C.byref(_options(self.algo, self.profiler))
+
     def forward(self, ch: torch.Tensor, w, b: float = 0.0, act: int = ACT_IDENTITY, x0=None,
                 x_out: Optional[torch.Tensor] = None, want_rayleigh: bool = False, F_out=None,
                 stream=None, check: bool = True) -> torch.Tensor:
-        _require(ch, "ch", 5)
-        B, Cn, T, H, W = ch.shape
-        if (B, T, H, W) != self.shape or Cn != self.C:
-            raise ValueError("ch shape does not match the solver")
+        B, T, H, W = self.shape
+        _require(ch, "ch", 5, shape=(B, self.C, T, H, W), device=self.device)
         if x0 is not None:
-            _require(x0, "x0", 4)
+            _require(x0, "x0", 4, shape=self.shape, device=self.device)
+        if F_out is not None:
+            _require(F_out, "F_out", 4, shape=self.shape, device=self.device)
         if x_out is None:
-            x_out = torch.empty(self.shape, dtype=torch.float32, device=ch.device)
-        st = lib().sfseg_power_iterate(
-            _ptr(ch), Cn, _weights(w, Cn), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
+            x_out = torch.empty(self.shape, dtype=torch.float32, device=self.device)
+        _require(x_out, "x_out", 4, shape=self.shape, device=self.device)
+        st = lib().sfseg_power_iterate_ex(
+            _ptr(ch), self.C, _weights(w, self.C), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
             _ptr(x0), _ptr(x_out), _ptr(F_out), _ptr(self.stats), int(want_rayleigh), _ptr(self.tape),
-            _ptr(self.ws), self.ws_bytes, None, _stream(stream))
+            _ptr(self.ws), self.ws_bytes, None, self._opt(), _stream(stream))
         _check(st, "sfseg_power_iterate")
         if check:
             self.sync(stream)
@@ -268,22 +317,26 @@ class Solver:
                  x0=None, stream=None):
         if self.tape is None:
             raise RuntimeError("Solver was built without want_tape")
-        _require(ch, "ch", 5)
-        _require(dL_dx, "dL_dx", 4)
-        Cn = ch.shape[1]
-        dw = (C.c_double * Cn)()
+        B, T, H, W = self.shape
+        _require(ch, "ch", 5, shape=(B, self.C, T, H, W), device=self.device)
+        _require(dL_dx, "dL_dx", 4, shape=self.shape, device=self.device)
+        if x0 is not None:
+            _require(x0, "x0", 4, shape=self.shape, device=self.device)
+        dw = (C.c_double * self.C)()
         db = C.c_double(0.0)
-        st = lib().sfseg_power_iterate_backward(
-            _ptr(ch), Cn, _weights(w, Cn), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
+        st = lib().sfseg_power_iterate_backward_ex(
+            _ptr(ch), self.C, _weights(w, self.C), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
             _ptr(x0), _ptr(self.tape), _ptr(dL_dx), dw, C.byref(db), _ptr(self.ws), self.ws_bytes, None,
-            _stream(stream))
+            self._opt(), _stream(stream))
         _check(st, "sfseg_power_iterate_backward")
-        return [dw[i] for i in range(Cn)], db.value
+        return [dw[i] for i in range(self.C)], db.value
 
     def threshold(self, x: torch.Tensor, tau: float, mode: int = THR_PER_FRAME_MAX,
                   mask: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        _require(x, "x", 4, shape=self.shape, device=self.device)
         if mask is None:
             mask = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+        _require(mask, "mask", 4, dtype=torch.uint8, shape=self.shape, device=self.device)
         thr_ws = self.ws.narrow(0, self.ws_bytes + (-self.ws_bytes) % 256, self.thr_ws_bytes) \
             if self.thr_ws_bytes else None
         _check(lib().sfseg_threshold(_ptr(x), _shape(x), float(tau), int(mode), _ptr(mask), _ptr(thr_ws),
@@ -292,24 +345,26 @@ class Solver:
 
 
 def power_iterate(ch: torch.Tensor, w, gauss: Gauss, K: int, b: float = 0.0, act: int = ACT_IDENTITY,
-                  x0=None, want_rayleigh: bool = False):
+                  x0=None, want_rayleigh: bool = False, algo: int = ALGO_AUTO):
     """One-shot solve; returns (x_K [B][T][H][W], stats float64 [B][K][3])."""
     B, Cn, T, H, W = ch.shape
-    s = Solver((B, T, H, W), Cn, gauss, K, device=ch.device)
+    s = Solver((B, T, H, W), Cn, gauss, K, device=ch.device, algo=algo)
     x = s.forward(ch, w, b, act, x0=x0, want_rayleigh=want_rayleigh)
     return x, s.stats.clone()
 
 
-def power_iterate_backward(ch, w, gauss: Gauss, K: int, dL_dx, b: float = 0.0, act: int = ACT_IDENTITY, x0=None):
+def power_iterate_backward(ch, w, gauss: Gauss, K: int, dL_dx, b: float = 0.0, act: int = ACT_IDENTITY, x0=None,
+                           algo: int = ALGO_AUTO):
     B, Cn, T, H, W = ch.shape
-    s = Solver((B, T, H, W), Cn, gauss, K, device=ch.device, want_tape=True)
+    s = Solver((B, T, H, W), Cn, gauss, K, device=ch.device, want_tape=True, algo=algo)
     x = s.forward(ch, w, b, act, x0=x0)
     dw, db = s.backward(ch, w, dL_dx, b, act, x0=x0)
     return x, dw, db
 
 
 def power_iterate_slabs(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, b: float = 0.0,
-                        act: int = ACT_IDENTITY, x0=None, want_rayleigh: bool = False, stream=None):
+                        act: int = ACT_IDENTITY, x0=None, want_rayleigh: bool = False, stream=None,
+                        algo: int = ALGO_AUTO):
     """Time-slab decomposition of the solve emulated on ONE GPU (sfseg_power_iterate_slabs):
     the per-rank phases of the multi-GPU path with in-process halo copies and reduction."""
     _require(ch, "ch", 5)
@@ -318,15 +373,17 @@ def power_iterate_slabs(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, 
     n = C.c_size_t(0)
     _check(lib().sfseg_slabs_workspace_bytes(shp, Cn, g, int(K), int(nslabs), C.byref(n)),
            "sfseg_slabs_workspace_bytes")
-    ws = _alloc_bytes(n.value, ch.device)
+    ws = torch.zeros(max(n.value, 256), dtype=torch.uint8, device=ch.device)  # every slab header zeroed
+    nsl = int(nslabs)
     x = torch.empty((B, T, H, W), dtype=torch.float32, device=ch.device)
     stats = torch.zeros((B, int(K), 3), dtype=torch.float64, device=ch.device)
     if x0 is not None:
-        _require(x0, "x0", 4)
+        _require(x0, "x0", 4, shape=(B, T, H, W), device=ch.device)
     _check(lib().sfseg_power_iterate_slabs(_ptr(ch), Cn, _weights(w, Cn), float(b), int(act), shp, g, int(K),
-                                           int(nslabs), _ptr(x0), _ptr(x), _ptr(stats), int(want_rayleigh),
-                                           _ptr(ws), n.value, _stream(stream)), "sfseg_power_iterate_slabs")
-    _check(lib().sfseg_slabs_sync_status(shp, Cn, g, int(K), int(nslabs), _ptr(ws), _stream(stream)),
+                                           nsl, _ptr(x0), _ptr(x), _ptr(stats), int(want_rayleigh),
+                                           _ptr(ws), n.value, C.byref(_options(algo)), _stream(stream)),
+           "sfseg_power_iterate_slabs")
+    _check(lib().sfseg_slabs_sync_status(shp, Cn, g, int(K), nsl, _ptr(ws), _stream(stream)),
            "sfseg_power_iterate_slabs (device)")
     return x, stats
 
@@ -347,6 +404,16 @@ def solve_host(ch_host: torch.Tensor, w, gauss: Gauss, K: int, tau: float, solve
                b: float = 0.0, act: int = ACT_IDENTITY, thr_mode: int = THR_PER_FRAME_MAX, stream=None):
     """End-to-end call over HOST buffers (H2D, solve, threshold, D2H, sync) via sfseg_solve_host."""
     B, Cn, T, H, W = ch_host.shape
+    if ch_host.is_cuda or ch_host.dtype != torch.float32 or not ch_host.is_contiguous():
+        raise ValueError("ch_host must be a contiguous float32 host tensor")
+    if (B, T, H, W) != solver.shape or Cn != solver.C:
+        raise ValueError("ch_host does not match the solver")
+    _require(d_ch, "d_ch", 5, shape=ch_host.shape, device=solver.device)
+    _require(d_x, "d_x", 4, shape=solver.shape, device=solver.device)
+    _require(d_mask, "d_mask", 4, dtype=torch.uint8, shape=solver.shape, device=solver.device)
+    for t, nm, dt in ((x_out_host, "x_out_host", torch.float32), (mask_out_host, "mask_out_host", torch.uint8)):
+        if t is not None and (t.is_cuda or t.dtype != dt or tuple(t.shape) != solver.shape or not t.is_contiguous()):
+            raise ValueError(f"{nm} must be a contiguous {dt} host tensor of shape {solver.shape}")
     _check(lib().sfseg_solve_host(
         C.c_void_p(ch_host.data_ptr()), Cn, _weights(w, Cn), float(b), int(act), Shape(B, T, H, W), gauss.c(),
         int(K), float(tau), int(thr_mode), _ptr(d_ch), _ptr(d_x), _ptr(d_mask),
@@ -381,7 +448,8 @@ class HostStream:
 
     def run(self, ch_hosts, w, tau: float, x_hosts, mask_hosts, b: float = 0.0, act: int = ACT_IDENTITY,
             thr_mode: int = THR_PER_FRAME_MAX) -> None:
-        """Solve len(ch_hosts) volumes; results land in x_hosts[i] / mask_hosts[i]. Syncs."""
+        """Solve len(ch_hosts) volumes; results land in x_hosts[i] / mask_hosts[i].  Syncs, then
+        reports the first device error of ANY volume (the error word is sticky)."""
         s_cmp = torch.cuda.current_stream(self.device)
         for i, chh in enumerate(ch_hosts):
             sl = self.slots[i % 2]
@@ -416,15 +484,19 @@ class FullSolver:
     """The full SFSeg / SFSeg++ operator (Eq.7 / Eq.10 with
     unary exponent p, pairwise map F and alpha) through sfseg_power_iterate_full."""
 
-    def __init__(self, shape, Cs: int, Cf: int, gauss: Gauss, K: int, device="cuda"):
+    def __init__(self, shape, Cs: int, Cf: int, gauss: Gauss, K: int, device="cuda", algo: int = ALGO_AUTO,
+                 profiler: Optional[Profiler] = None):
         self.shape = tuple(int(v) for v in shape)
         self.Cs, self.Cf, self.gauss, self.K = int(Cs), int(Cf), gauss, int(K)
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.algo, self.profiler = int(algo), profiler
         n = C.c_size_t(0)
         _check(lib().sfseg_workspace_bytes_full(Shape(*self.shape), self.Cs, self.Cf, gauss.c(), self.K,
                                                 C.byref(n)), "sfseg_workspace_bytes_full")
         self.ws_bytes = n.value
-        self.ws = _alloc_bytes(self.ws_bytes, self.device)
+        self.ws = _alloc_ws(self.ws_bytes, self.device)
         self.stats = torch.zeros((self.shape[0], self.K, 3), dtype=torch.float64, device=self.device)
 
     def forward(self, s_ch: torch.Tensor, ws, f_ch: torch.Tensor, wf, p: float, alpha: float,
@@ -432,21 +504,28 @@ class FullSolver:
                 x0=None, x_out: Optional[torch.Tensor] = None, binarize=None, stream=None,
                 check: bool = True) -> torch.Tensor:
         """binarize = (n_cont, kappa0, growth): Alg.1 STEP 3 soft-binarisation (row f2)."""
-        _require(s_ch, "s_ch", 5)
-        _require(f_ch, "f_ch", 5)
+        B, T, H, W = self.shape
+        _require(s_ch, "s_ch", 5, shape=(B, self.Cs, T, H, W), device=self.device)
+        _require(f_ch, "f_ch", 5, shape=(B, self.Cf, T, H, W), device=self.device)
+        if x0 is not None:
+            _require(x0, "x0", 4, shape=self.shape, device=self.device)
         if x_out is None:
-            x_out = torch.empty(self.shape, dtype=torch.float32, device=s_ch.device)
+            x_out = torch.empty(self.shape, dtype=torch.float32, device=self.device)
+        _require(x_out, "x_out", 4, shape=self.shape, device=self.device)
         st = lib().sfseg_power_iterate_full(
             _ptr(s_ch), self.Cs, _weights(ws, self.Cs), float(bs), int(act_s),
             _ptr(f_ch), self.Cf, _weights(wf, self.Cf), float(bf), int(act_f), float(p), float(alpha),
             Shape(*self.shape), self.gauss.c(), self.K, _ptr(x0), _ptr(x_out), _ptr(self.stats),
             None if binarize is None else C.byref(BinarizeC(int(binarize[0]), float(binarize[1]),
                                                             float(binarize[2]))),
-            _ptr(self.ws), self.ws_bytes, _stream(stream))
+            _ptr(self.ws), self.ws_bytes, C.byref(_options(self.algo, self.profiler)), _stream(stream))
         _check(st, "sfseg_power_iterate_full")
         if check:
-            _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate_full (device)")
+            self.sync(stream)
         return x_out
+
+    def sync(self, stream=None) -> None:
+        _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate_full (device)")
 
 
 def power_iterate_online(ch: torch.Tensor, w, gauss: Gauss, K: int, q: int, stride: int, b: float = 0.0,
@@ -458,7 +537,7 @@ def power_iterate_online(ch: torch.Tensor, w, gauss: Gauss, K: int, q: int, stri
     n = C.c_size_t(0)
     _check(lib().sfseg_workspace_bytes_online(shp, Cn, gauss.c(), int(K), int(q), C.byref(n)),
            "sfseg_workspace_bytes_online")
-    ws = _alloc_bytes(n.value, ch.device)
+    ws = _alloc_ws(n.value, ch.device)
     x = torch.empty((B, T, H, W), dtype=torch.float32, device=ch.device)
     _check(lib().sfseg_power_iterate_online(_ptr(ch), Cn, _weights(w, Cn), float(b), int(act), shp, gauss.c(),
                                             int(K), int(q), int(stride), _ptr(x), _ptr(ws), n.value,
@@ -467,35 +546,23 @@ def power_iterate_online(ch: torch.Tensor, w, gauss: Gauss, K: int, q: int, stri
     return x
 
 
-class AdamW:
-    """AdamW with AMSGrad (Eq.13, PAPER.md:224-229; "AdamW optimizer with AMSGrad", P:603) over
-    the handful of combine parameters (w, b) of Eq.9 -- host-side, like any optimizer state of
-    a C+1-parameter model (reading A22: PyTorch's update order)."""
+class AdamWState:
+    """Device state of sfseg_adamw_step (Eq.13 with AMSGrad) for n
+    parameters: the parameters and the moments [m | v | v_max] live in device memory and are
+    updated by the library's kernel; this class only holds the buffers and the step count."""
 
-    def __init__(self, n: int, lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
-                 amsgrad: bool = True):
-        import numpy as np
-        self.np = np
-        self.lr, self.b1, self.b2, self.eps, self.wd, self.ams = lr, betas[0], betas[1], eps, weight_decay, amsgrad
-        self.m = np.zeros(n)
-        self.v = np.zeros(n)
-        self.vmax = np.zeros(n)
+    def __init__(self, params, lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
+                 amsgrad: bool = True, device="cuda"):
+        self.w = torch.tensor([float(v) for v in params], dtype=torch.float64, device=device)
+        self.state = torch.zeros(3 * self.w.numel(), dtype=torch.float64, device=device)
+        self.hp = AdamwC(float(lr), float(betas[0]), float(betas[1]), float(eps), float(weight_decay), int(amsgrad))
         self.t = 0
 
-    def step(self, params, grad):
-        np = self.np
+    def step(self, grad: torch.Tensor, stream=None) -> None:
+        _require(grad, "grad", 1, dtype=torch.float64, shape=self.w.shape, device=self.w.device)
         self.t += 1
-        p = np.asarray(params, np.float64) * (1.0 - self.lr * self.wd)
-        g = np.asarray(grad, np.float64)
-        self.m = self.b1 * self.m + (1.0 - self.b1) * g
-        self.v = self.b2 * self.v + (1.0 - self.b2) * g * g
-        bc1, bc2 = 1.0 - self.b1 ** self.t, 1.0 - self.b2 ** self.t
-        if self.ams:
-            self.vmax = np.maximum(self.vmax, self.v)
-            denom = np.sqrt(self.vmax) / bc2 ** 0.5 + self.eps
-        else:
-            denom = np.sqrt(self.v) / bc2 ** 0.5 + self.eps
-        return p - (self.lr / bc1) * self.m / denom
+        _check(lib().sfseg_adamw_step(_ptr(self.w), _ptr(grad), _ptr(self.state), self.w.numel(), self.t,
+                                      C.byref(self.hp), _stream(stream)), "sfseg_adamw_step")
 
 
 def train_weights(ch: torch.Tensor, mask: torch.Tensor, w0, b0: float, act: int, gauss: Gauss, K: int, steps: int,
@@ -503,25 +570,24 @@ def train_weights(ch: torch.Tensor, mask: torch.Tensor, w0, b0: float, act: int,
     """Learn the Eq.9 weights end to end: each step runs
     sfseg_power_iterate with a tape, the MSE loss of reading A13 against the
     unit-normalised mask (harness-side elementwise gradient), then
-    sfseg_power_iterate_backward for dL/dw, dL/db, and an AdamW/AMSGrad update.
+    sfseg_power_iterate_backward for dL/dw, dL/db, and sfseg_adamw_step.
     Returns (w, b, losses)."""
-    import numpy as np
     _require(ch, "ch", 5)
     B, Cn, T, H, W = ch.shape
     solver = Solver((B, T, H, W), Cn, gauss, K, device=ch.device, want_tape=True)
     m = mask.to(torch.float32)
     mn = torch.linalg.vector_norm(m.reshape(B, -1).double(), dim=1).float().clamp_min(1e-30)
     mh = m / mn.view(B, 1, 1, 1)
-    w = np.asarray(w0, np.float64).copy()
-    b = float(b0)
-    opt = AdamW(w.size + 1, lr, weight_decay=weight_decay)
+    opt = AdamWState(list(w0) + [float(b0)], lr, weight_decay=weight_decay, device=ch.device)
     losses = []
     for _ in range(steps):
-        x = solver.forward(ch, w.astype(np.float32), float(b), act)
+        p = opt.w.cpu().tolist()
+        w, b = [float(v) for v in p[:-1]], float(p[-1])
+        x = solver.forward(ch, w, b, act)
         d = x - mh
         losses.append(float((d.double() ** 2).mean()))
         g = (2.0 / x.numel()) * d
-        dw, db = solver.backward(ch, w.astype(np.float32), g.contiguous(), float(b), act)
-        pb = opt.step(np.concatenate([w, [b]]), np.concatenate([dw, [db]]))
-        w, b = pb[:-1], float(pb[-1])
-    return w, b, losses
+        dw, db = solver.backward(ch, w, g.contiguous(), b, act)
+        opt.step(torch.tensor(list(dw) + [db], dtype=torch.float64, device=ch.device))
+    p = opt.w.cpu().tolist()
+    return p[:-1], float(p[-1]), losses

@@ -61,6 +61,7 @@ struct sfseg_comm {
   int nranks = 1;
   int rank = 0;
   int device = 0;
+  int32_t* flag = nullptr;  // device word of the pre-solve validation agreement (dist_agree)
 };
 
 namespace sfseg {

@@ -70,6 +70,23 @@ __device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uin
   lo = l;
 }
 
+// (a, b) -> PL bf16x2 planes (a in the low half): plane i holds bf16 of what planes
+// 0..i-1 left over, so a = sum_i plane_i to 2^-(9 PL) relative (PL = 3: the full fp32
+// significand, 2^-27).  PL = 2 is split_bf16x2.
+template <int PL>
+__device__ __forceinline__ void split_planes(float a, float b, uint32_t (&o)[PL]) {
+#pragma unroll
+  for (int i = 0; i < PL; ++i) {
+    uint32_t h;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+    o[i] = h;
+    if (i + 1 < PL) {
+      a -= __uint_as_float(h << 16);
+      b -= __uint_as_float(h & 0xffff0000u);
+    }
+  }
+}
+
 // L2 eviction-priority policy (createpolicy) and a hinted 16-byte global store.
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;

@@ -7,13 +7,8 @@ namespace {
 template <int RT, int R, bool OPT>
 cudaError_t f3d_launch_opt(const F3dParams& P, int grid, cudaStream_t st) {
   const size_t smem = f3d_smem_bytes(RT, R);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(f3d_kernel<RT, R, OPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(f3d_kernel<RT, R, OPT>), smem);
+  if (e != cudaSuccess) return e;
   f3d_kernel<RT, R, OPT><<<grid, kF3dThreads, smem, st>>>(P);
   return cudaGetLastError();
 }

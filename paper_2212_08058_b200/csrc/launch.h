@@ -6,7 +6,6 @@
 #include "spass.cuh"
 #include "tpass.cuh"
 #include "f3d.cuh"
-#include "mk.cuh"
 
 namespace sfseg {
 cudaError_t launch_spass_fwd(int R, const SpassParams& P, int grid, cudaStream_t st);
@@ -21,6 +20,7 @@ cudaError_t launch_spass_tc(int R, const SpassParams& P, int grid, cudaStream_t 
 bool f3d_supported(int RT, int R);
 int f3d_occupancy(int RT, int R);
 cudaError_t launch_f3d(int RT, int R, const F3dParams& P, int grid, cudaStream_t st);
-bool mk_supported(int RT, int R);
-cudaError_t launch_mk(int RT, int R, const MkParams& P, int* grid_out, cudaStream_t st, bool launch);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
+// per device, so a process-wide "done" flag would skip it on the second GPU (sfseg_api.cu).
+cudaError_t set_smem_attr_once(const void* kernel, size_t smem);
 }  // namespace sfseg

@@ -6,6 +6,9 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstddef>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -23,9 +26,26 @@
 #include "full.cuh"
 #include "online.cuh"
 #include "bwd.cuh"
+#include "learn.cuh"
 #include "launch.h"
 
 using namespace sfseg;
+
+namespace sfseg {
+cudaError_t set_smem_attr_once(const void* kernel, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = done.find({kernel, dev});
+  if (it != done.end() && it->second >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done[{kernel, dev}] = smem;
+  return e;
+}
+}  // namespace sfseg
 
 namespace {
 
@@ -38,28 +58,22 @@ namespace {
     }                                                                   \
   } while (0)
 
-// Process-wide forward-path selection (sfseg_set_algorithm): auto / force the
-// two-pass tpass+spass iteration (tests compare both paths on small radii).
-int g_algorithm = SFSEG_ALGO_AUTO;
-
 cudaError_t& last_cuda_error() {
   static thread_local cudaError_t e = cudaSuccess;
   return e;
 }
 
-// SFSEG_DEBUG_SYNC=1: synchronise after every launch and name the failing kernel.
-bool debug_sync() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SFSEG_DEBUG_SYNC");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
+// Debug builds only (-DSFSEG_DEBUG_SYNC): synchronise after every launch and name the
+// failing kernel.  The release library never synchronises inside an asynchronous call.
 cudaError_t after_launch(const char* name, cudaStream_t st) {
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess && debug_sync()) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess && debug_sync()) fprintf(stderr, "[sfseg] kernel %s failed: %s\n", name, cudaGetErrorString(e));
+#ifdef SFSEG_DEBUG_SYNC
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) fprintf(stderr, "[sfseg] kernel %s failed: %s\n", name, cudaGetErrorString(e));
+#else
+  (void)name;
+  (void)st;
+#endif
   return e;
 }
 
@@ -97,13 +111,17 @@ void gauss_taps(double sigma, int r, int Rpad, float* out /* 2*Rpad+1 */) {
   }
 }
 
+// SM count of the CURRENT device (cached per device id: plans are made per call on the
+// caller's current device).
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+  std::atomic<int>& c = cache[dev & 63];
+  int n = c.load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    c.store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -151,15 +169,15 @@ int spass_occupancy(int R) {
   }
 }
 
+}  // namespace
 // ------------------------------------------------------------------ optional per-kernel event timing
-// (bench instrumentation: sfseg_profile_enable / sfseg_profile_read)
+// (bench instrumentation: a caller-owned sfseg_profiler passed in sfseg_options)
 struct ProfRec {
   int cat;
   cudaEvent_t a, b;
 };
-struct Profiler {
+struct sfseg_profiler {
   std::mutex mu;
-  bool on = false;
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t get() {
@@ -173,31 +191,28 @@ struct Profiler {
     return e;
   }
 };
-Profiler& prof() {
-  static Profiler p;
-  return p;
-}
+namespace {
+using Profiler = sfseg_profiler;
 enum ProfCat { PC_TPASS = 0, PC_SPASS = 1, PC_ONCE = 2, PC_BWD = 3, PC_F3D = 4, PC_MK = 5, PC_N = 6 };
 
 // RAII scope that brackets a launch with events when profiling is on.
 struct ProfScope {
+  Profiler* p;
   cudaStream_t st;
   int cat;
   cudaEvent_t a = nullptr, b = nullptr;
-  ProfScope(cudaStream_t s, int c) : st(s), cat(c) {
-    Profiler& p = prof();
-    if (!p.on) return;
-    std::lock_guard<std::mutex> g(p.mu);
-    a = p.get();
-    b = p.get();
+  ProfScope(Profiler* prof, cudaStream_t s, int c) : p(prof), st(s), cat(c) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(p->mu);
+    a = p->get();
+    b = p->get();
     cudaEventRecord(a, st);
   }
   ~ProfScope() {
     if (!a) return;
-    Profiler& p = prof();
     cudaEventRecord(b, st);
-    std::lock_guard<std::mutex> g(p.mu);
-    p.recs.push_back({cat, a, b});
+    std::lock_guard<std::mutex> g(p->mu);
+    p->recs.push_back({cat, a, b});
   }
 };
 
@@ -229,16 +244,24 @@ struct Plan {
   int TX, TY;         // f3d tiles per frame (64 columns x f3d_th(RS) rows)
   int64_t U3;         // f3d units = B * TY * TX * T
   int G3;             // f3d grid
-  bool mk;            // persistent wavefront megakernel for the forward (large radii, no tape)
-  int NF, NFC, NCC, NCOLS;  // megakernel T-item geometry
+  int algo;           // SFSEG_ALGO_* of this call (sfseg_options; no process-global switch)
+  Profiler* prof;     // per-launch event timing (nullable)
   // workspace offsets
-  size_t off_sc, off_part, off_out, off_F, off_p, off_v, off_p2, off_mk, off_xbar, off_Fbar, off_x0p, ws_fwd, ws_bwd;
-  size_t mk_part, mk_nu, mk_ctr, mk_ctr_bytes;  // offsets inside the megakernel region
+  size_t off_sc, off_part, off_out, off_F, off_p, off_v, off_p2, off_xbar, off_Fbar, off_x0p, ws_fwd, ws_bwd;
   size_t n_part;
   size_t tape_nu_bytes, tape_bytes;
 };
 
-sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan* P) {
+bool valid_algo(int32_t algo) {
+  return algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_FP32;
+}
+
+sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan* P,
+                       const sfseg_options* opt = nullptr) {
+  const int algo = opt ? opt->algo : SFSEG_ALGO_AUTO;
+  if (!valid_algo(algo)) return SFSEG_ERR_INVALID_ARGUMENT;
+  P->algo = algo;
+  P->prof = opt ? opt->profiler : nullptr;
   if (C < 1 || C > kMaxC) return C < 1 ? SFSEG_ERR_INVALID_ARGUMENT : SFSEG_ERR_UNSUPPORTED;
   if (K < 1) return SFSEG_ERR_INVALID_ARGUMENT;
   if (!(g.sigma_t > 0.0) || !(g.sigma_s > 0.0) || !std::isfinite(g.sigma_t) || !std::isfinite(g.sigma_s))
@@ -267,18 +290,13 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   const int64_t cap = (int64_t)num_sms() * spass_occupancy(P->RS);
   P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 4));
   P->gx = ew_gx(P->H, P->BT);
-  P->tc = g_algorithm != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
+  P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
   P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * spass_tc_occupancy(P->RS), P->U / 4));
-  P->f3d = (g_algorithm == SFSEG_ALGO_AUTO || g_algorithm == SFSEG_ALGO_MEGAKERNEL) && f3d_supported(P->RT, P->RS);
+  P->f3d = algo == SFSEG_ALGO_AUTO && f3d_supported(P->RT, P->RS);
   P->TX = (int)((sh.W + kF3dTW - 1) / kF3dTW);
   P->TY = (int)((sh.H + f3d_th(std::min(P->RS, kF3dMaxR)) - 1) / f3d_th(std::min(P->RS, kF3dMaxR)));
   P->U3 = P->B * P->TY * P->TX * P->T;
   P->G3 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * f3d_occupancy(P->RT, P->RS), P->U3 / 4));
-  P->mk = g_algorithm == SFSEG_ALGO_MEGAKERNEL && !P->f3d && mk_supported(P->RT, P->RS);
-  P->NF = (int)std::min<int64_t>(P->T, mk_nf(P->RT));
-  P->NFC = (int)((P->T + P->NF - 1) / P->NF);
-  P->NCOLS = 4;
-  P->NCC = (int)((P->H * P->Wp / 4 + 128 * P->NCOLS - 1) / (128 * P->NCOLS));
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
   size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max({(size_t)P->G * kSpassPartSlots, (size_t)P->Gtc, (size_t)P->G3 * kF3dCW}),
                                    2 * (size_t)P->BT * P->gx);
@@ -301,20 +319,8 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   off += vb;
   P->off_v = off;
   off += vb;
-  P->off_p2 = off;  // second iterate buffer (megakernel ping-pong)
+  P->off_p2 = off;  // scratch volume (backward: u = G_xy * v of the tensor-core plain pass)
   off += vb;
-  P->off_mk = off;
-  {
-    const size_t nk = (size_t)(K + 1) * P->B;
-    P->mk_part = 0;
-    size_t m = align_up(sizeof(double) * nk * (size_t)P->T * P->S * 2);
-    P->mk_nu = m;
-    m += align_up(sizeof(double) * nk * 2);
-    P->mk_ctr = m;
-    P->mk_ctr_bytes = sizeof(unsigned) * (1 + nk * ((size_t)P->NFC + P->T + 2));
-    m += align_up(P->mk_ctr_bytes);
-    off += m;
-  }
   P->ws_fwd = off;
   P->off_xbar = off;
   off += vb;
@@ -326,6 +332,15 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->tape_nu_bytes = align_up(sizeof(double) * P->B * K);
   P->tape_bytes = P->tape_nu_bytes + (size_t)K * vb;
   return SFSEG_OK;
+}
+
+// Zero the per-call part of the workspace (counters, per-volume scalars) but NOT the error
+// word: device errors are sticky across calls on one workspace until sfseg_sync_status reads
+// and clears them (online windows, pipelined solves).  A fresh workspace's header is zeroed
+// once by sfseg_workspace_reset.
+cudaError_t clear_header(void* ws, size_t bytes, cudaStream_t st) {
+  static_assert(offsetof(WsHeader, err) == 0, "error word first");
+  return cudaMemsetAsync(static_cast<char*>(ws) + sizeof(unsigned), 0, bytes - sizeof(unsigned), st);
 }
 
 template <class T>
@@ -472,7 +487,7 @@ sfseg_status rank_setup(Rank& r, cudaStream_t st) {
   r.hhi = at<float>(r.ws, r.so.off_hhi);
   r.loc = at<double>(r.ws, r.so.off_loc);
   r.glob = at<double>(r.ws, r.so.off_glob);
-  SF_CUDA(cudaMemsetAsync(r.ws, 0, P.off_part, st));
+  SF_CUDA(clear_header(r.ws, P.off_part, st));
   std::memset(&r.sp, 0, sizeof(r.sp));
   if (!make_spass_fwd_tmap(&r.sp.tmap, P, r.v)) return SFSEG_ERR_CUDA;
   fill_spass_common(r.sp, P, r.ws);
@@ -518,7 +533,7 @@ sfseg_status ph_finalize(Rank& r, int k, cudaStream_t st) {
 }
 
 sfseg_status ph_T(Rank& r, cudaStream_t st) {
-  ProfScope ps(st, PC_TPASS);
+  ProfScope ps(r.P.prof, st, PC_TPASS);
   SF_CUDA(launch_tpass_fwd(r.P.RT, r.tp, (int)r.P.B, st));
   SF_CUDA(after_launch("tpass(slab)", st));
   return SFSEG_OK;
@@ -529,7 +544,7 @@ sfseg_status ph_S(Rank& r, int k, cudaStream_t st) {
   r.sp.pprev = r.rayleigh ? r.p : nullptr;
   r.sp.k = k;
   r.sp.last = (k == r.P.K) ? 1 : 0;
-  ProfScope ps(st, PC_SPASS);
+  ProfScope ps(r.P.prof, st, PC_SPASS);
   SF_CUDA(launch_spass_forward(r.P, r.sp, st));
   SF_CUDA(after_launch("spass(slab)", st));
   return SFSEG_OK;
@@ -607,15 +622,42 @@ sfseg_status local_allreduce(std::vector<Rank>& R, cudaStream_t st) {
   return SFSEG_OK;
 }
 
+// Every rank's argument check ends in one agreement allreduce (max of the status codes,
+// on the communicator's own device word) BEFORE the first data-path collective, so a rank
+// that fails validation cannot leave its peers blocked in ncclAllReduce / ncclSend.
+// Syncs `st` once (the host needs the agreed status).
+sfseg_status dist_agree(sfseg_comm* c, sfseg_status mine, cudaStream_t st) {
+  NcclApi& api = nccl();
+  if (!api.ok || !c->flag) return SFSEG_ERR_NCCL;
+  int32_t h = (int32_t)mine;
+  SF_CUDA(cudaMemcpyAsync(c->flag, &h, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  if (api.AllReduce(c->flag, c->flag, 1, ncclInt32, ncclMax, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
+  SF_CUDA(cudaMemcpyAsync(&h, c->flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  return (sfseg_status)h;
+}
+
 // One rank of an NCCL-connected time-slab solve.
-sfseg_status dist_power_iterate(const Plan& P, const float* ch, const float* w_host, float b, int act,
-                                const float* x0, float* x_out, float* F_out, double* stats, int want_rayleigh,
-                                void* tape, void* ws, size_t ws_bytes, const sfseg_dist* dist, void* stream) {
-  if (!dist->comm || !dist->comm->comm) return SFSEG_ERR_INVALID_ARGUMENT;
-  if (tape || F_out) return SFSEG_ERR_UNSUPPORTED;  // backward / F export are single-GPU only for now
+sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
+                                sfseg_shape sh, sfseg_gauss gauss, int32_t K, const float* x0, float* x_out,
+                                float* F_out, double* stats, int32_t want_rayleigh, void* tape, void* ws,
+                                size_t ws_bytes, const sfseg_dist* dist, const sfseg_options* opt, void* stream) {
+  if (!dist->comm || !dist->comm->comm) return SFSEG_ERR_INVALID_ARGUMENT;  // no communicator to agree on
   sfseg_comm* c = dist->comm;
-  if (dist->t_offset < 0 || dist->t_offset + P.T > dist->T_global) return SFSEG_ERR_SHAPE;
-  if (c->nranks > 1 && P.T < P.RT) return SFSEG_ERR_SHAPE;  // halo must come from one neighbour
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // ---- local validation: no early return before the agreement
+  Plan P;
+  sfseg_status s = SFSEG_OK;
+  if (!ch || !w_host || !x_out || !validate_act(act)) s = SFSEG_ERR_INVALID_ARGUMENT;
+  else if ((s = make_plan(sh, C, gauss, K, &P, opt)) != SFSEG_OK) {
+  } else if (!finite_weights(w_host, C, b)) s = SFSEG_ERR_INVALID_ARGUMENT;
+  else if (tape || F_out) s = SFSEG_ERR_UNSUPPORTED;  // backward / F export are single-GPU only
+  else if (dist->t_offset < 0 || dist->t_offset + P.T > dist->T_global) s = SFSEG_ERR_SHAPE;
+  else if (c->nranks > 1 && P.T < P.RT) s = SFSEG_ERR_SHAPE;  // the halo must come from one neighbour
+  else s = check_ws(ws, ws_bytes, slab_offsets(P).total);
+  const sfseg_status agreed = dist_agree(c, s, st);
+  if (s != SFSEG_OK) return s;
+  if (agreed != SFSEG_OK) return agreed;  // a peer failed its validation: nobody starts the solve
   Rank r;
   r.P = P;
   r.ch = ch;
@@ -628,9 +670,6 @@ sfseg_status dist_power_iterate(const Plan& P, const float* ch, const float* w_h
   r.ws = ws;
   r.has_lo = dist->t_offset > 0 && c->rank > 0;
   r.has_hi = dist->t_offset + P.T < dist->T_global && c->rank < c->nranks - 1;
-  sfseg_status s = check_ws(ws, ws_bytes, slab_offsets(P).total);
-  if (s != SFSEG_OK) return s;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   if ((s = rank_setup(r, st)) != SFSEG_OK) return s;
   if ((s = ph_combine(r, w_host, b, act, st)) != SFSEG_OK) return s;
   if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) return s;
@@ -673,25 +712,18 @@ int32_t sfseg_abi_version(void) { return SFSEG_ABI_VERSION; }
 
 const char* sfseg_last_cuda_error(void) { return cudaGetErrorString(last_cuda_error()); }
 
-sfseg_status sfseg_forward_path(sfseg_shape sh, sfseg_gauss g, int32_t* info) {
+sfseg_status sfseg_forward_path(sfseg_shape sh, sfseg_gauss g, int32_t algo, int32_t* info) {
   if (!info) return SFSEG_ERR_INVALID_ARGUMENT;
   Plan P;
-  sfseg_status s = make_plan(sh, 1, g, 1, &P);
+  const sfseg_options opt{algo, nullptr};
+  sfseg_status s = make_plan(sh, 1, g, 1, &P, &opt);
   if (s != SFSEG_OK) return s;
-  info[0] = P.f3d ? SFSEG_PATH_FUSED_3D : P.mk ? SFSEG_PATH_MEGAKERNEL : P.tc ? SFSEG_PATH_TWO_PASS_TC
-                                                                            : SFSEG_PATH_TWO_PASS_FP32;
+  info[0] = P.f3d ? SFSEG_PATH_FUSED_3D : P.tc ? SFSEG_PATH_TWO_PASS_TC : SFSEG_PATH_TWO_PASS_FP32;
   info[1] = P.RT;
   info[2] = P.RS;
   return SFSEG_OK;
 }
 
-sfseg_status sfseg_set_algorithm(int32_t algo) {
-  if (algo != SFSEG_ALGO_AUTO && algo != SFSEG_ALGO_TWO_PASS && algo != SFSEG_ALGO_MEGAKERNEL &&
-      algo != SFSEG_ALGO_TWO_PASS_FP32)
-    return SFSEG_ERR_INVALID_ARGUMENT;
-  g_algorithm = algo;
-  return SFSEG_OK;
-}
 
 void sfseg_max_radii(int32_t* rs, int32_t* rt) {
   if (rs) *rs = kMaxRS;
@@ -742,19 +774,28 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
                                  sfseg_shape sh, sfseg_gauss gauss, int32_t K, const float* x0, float* x_out,
                                  float* F_out, double* stats, int32_t want_rayleigh, void* tape, void* ws,
                                  size_t ws_bytes, const sfseg_dist* dist, void* stream) {
+  return sfseg_power_iterate_ex(ch, C, w_host, b, act, sh, gauss, K, x0, x_out, F_out, stats, want_rayleigh, tape,
+                                ws, ws_bytes, dist, nullptr, stream);
+}
+
+sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
+                                    sfseg_shape sh, sfseg_gauss gauss, int32_t K, const float* x0, float* x_out,
+                                    float* F_out, double* stats, int32_t want_rayleigh, void* tape, void* ws,
+                                    size_t ws_bytes, const sfseg_dist* dist, const sfseg_options* opt,
+                                    void* stream) {
+  if (dist) return dist_power_iterate(ch, C, w_host, b, act, sh, gauss, K, x0, x_out, F_out, stats, want_rayleigh,
+                                      tape, ws, ws_bytes, dist, opt, stream);
   if (!ch || !w_host || !x_out || !validate_act(act)) return SFSEG_ERR_INVALID_ARGUMENT;
   Plan P;
-  sfseg_status s = make_plan(sh, C, gauss, K, &P);
+  sfseg_status s = make_plan(sh, C, gauss, K, &P, opt);
   if (s != SFSEG_OK) return s;
   if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
-  if (dist) return dist_power_iterate(P, ch, w_host, b, act, x0, x_out, F_out, stats, want_rayleigh, tape,
-                                             ws, ws_bytes, dist, stream);
   if ((s = check_ws(ws, ws_bytes, P.ws_fwd)) != SFSEG_OK) return s;
   if (tape && (reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) return SFSEG_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   // header + per-volume scalars start from zero
-  SF_CUDA(cudaMemsetAsync(ws, 0, P.off_part, st));
+  SF_CUDA(clear_header(ws, P.off_part, st));
 
   float* F = at<float>(ws, P.off_F);
   float* p = at<float>(ws, P.off_p);
@@ -804,8 +845,6 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     for (int i = 0; i < 2 * P.RT + 1; ++i) fp.gt[i] = P.gt[i];
     for (int d = 0; d <= P.RS; ++d) fp.gs[d] = P.gs[P.RS + d];
     float* last_out = p;
-    const char* f3d_trace = std::getenv("SFSEG_F3D_TRACE");  // debug: per-CTA timing of the last launch
-    if (f3d_trace && *f3d_trace) SF_CUDA(cudaMalloc(&fp.trace, sizeof(unsigned long long) * 4 * P.G3));
     for (int k = 1; k <= K; ++k) {
       const bool odd = (k & 1) != 0;
       fp.tmap = odd ? map_p : map_v;
@@ -813,100 +852,14 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
       fp.tape_u = tape ? tape_u(k - 1) : nullptr;
       fp.k = k;
       fp.last = (k == K) ? 1 : 0;
-      ProfScope ps(st, PC_F3D);
+      ProfScope ps(P.prof, st, PC_F3D);
       SF_CUDA(launch_f3d(P.RT, P.RS, fp, P.G3, st));
       SF_CUDA(after_launch("f3d", st));
       last_out = fp.out;
     }
-    if (fp.trace) {
-      std::vector<unsigned long long> h((size_t)4 * P.G3);
-      SF_CUDA(cudaMemcpyAsync(h.data(), fp.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
-      SF_CUDA(cudaStreamSynchronize(st));
-      cudaFree(fp.trace);
-      if (FILE* f = std::fopen(f3d_trace, "w")) {
-        std::fprintf(f, "cta,sm,t_start,t_bar,t_exit\n");
-        for (int i = 0; i < P.G3; ++i)
-          std::fprintf(f, "%d,%llu,%llu,%llu,%llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
-        std::fclose(f);
-      }
-    }
     dim3 grid((unsigned)P.gx, (unsigned)P.BT);
     final_scale_kernel<<<grid, kEwThreads, 0, st>>>(last_out, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H,
                                                     (int)P.W, (int)P.Wp, (int)P.T, 0);
-    SF_CUDA(after_launch("final_scale", st));
-    return SFSEG_OK;
-  }
-
-  if (P.mk && !tape) {
-    // all K iterations in one persistent launch (mk.cuh), then the lagged-norm finalize
-    MkParams mp;
-    std::memset(&mp, 0, sizeof(mp));
-    if (!make_volume_tmap(&mp.sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))) return SFSEG_ERR_CUDA;
-    fill_spass_common(mp.sp, P, ws);
-    char* mkb = static_cast<char*>(ws) + P.off_mk;
-    mp.pbuf0 = p;
-    mp.pbuf1 = at<float>(ws, P.off_p2);
-    mp.v = v;
-    mp.sc = at<double>(ws, P.off_sc);
-    mp.part = reinterpret_cast<double*>(mkb + P.mk_part);
-    mp.nu = reinterpret_cast<double*>(mkb + P.mk_nu);
-    unsigned* ctr = reinterpret_cast<unsigned*>(mkb + P.mk_ctr);
-    const size_t nk = (size_t)(K + 1) * P.B;
-    mp.ticket = ctr;
-    mp.tdone = ctr + 1;
-    mp.sdone = mp.tdone + nk * P.NFC;
-    mp.sall = mp.sdone + nk * P.T;
-    mp.nready = mp.sall + nk;
-    mp.frame4 = P.H * P.Wp / 4;
-    mp.B = (int)P.B;
-    mp.T = (int)P.T;
-    mp.S = P.S;
-    mp.K = K;
-    mp.NF = P.NF;
-    mp.NFC = P.NFC;
-    mp.NCC = P.NCC;
-    mp.NCOLS = P.NCOLS;
-    mp.rayleigh = want_rayleigh ? 1 : 0;
-    for (int i = 0; i < 2 * P.RT + 1; ++i) mp.gt[i] = P.gt[i];
-    SF_CUDA(cudaMemsetAsync(ctr, 0, P.mk_ctr_bytes, st));
-    // debug: SFSEG_MK_TRACE=<file> records per-item timestamps of this solve (syncs)
-    const char* trace_path = std::getenv("SFSEG_MK_TRACE");
-    const long n_items = (long)K * P.B * ((long)P.NFC * P.NCC + (long)P.T * P.S);
-    if (trace_path && *trace_path) SF_CUDA(cudaMalloc(&mp.trace, sizeof(unsigned long long) * 4 * n_items));
-    int grid = 0;
-    {
-      ProfScope ps(st, PC_MK);
-      SF_CUDA(launch_mk(P.RT, P.RS, mp, &grid, st, true));
-      SF_CUDA(after_launch("mk", st));
-    }
-    if (mp.trace) {
-      std::vector<unsigned long long> h((size_t)4 * n_items);
-      SF_CUDA(cudaMemcpyAsync(h.data(), mp.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
-      SF_CUDA(cudaStreamSynchronize(st));
-      cudaFree(mp.trace);
-      mp.trace = nullptr;
-      if (FILE* f = std::fopen(trace_path, "w")) {
-        std::fprintf(f, "# grid=%d NF=%d NFC=%d NCC=%d S=%d T=%d K=%d\nticket,sm,kind,t_grab,t_ready,t_done\n", grid,
-                     P.NF, P.NFC, P.NCC, P.S, (int)P.T, K);
-        for (long i = 0; i < n_items; ++i)
-          std::fprintf(f, "%ld,%llu,%llu,%llu,%llu,%llu\n", i, h[4 * i] >> 8, h[4 * i] & 255ull, h[4 * i + 1],
-                       h[4 * i + 2], h[4 * i + 3]);
-        std::fclose(f);
-      }
-    }
-    MkFinParams fp;
-    fp.nu = mp.nu;
-    fp.sc = at<double>(ws, P.off_sc);
-    fp.stats = stats;
-    fp.err = &at<WsHeader>(ws, 0)->err;
-    fp.B = (int)P.B;
-    fp.K = K;
-    fp.rayleigh = mp.rayleigh;
-    mk_finalize_kernel<<<(unsigned)((P.B + 127) / 128), 128, 0, st>>>(fp);
-    SF_CUDA(after_launch("mk_finalize", st));
-    dim3 grid2((unsigned)P.gx, (unsigned)P.BT);
-    final_scale_kernel<<<grid2, kEwThreads, 0, st>>>((K & 1) ? mp.pbuf1 : mp.pbuf0, x_out, at<double>(ws, P.off_sc),
-                                                     (int)P.T, (int)P.H, (int)P.W, (int)P.Wp, (int)P.T, 0);
     SF_CUDA(after_launch("final_scale", st));
     return SFSEG_OK;
   }
@@ -926,7 +879,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
   for (int k = 1; k <= K; ++k) {
     // (a2)+(a3) v = s_{k-1} * G_t * p_{k-1}
     {
-      ProfScope ps(st, PC_TPASS);
+      ProfScope ps(P.prof, st, PC_TPASS);
       SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
       SF_CUDA(after_launch("tpass_fwd", st));
     }
@@ -937,7 +890,7 @@ sfseg_status sfseg_power_iterate(const float* ch, int32_t C, const float* w_host
     sp.k = k;
     sp.last = (k == K) ? 1 : 0;
     {
-      ProfScope ps(st, PC_SPASS);
+      ProfScope ps(P.prof, st, PC_SPASS);
       SF_CUDA(launch_spass_forward(P, sp, st));
       SF_CUDA(after_launch("spass_fwd", st));
     }
@@ -957,16 +910,25 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
                                           const void* tape, const float* dL_dx, double* dL_dw_host,
                                           double* dL_db_host, void* ws, size_t ws_bytes, const sfseg_dist* dist,
                                           void* stream) {
+  return sfseg_power_iterate_backward_ex(ch, C, w_host, b, act, sh, gauss, K, x0, tape, dL_dx, dL_dw_host,
+                                         dL_db_host, ws, ws_bytes, dist, nullptr, stream);
+}
+
+sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
+                                             sfseg_shape sh, sfseg_gauss gauss, int32_t K, const float* x0,
+                                             const void* tape, const float* dL_dx, double* dL_dw_host,
+                                             double* dL_db_host, void* ws, size_t ws_bytes, const sfseg_dist* dist,
+                                             const sfseg_options* opt, void* stream) {
   if (!ch || !w_host || !tape || !dL_dx || !dL_dw_host || !validate_act(act)) return SFSEG_ERR_INVALID_ARGUMENT;
   Plan P;
-  sfseg_status s = make_plan(sh, C, gauss, K, &P);
+  sfseg_status s = make_plan(sh, C, gauss, K, &P, opt);
   if (s != SFSEG_OK) return s;
   if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
   if (dist) return SFSEG_ERR_UNSUPPORTED;
   if ((s = check_ws(ws, ws_bytes, P.ws_bwd)) != SFSEG_OK) return s;
   if ((reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) return SFSEG_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SF_CUDA(cudaMemsetAsync(ws, 0, P.off_part, st));
+  SF_CUDA(clear_header(ws, P.off_part, st));
 
   float* F = at<float>(ws, P.off_F);
   float* v = at<float>(ws, P.off_v);
@@ -1049,7 +1011,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
   for (int k = K; k >= 1; --k) {
     tp.u1 = tape_u(k - 1);
     {
-      ProfScope ps(st, PC_BWD);
+      ProfScope ps(P.prof, st, PC_BWD);
       SF_CUDA(launch_tpass_bwd(P.RT, tp, (int)P.B, st));
       SF_CUDA(after_launch("tpass_bwd", st));
     }
@@ -1061,7 +1023,7 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
       pl.plain = 1;
       pl.out = ubuf;
       {
-        ProfScope ps(st, PC_BWD);
+        ProfScope ps(P.prof, st, PC_BWD);
         SF_CUDA(launch_spass_forward(P, pl, st));
         SF_CUDA(after_launch("spass_tc(plain, bwd)", st));
       }
@@ -1069,12 +1031,12 @@ sfseg_status sfseg_power_iterate_backward(const float* ch, int32_t C, const floa
       be.u2 = sp.u2;
       be.k = k;
       {
-        ProfScope ps(st, PC_BWD);
+        ProfScope ps(P.prof, st, PC_BWD);
         bwd_epi_kernel<<<dim3((unsigned)P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(be);
         SF_CUDA(after_launch("bwd_epi", st));
       }
     } else {
-      ProfScope ps(st, PC_BWD);
+      ProfScope ps(P.prof, st, PC_BWD);
       SF_CUDA(launch_spass_bwd(P.RS, sp, P.G, st));
       SF_CUDA(after_launch("spass_bwd", st));
     }
@@ -1162,7 +1124,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
                                       const float* f_ch, int32_t Cf, const float* wf_host, float bf, int32_t act_f,
                                       double p, double alpha, sfseg_shape sh, sfseg_gauss gauss, int32_t K,
                                       const float* x0, float* x_out, double* stats, const sfseg_binarize* bin,
-                                      void* ws, size_t ws_bytes, void* stream) {
+                                      void* ws, size_t ws_bytes, const sfseg_options* opt, void* stream) {
   if (!s_ch || !f_ch || !ws_host || !wf_host || !x_out || !validate_act(act_s) || !validate_act(act_f))
     return SFSEG_ERR_INVALID_ARGUMENT;
   if (bin && (bin->n_cont < 0 || !(bin->kappa0 > 0.f) || !std::isfinite(bin->kappa0) || !(bin->growth > 0.f) ||
@@ -1171,12 +1133,12 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   sfseg_status s = full_check(Cs, Cf, p, alpha);
   if (s != SFSEG_OK) return s;
   Plan P;
-  if ((s = make_plan(sh, std::max(Cs, Cf), gauss, K, &P)) != SFSEG_OK) return s;
+  if ((s = make_plan(sh, std::max(Cs, Cf), gauss, K, &P, opt)) != SFSEG_OK) return s;
   if (!finite_weights(ws_host, Cs, bs) || !finite_weights(wf_host, Cf, bf)) return SFSEG_ERR_INVALID_ARGUMENT;
   const FullLayout L = full_layout(P);
   if ((s = check_ws(ws, ws_bytes, L.total)) != SFSEG_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SF_CUDA(cudaMemsetAsync(ws, 0, P.off_part, st));
+  SF_CUDA(clear_header(ws, P.off_part, st));
   float* U = at<float>(ws, L.off_U);
   float* F = at<float>(ws, L.off_F);
   float* a = at<float>(ws, L.off_a);
@@ -1250,7 +1212,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   for (int k = 1; k <= K; ++k) {
     for (int c = 0; c < 3; ++c) {
       {
-        ProfScope ps(st, PC_TPASS);
+        ProfScope ps(P.prof, st, PC_TPASS);
         if (fexp[c] == 0) {
           SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
         } else {
@@ -1262,7 +1224,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
       sp.out = uo[c];
       sp.k = k;
       {
-        ProfScope ps(st, PC_SPASS);
+        ProfScope ps(P.prof, st, PC_SPASS);
         SF_CUDA(launch_spass_forward(P, sp, st));
         SF_CUDA(after_launch("spass_plain", st));
       }
@@ -1366,6 +1328,8 @@ sfseg_status sfseg_power_iterate_online(const float* ch, int32_t C, const float*
                                         sfseg_shape sh, sfseg_gauss gauss, int32_t K, int32_t q, int32_t stride,
                                         float* x_out, void* ws, size_t ws_bytes, void* stream) {
   if (!ch || !w_host || !x_out || !validate_act(act) || stride < 1) return SFSEG_ERR_INVALID_ARGUMENT;
+  // windows must tile the video: a stride longer than the window would leave frames unwritten
+  if (q < sh.T && stride > q) return SFSEG_ERR_INVALID_ARGUMENT;
   OnlineLayout L;
   sfseg_status s = online_layout(sh, C, gauss, K, q, &L);
   if (s != SFSEG_OK) return s;
@@ -1444,6 +1408,13 @@ sfseg_status sfseg_threshold(const float* x, sfseg_shape sh, float tau, int32_t 
   return map_cuda(cudaGetLastError());
 }
 
+sfseg_status sfseg_workspace_reset(void* ws, void* stream) {
+  if (!ws) return SFSEG_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return SFSEG_ERR_WORKSPACE;
+  SF_CUDA(cudaMemsetAsync(ws, 0, align_up(sizeof(WsHeader)), static_cast<cudaStream_t>(stream)));
+  return SFSEG_OK;
+}
+
 sfseg_status sfseg_sync_status(void* ws, void* stream) {
   if (!ws) return SFSEG_ERR_INVALID_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1507,7 +1478,12 @@ sfseg_status sfseg_comm_create(const uint8_t id_host[128], int32_t nranks, int32
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
+  if (cudaMalloc(&c->flag, sizeof(int32_t)) != cudaSuccess) {  // agreement word (setup call, not a solve)
+    delete c;
+    return SFSEG_ERR_CUDA;
+  }
   if (api.CommInitRank(&c->comm, nranks, id, rank) != ncclSuccess) {
+    cudaFree(c->flag);
     delete c;
     return SFSEG_ERR_NCCL;
   }
@@ -1520,20 +1496,32 @@ sfseg_status sfseg_comm_destroy(sfseg_comm* c) {
   NcclApi& api = nccl();
   sfseg_status s = SFSEG_OK;
   if (c->comm && api.ok && api.CommDestroy(c->comm) != ncclSuccess) s = SFSEG_ERR_NCCL;
+  if (c->flag) cudaFree(c->flag);
   delete c;
   return s;
 }
 
-sfseg_status sfseg_profile_enable(int32_t on) {
-  Profiler& p = prof();
-  std::lock_guard<std::mutex> g(p.mu);
-  p.on = on != 0;
+sfseg_status sfseg_profiler_create(sfseg_profiler** out) {
+  if (!out) return SFSEG_ERR_INVALID_ARGUMENT;
+  *out = new (std::nothrow) sfseg_profiler;
+  return *out ? SFSEG_OK : SFSEG_ERR_CUDA;
+}
+
+sfseg_status sfseg_profiler_destroy(sfseg_profiler* p) {
+  if (!p) return SFSEG_ERR_INVALID_ARGUMENT;
+  for (ProfRec& r : p->recs) {
+    cudaEventSynchronize(r.b);
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : p->pool) cudaEventDestroy(e);
+  delete p;
   return SFSEG_OK;
 }
 
-sfseg_status sfseg_profile_read(double* ms_host, int64_t* count_host) {
-  if (!ms_host || !count_host) return SFSEG_ERR_INVALID_ARGUMENT;
-  Profiler& p = prof();
+sfseg_status sfseg_profiler_read(sfseg_profiler* pp, double* ms_host, int64_t* count_host) {
+  if (!pp || !ms_host || !count_host) return SFSEG_ERR_INVALID_ARGUMENT;
+  Profiler& p = *pp;
   std::lock_guard<std::mutex> g(p.mu);
   for (int i = 0; i < PC_N; ++i) {
     ms_host[i] = 0.0;
@@ -1574,7 +1562,7 @@ sfseg_status sfseg_slabs_workspace_bytes(sfseg_shape sh, int32_t C, sfseg_gauss 
 sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
                                        sfseg_shape sh, sfseg_gauss gauss, int32_t K, int32_t nslabs,
                                        const float* x0, float* x_out, double* stats, int32_t want_rayleigh,
-                                       void* ws, size_t ws_bytes, void* stream) {
+                                       void* ws, size_t ws_bytes, const sfseg_options* opt, void* stream) {
   if (!ch || !w_host || !x_out || !validate_act(act) || nslabs < 1 || nslabs > kMaxLocalRanks)
     return SFSEG_ERR_INVALID_ARGUMENT;
   if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
@@ -1589,7 +1577,7 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
     const int64_t t0 = slab_start(sh.T, nslabs, i), t1 = slab_start(sh.T, nslabs, i + 1);
     sfseg_shape ls = sh;
     ls.T = t1 - t0;
-    if ((s = make_plan(ls, C, gauss, K, &R[i].P)) != SFSEG_OK) return s;
+    if ((s = make_plan(ls, C, gauss, K, &R[i].P, opt)) != SFSEG_OK) return s;
     if (nslabs > 1 && R[i].P.T < R[i].P.RT) return SFSEG_ERR_SHAPE;
     R[i].ch = ch;
     R[i].x0 = x0;
@@ -1645,6 +1633,30 @@ sfseg_status sfseg_slabs_sync_status(sfseg_shape sh, int32_t C, sfseg_gauss gaus
     off += align_up(slab_offsets(P).total);
   }
   return worst;
+}
+
+// ====================================================================== learning loop (§8(f) f4)
+sfseg_status sfseg_adamw_step(double* w, const double* grad, double* state, int32_t n, int64_t t,
+                              const sfseg_adamw* hp, void* stream) {
+  if (!w || !grad || !state || !hp || n < 1 || t < 1) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (!(hp->lr >= 0.0) || !(hp->beta1 >= 0.0 && hp->beta1 < 1.0) || !(hp->beta2 >= 0.0 && hp->beta2 < 1.0) ||
+      !(hp->eps > 0.0) || !(hp->weight_decay >= 0.0) || !std::isfinite(hp->lr) || !std::isfinite(hp->weight_decay))
+    return SFSEG_ERR_INVALID_ARGUMENT;
+  AdamwParams P;
+  P.w = w;
+  P.grad = grad;
+  P.state = state;
+  P.n = n;
+  P.lr = hp->lr;
+  P.beta1 = hp->beta1;
+  P.beta2 = hp->beta2;
+  P.eps = hp->eps;
+  P.weight_decay = hp->weight_decay;
+  P.c1 = 1.0 - std::pow(hp->beta1, (double)t);
+  P.c2 = 1.0 - std::pow(hp->beta2, (double)t);
+  P.amsgrad = hp->amsgrad ? 1 : 0;
+  adamw_kernel<<<(unsigned)((n + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(P);
+  return map_cuda(cudaGetLastError());
 }
 
 }  // extern "C"

@@ -7,13 +7,8 @@ namespace {
 template <int R, int EPI>
 cudaError_t launch_tc_epi(const SpassParams& P, int grid, cudaStream_t st) {
   const size_t smem = sptc_smem_bytes(R);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(spass_tc_kernel<R, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(spass_tc_kernel<R, EPI>), smem);
+  if (e != cudaSuccess) return e;
   spass_tc_kernel<R, EPI><<<grid, kSpassThreads, smem, st>>>(P);
   return cudaGetLastError();
 }

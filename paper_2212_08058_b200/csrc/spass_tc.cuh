@@ -9,11 +9,14 @@
 // with 3 bf16 products per tap (measured mma.sync bf16 rate 555 TFLOP/s, 7.5x the
 // FP32 peak; tools/mma_microbench.cu, profiles/mma).
 //
-// Precision (reading A23): every operand a is split a = a_hi + a_lo with
-// a_hi = bf16(a), a_lo = bf16(a - a_hi) (|a - a_hi - a_lo| <= 2^-18 |a|), the same for
-// the taps g; each product is a_hi g_hi + a_lo g_hi + a_hi g_lo (the dropped
-// a_lo g_lo <= 2^-18), accumulated in fp32 by the tensor core: relative error per
-// output ~1e-5 worst case, far inside the 1e-4 x_K tolerance.
+// Precision (reading A23): every operand a is split into PL = 3 bf16
+// planes a = a1 + a2 + a3 (a1 = bf16(a), a2 = bf16(a - a1), a3 = bf16(a - a1 - a2);
+// |a - a1 - a2 - a3| <= 2^-27 |a|: the 24-bit fp32 significand in three 8-bit pieces),
+// the same for the taps g, and every tap product is the six terms a_i g_j with
+// i + j <= 4 (a1g1, a2g1, a1g2, a3g1, a2g2, a1g3; the dropped terms are <= 2^-26 of
+// the product), accumulated in fp32 by the tensor core: fp32-class arithmetic
+// (per product below the 2^-24 rounding unit of an fp32 FMA).  PL = 2 (three terms,
+// ~2^-17) is the round-1 variant, kept compilable for A/B only.
 //
 // Tiling.  Same work list, segments, TMA producer, ring streaming and finalize as
 // spass_kernel (spass.cuh header), with:
@@ -21,7 +24,7 @@
 //     Toeplitz slice Tx depends only on the output tile's parity (8-column shift
 //     inside a 16-column k block) and the k step, so its bf16 fragments live in
 //     registers for the whole kernel; warp w: rows 16 (w & 1).., columns 32 (w >> 1)..
-//   ring: x-pass output as two bf16 planes (hi, lo), row-major, row stride 72
+//   ring: x-pass output as PL bf16 planes, row-major, row stride 72
 //     (conflict-free u32 stores and ldmatrix); the x-block grid starts R rows above
 //     the segment so every y window of a 16-row output tile is 16-aligned and never
 //     straddles a 32-row slot: no duplicated rows.
@@ -36,6 +39,15 @@
 namespace sfseg {
 
 constexpr int kTcRingStride = 72;  // bf16 per ring row (64 + 8: conflict-free)
+#ifndef SPTC_PLANES
+#define SPTC_PLANES 3
+#endif
+constexpr int kTcPlanes = SPTC_PLANES;  // bf16 planes per operand (3: fp32-class, 6 products)
+static_assert(kTcPlanes == 2 || kTcPlanes == 3, "2 or 3 bf16 planes");
+// products (i, j) of plane i of the data and plane j of the taps, largest first
+__host__ __device__ constexpr int sptc_nprod() { return kTcPlanes == 3 ? 6 : 3; }
+__host__ __device__ constexpr int sptc_pa(int p) { return p == 1 ? 1 : p == 3 ? 2 : p == 4 ? 1 : 0; }
+__host__ __device__ constexpr int sptc_pb(int p) { return p == 2 ? 1 : p == 4 ? 1 : p == 5 ? 2 : 0; }
 
 __host__ __device__ constexpr int sptc_nkx(int R) { return (16 + spass_ra(R) + R + 15) / 16; }
 __host__ __device__ constexpr int sptc_nky(int R) { return (16 + 2 * R + 15) / 16; }
@@ -44,11 +56,17 @@ __host__ __device__ constexpr int sptc_pro(int R) { return (31 + 2 * R) / 32; }
 __host__ __device__ constexpr int sptc_nslot(int R) { return sptc_pro(R) + 1; }
 __host__ __device__ constexpr size_t sptc_smem_for(int R, int stages) {
   return sizeof(float) * (size_t)stages * kM * sptc_boxw(R)                       // TMA stages
-         + 2 * sizeof(uint16_t) * (size_t)sptc_nslot(R) * kM * kTcRingStride  // ring (hi, lo)
-         + (size_t)sptc_nky(R) * 2 * 32 * 16                                   // Ty fragments
+         + kTcPlanes * sizeof(uint16_t) * (size_t)sptc_nslot(R) * kM * kTcRingStride  // ring planes
+         + (size_t)sptc_nky(R) * kTcPlanes * 32 * 16                                   // Ty fragments
          + 2 * 8 + 8 * 8 + 16;
 }
-__host__ __device__ constexpr int sptc_stages(int R) { return spass_fit_n(sptc_smem_for(R, 2)) >= 2 ? 2 : 1; }
+#ifndef SPTC_MIN_CTAS
+#define SPTC_MIN_CTAS 3
+#endif
+// two TMA stages when SPTC_MIN_CTAS CTAs still share an SM, else one
+__host__ __device__ constexpr int sptc_stages(int R) {
+  return spass_fit_n(sptc_smem_for(R, 2)) >= SPTC_MIN_CTAS ? 2 : 1;
+}
 __host__ __device__ constexpr size_t sptc_smem_bytes(int R) { return sptc_smem_for(R, sptc_stages(R)); }
 __host__ __device__ constexpr int sptc_ctas_per_sm(int R) {
   return spass_fit_n(sptc_smem_bytes(R)) < 3 ? spass_fit_n(sptc_smem_bytes(R)) : 3;
@@ -102,9 +120,11 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
 
   extern __shared__ __align__(128) unsigned char smem[];
   float* stage = reinterpret_cast<float*>(smem);                          // [NST][32][BOXW]
-  uint32_t* ring = reinterpret_cast<uint32_t*>(stage + NST * kM * BOXW);  // [2 planes][NSLOT*32][RSW]
-  uint4* tyf = reinterpret_cast<uint4*>(ring + 2 * PLANE);                 // [NKY][2][32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tyf + NKY * 2 * 32);
+  constexpr int PL = kTcPlanes;
+  constexpr int NPR = sptc_nprod();
+  uint32_t* ring = reinterpret_cast<uint32_t*>(stage + NST * kM * BOXW);  // [PL planes][NSLOT*32][RSW]
+  uint4* tyf = reinterpret_cast<uint4*>(ring + PL * PLANE);                // [NKY][PL][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tyf + NKY * PL * 32);
   double* red = reinterpret_cast<double*>(bars + 2);
   int* flag = reinterpret_cast<int*>(red + 8);
 
@@ -126,22 +146,22 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
   }
   __syncthreads();
   // Ty fragments (A operand of the y-pass): A[i][kk] = w(16 s + kk - i - R)
-  for (int idx = tid; idx < NKY * 2 * 32; idx += kSpassThreads) {
-    const int s = idx / 64, pl = (idx >> 5) & 1, l = idx & 31;
+  for (int idx = tid; idx < NKY * PL * 32; idx += kSpassThreads) {
+    const int s = idx / (32 * PL), pl = (idx >> 5) % PL, l = idx & 31;
     const int gi = l >> 2, ti = l & 3;
     uint32_t v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int i = gi + 8 * (j & 1);
       const int kk = 16 * s + 2 * ti + 8 * (j >> 1);
-      uint32_t hi, lo;
-      split_bf16x2(sptc_w(gsm, kk - i - R, R), sptc_w(gsm, kk + 1 - i - R, R), hi, lo);
-      v[j] = pl ? lo : hi;
+      uint32_t pp[PL];
+      split_planes<PL>(sptc_w(gsm, kk - i - R, R), sptc_w(gsm, kk + 1 - i - R, R), pp);
+      v[j] = pp[pl];
     }
     tyf[idx] = make_uint4(v[0], v[1], v[2], v[3]);
   }
   // Tx fragments (B operand of the x-pass), registers: B[kk][jj] = w(16 s + kk - jj - 8 par - RA)
-  uint32_t bxh[2][NKX][2], bxl[2][NKX][2];
+  uint32_t bx[PL][2][NKX][2];
 #pragma unroll
   for (int par = 0; par < 2; ++par)
 #pragma unroll
@@ -149,7 +169,10 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int d = 16 * s + 2 * t + 8 * j - g - 8 * par - RA;
-        split_bf16x2(sptc_w(gsm, d, R), sptc_w(gsm, d + 1, R), bxh[par][s][j], bxl[par][s][j]);
+        uint32_t pp[PL];
+        split_planes<PL>(sptc_w(gsm, d, R), sptc_w(gsm, d + 1, R), pp);
+#pragma unroll
+        for (int q = 0; q < PL; ++q) bx[q][par][s][j] = pp[q];
       }
   __syncthreads();
 
@@ -253,11 +276,15 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
       }
     };
     auto ypass = [&](int m, const Pre& pr) {
-      float acc[4][4];
+      // acc: the leading product (plane 1 x plane 1) only; acs: the five correction products.
+      // The tensor core truncates each accumulation to the accumulator's magnitude, so the
+      // corrections (<= 2^-8 of the result) are summed in their own accumulator and added
+      // with one round-to-nearest FADD: 4 instead of 24 full-magnitude truncations per pass.
+      float acc[4][4], acs[4][4];
 #pragma unroll
       for (int nl = 0; nl < 4; ++nl)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[nl][i] = 0.f;
+        for (int i = 0; i < 4; ++i) acc[nl][i] = acs[nl][i] = 0.f;
       // ring slot of each x-block of this y window (x-blocks m .. m + PRO)
       uint32_t slot_addr[PRO + 1];
       {
@@ -270,26 +297,35 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
       }
 #pragma unroll
       for (int s = 0; s < NKY; ++s) {
-        const uint4 ah = tyf[(2 * s) * 32 + lane];
-        const uint4 al = tyf[(2 * s + 1) * 32 + lane];
+        uint4 ay[PL];
+#pragma unroll
+        for (int q = 0; q < PL; ++q) ay[q] = tyf[(PL * s + q) * 32 + lane];
         // window rows 16 mt + 16 s ..: x-block (16 mt + 16 s) >> 5 of the window, mt runtime
         const uint32_t sa = (mt ? slot_addr[(16 + 16 * s) >> 5] + 4u * (uint32_t)(((16 + 16 * s) & 31) * RSW)
                                 : slot_addr[(16 * s) >> 5] + 4u * (uint32_t)(((16 * s) & 31) * RSW));
-        uint32_t bh[8], bl[8];  // B fragments of the four n tiles (2 regs each), hi and lo planes
+        uint32_t bq[PL][8];  // B fragments of the four n tiles (2 regs each), per ring plane
 #pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          const uint32_t addr = sa + 4u * (uint32_t)(8 * pp);
-          ldsm_x4_trans(addr, bh[4 * pp], bh[4 * pp + 1], bh[4 * pp + 2], bh[4 * pp + 3]);
-          ldsm_x4_trans(addr + 4u * PLANE, bl[4 * pp], bl[4 * pp + 1], bl[4 * pp + 2], bl[4 * pp + 3]);
-        }
-        // product-major order: consecutive HMMAs write different accumulators
+        for (int q = 0; q < PL; ++q)
 #pragma unroll
-        for (int nl = 0; nl < 4; ++nl) mma16816(acc[nl], ah.x, ah.y, ah.z, ah.w, bh[2 * nl], bh[2 * nl + 1]);
+          for (int pp = 0; pp < 2; ++pp) {
+            const uint32_t addr = sa + 4u * (uint32_t)(8 * pp + q * PLANE);
+            ldsm_x4_trans(addr, bq[q][4 * pp], bq[q][4 * pp + 1], bq[q][4 * pp + 2], bq[q][4 * pp + 3]);
+          }
+        // product-major order: consecutive HMMAs write different accumulators.  Here the
+        // taps are the A operand: product (i, j) = data plane i (B) x tap plane j (A).
 #pragma unroll
-        for (int nl = 0; nl < 4; ++nl) mma16816(acc[nl], ah.x, ah.y, ah.z, ah.w, bl[2 * nl], bl[2 * nl + 1]);
+        for (int p = 0; p < NPR; ++p)
 #pragma unroll
-        for (int nl = 0; nl < 4; ++nl) mma16816(acc[nl], al.x, al.y, al.z, al.w, bh[2 * nl], bh[2 * nl + 1]);
+          for (int nl = 0; nl < 4; ++nl) {
+            const uint4& a = ay[sptc_pb(p)];
+            mma16816(p == 0 ? acc[nl] : acs[nl], a.x, a.y, a.z, a.w, bq[sptc_pa(p)][2 * nl],
+                     bq[sptc_pa(p)][2 * nl + 1]);
+          }
       }
+#pragma unroll
+      for (int nl = 0; nl < 4; ++nl)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[nl][i] += acs[nl][i];
       // epilogue
       float s0 = 0.f, s1 = 0.f;
       const int yb = (sg.yb0 + m) * kM + 16 * mt + g;
@@ -329,11 +365,11 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
       const bool live = (row0 + kM > 0) && (row0 < H);
       const int slot_row = (n % NSLOT) * kM + 16 * mt + g;
       if (wlive) {
-        float acc[4][4];
+        float acc[4][4], acs[4][4];  // leading product / corrections (see the y-pass)
 #pragma unroll
         for (int nl = 0; nl < 4; ++nl)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[nl][i] = 0.f;
+          for (int i = 0; i < 4; ++i) acc[nl][i] = acs[nl][i] = 0.f;
         if (live) {
           const int st = (NST == 2) ? (cseq & 1) : 0;
           mbar_wait(&bars[st], (NST == 2) ? ((cseq >> 1) & 1) : (cseq & 1));
@@ -348,24 +384,24 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
             const float2 v10 = *reinterpret_cast<const float2*>(p0 + 8 * BOXW);
             const float2 v01 = *reinterpret_cast<const float2*>(p0 + 8);
             const float2 v11 = *reinterpret_cast<const float2*>(p0 + 8 * BOXW + 8);
-            uint32_t ah[4], al[4];
-            split_bf16x2(v00.x, v00.y, ah[0], al[0]);
-            split_bf16x2(v10.x, v10.y, ah[1], al[1]);
-            split_bf16x2(v01.x, v01.y, ah[2], al[2]);
-            split_bf16x2(v11.x, v11.y, ah[3], al[3]);
+            uint32_t a0[PL], a1[PL], a2[PL], a3[PL];
+            split_planes<PL>(v00.x, v00.y, a0);
+            split_planes<PL>(v10.x, v10.y, a1);
+            split_planes<PL>(v01.x, v01.y, a2);
+            split_planes<PL>(v11.x, v11.y, a3);
             // product-major order: consecutive HMMAs write different accumulators
 #pragma unroll
-            for (int pr3 = 0; pr3 < 3; ++pr3)
+            for (int p = 0; p < NPR; ++p)
 #pragma unroll
               for (int qq = 0; qq < 2; ++qq) {
                 const int s = j - qq;
                 if (s < 0 || s >= NKX) continue;
 #pragma unroll
                 for (int par = 0; par < 2; ++par) {
-                  float(&d)[4] = acc[2 * qq + par];
-                  const uint32_t* a = pr3 == 1 ? al : ah;
-                  const uint32_t* bb = pr3 == 2 ? bxl[par][s] : bxh[par][s];
-                  mma16816(d, a[0], a[1], a[2], a[3], bb[0], bb[1]);
+                  float(&d)[4] = p == 0 ? acc[2 * qq + par] : acs[2 * qq + par];
+                  const int qa = sptc_pa(p);
+                  const uint32_t* bb = bx[sptc_pb(p)][par][s];
+                  mma16816(d, a0[qa], a1[qa], a2[qa], a3[qa], bb[0], bb[1]);
                 }
               }
           }
@@ -373,14 +409,17 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
         // x-pass output (or the zero padding of a block outside rows [0, H)) -> ring planes
 #pragma unroll
         for (int nl = 0; nl < 4; ++nl) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[nl][i] += acs[nl][i];
           const int w0 = slot_row * RSW + 4 * (4 * hh + nl) + t;
-          uint32_t hi, lo;
-          split_bf16x2(acc[nl][0], acc[nl][1], hi, lo);
-          ring[w0] = hi;
-          ring[PLANE + w0] = lo;
-          split_bf16x2(acc[nl][2], acc[nl][3], hi, lo);
-          ring[w0 + 8 * RSW] = hi;
-          ring[PLANE + w0 + 8 * RSW] = lo;
+          uint32_t q0[PL], q1[PL];
+          split_planes<PL>(acc[nl][0], acc[nl][1], q0);
+          split_planes<PL>(acc[nl][2], acc[nl][3], q1);
+#pragma unroll
+          for (int q = 0; q < PL; ++q) {
+            ring[q * PLANE + w0] = q0[q];
+            ring[q * PLANE + w0 + 8 * RSW] = q1[q];
+          }
         }
       }
       __syncthreads();  // stage consumed; ring slot visible

@@ -13,7 +13,7 @@ from typing import Optional, Tuple
 
 import torch
 
-from . import (DistC, Gauss, Shape, _alloc_bytes, _check, _ptr, _require, _stream, _weights, lib,
+from . import (DistC, Gauss, Shape, _alloc_ws, _check, _ptr, _require, _stream, _weights, lib,
                ACT_IDENTITY)
 
 
@@ -65,19 +65,21 @@ class SlabSolver:
         self.comm, self.shape = comm, tuple(int(v) for v in local_shape)
         self.C, self.gauss, self.K = int(C_), gauss, int(K)
         self.dist = DistC(comm.handle, int(T_global), int(t_offset))
-        ws, _ = C.c_size_t(0), None
         n = C.c_size_t(0)
         _check(lib().sfseg_workspace_bytes(Shape(*self.shape), self.C, gauss.c(), self.K, 0, C.byref(self.dist),
                                            C.byref(n), None), "sfseg_workspace_bytes(dist)")
         self.ws_bytes = n.value
-        self.ws = _alloc_bytes(n.value, device)
+        self.ws = _alloc_ws(n.value, device)
+        self.device = self.ws.device
         self.stats = torch.zeros((self.shape[0], self.K, 3), dtype=torch.float64, device=device)
 
     def forward(self, ch: torch.Tensor, w, b: float = 0.0, act: int = ACT_IDENTITY,
                 x_out: Optional[torch.Tensor] = None, check: bool = True, stream=None) -> torch.Tensor:
-        _require(ch, "ch", 5)
+        B, T, H, W = self.shape
+        _require(ch, "ch", 5, shape=(B, self.C, T, H, W), device=self.device)
         if x_out is None:
-            x_out = torch.empty(self.shape, dtype=torch.float32, device=ch.device)
+            x_out = torch.empty(self.shape, dtype=torch.float32, device=self.device)
+        _require(x_out, "x_out", 4, shape=self.shape, device=self.device)
         _check(lib().sfseg_power_iterate(
             _ptr(ch), self.C, _weights(w, self.C), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
             None, _ptr(x_out), None, _ptr(self.stats), 0, None, _ptr(self.ws), self.ws_bytes,

@@ -100,29 +100,53 @@ def test_full_and_online_workspace_validation(lib):
     assert lib.sfseg_workspace_bytes_online(shp, 1, g.c(), 5, 0, C.byref(n)) == 1  # q < 1
     # the full operator needs 7 pitched volumes (U, F, a, v, ua, ub, uc)
     assert full >= 7 * 10 * 32 * 40 * 4
-    assert lib.sfseg_set_algorithm(7) == 1
-    assert lib.sfseg_set_algorithm(0) == 0
+
+
+def test_no_process_global_switch(lib):
+    """The path choice is a per-call option: no setter exists, and an invalid algo in the
+    options is rejected at validation (before any device work)."""
+    assert not hasattr(lib, "sfseg_set_algorithm") or "sfseg_set_algorithm" not in _declared_functions()
+    src = open(HEADER).read()
+    assert "sfseg_set_algorithm" not in src and "sfseg_profile_enable" not in src
+    info = (C.c_int32 * 3)()
+    assert lib.sfseg_forward_path(sf.Shape(1, 4, 8, 8), sf.Gauss(1.0, 2.0).c(), 7, info) == 1
+    shp = sf.Shape(1, 2, 3, 4)
+    w = (C.c_float * 1)(1.0)
+    bad = sf.OptionsC(7, None)
+    assert lib.sfseg_power_iterate_ex(None, 1, w, 0.0, 0, shp, sf.Gauss(1.0, 1.0).c(), 2, None, None, None, None,
+                                      0, None, None, 0, None, C.byref(bad), None) == 1
+
+
+def test_adamw_step_validation(lib):
+    hp = sf.AdamwC(0.1, 0.9, 0.999, 1e-8, 0.0, 1)
+    assert lib.sfseg_adamw_step(None, None, None, 3, 1, C.byref(hp), None) == 1
+    bad = sf.AdamwC(0.1, 1.5, 0.999, 1e-8, 0.0, 1)   # beta1 >= 1
+    p = C.c_void_p(16)
+    assert lib.sfseg_adamw_step(p, p, p, 3, 1, C.byref(bad), None) == 1
+    assert lib.sfseg_adamw_step(p, p, p, 3, 0, C.byref(hp), None) == 1   # step numbers start at 1
+
+
+def test_online_stride_longer_than_window_rejected(lib):
+    """A stride > q would leave frames of x_out unwritten: rejected before any launch."""
+    shp = sf.Shape(1, 20, 8, 8)
+    w = (C.c_float * 1)(1.0)
+    p = C.c_void_p(256)
+    assert lib.sfseg_power_iterate_online(p, 1, w, 0.0, 0, shp, sf.Gauss(1.0, 1.0).c(), 3, 5, 6, p, p,
+                                          1 << 30, None) == 1
 
 
 def test_forward_path_selection(lib):
-    """Host-side plan introspection: which forward kernels a problem runs on."""
+    """Host-side plan introspection: which forward kernels a problem runs on, per algo."""
     import paper_2212_08058_b200 as m
     shp = (1, 70, 480, 854)
-    try:
-        m.set_algorithm(m.ALGO_AUTO)
-        assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24)) == (m.PATH_TWO_PASS_TC, 6, 24)
-        assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3)) == (m.PATH_FUSED_3D, 1, 3)
-        # spatial radii below the tensor-core kernel's smallest compiled radius: FP32 pass
-        assert m.forward_path(shp, m.Gauss(2.0, 2.0, 6, 6))[0] == m.PATH_TWO_PASS_FP32
-        # requested radii round up to compiled ones (extra taps are zero)
-        assert m.forward_path(shp, m.Gauss(1.5, 6.0, 5, 17))[1:] == (5, 18)
-        m.set_algorithm(m.ALGO_TWO_PASS)
-        assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3))[0] == m.PATH_TWO_PASS_FP32
-        m.set_algorithm(m.ALGO_TWO_PASS_FP32)
-        assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24))[0] == m.PATH_TWO_PASS_FP32
-        m.set_algorithm(m.ALGO_MEGAKERNEL)
-        assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24))[0] == m.PATH_MEGAKERNEL
-    finally:
-        m.set_algorithm(m.ALGO_AUTO)
+    assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24)) == (m.PATH_TWO_PASS_TC, 6, 24)
+    assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3)) == (m.PATH_FUSED_3D, 1, 3)
+    # spatial radii below the tensor-core kernel's smallest compiled radius: FP32 pass
+    assert m.forward_path(shp, m.Gauss(2.0, 2.0, 6, 6))[0] == m.PATH_TWO_PASS_FP32
+    # requested radii round up to compiled ones (extra taps are zero)
+    assert m.forward_path(shp, m.Gauss(1.5, 6.0, 5, 17))[1:] == (5, 18)
+    assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3), m.ALGO_TWO_PASS)[0] == m.PATH_TWO_PASS_FP32
+    assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS)[0] == m.PATH_TWO_PASS_TC
+    assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_FP32)[0] == m.PATH_TWO_PASS_FP32
     with pytest.raises(m.SfsegError):
         m.forward_path((0, 1, 1, 1), m.Gauss(1.0, 1.0))

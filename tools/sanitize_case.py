@@ -35,12 +35,8 @@ s = sf.Solver((B, TT, H, W), C, g, 4, want_tape=True)
 x = s.forward(T(wl.ch), wl.w, want_rayleigh=True)
 dw, db = s.backward(T(wl.ch), wl.w, T(rng.normal(size=x.shape).astype(np.float32)))
 # two-pass forced on small radii
-sf.set_algorithm(sf.ALGO_TWO_PASS)
-sf.Solver((2, 5, 33, 90), 1, sf.Gauss(1.0, 1.0, 3, 3), 3).forward(T(rng.random((2, 1, 5, 33, 90)).astype(np.float32)), [1.0])
-# megakernel
-sf.set_algorithm(sf.ALGO_MEGAKERNEL)
-sf.Solver((1, 20, 60, 140), 1, g, 4).forward(T(rng.random((1, 1, 20, 60, 140)).astype(np.float32)), [1.0])
-sf.set_algorithm(sf.ALGO_AUTO)
+sf.Solver((2, 5, 33, 90), 1, sf.Gauss(1.0, 1.0, 3, 3), 3, algo=sf.ALGO_TWO_PASS).forward(
+    T(rng.random((2, 1, 5, 33, 90)).astype(np.float32)), [1.0])
 # full operator
 fs = sf.FullSolver((1, 6, 40, 100), 1, 2, g, 3)
 fs.forward(T(rng.random((1, 1, 6, 40, 100)).astype(np.float32)), [1.0],
