@@ -106,14 +106,28 @@ const char* sfseg_last_cuda_error(void);
  *     fp32 accumulation: fp32-class arithmetic.
  *   SFSEG_ALGO_TWO_PASS_FP32: the two-pass iteration with the FP32-FMA spatial pass.
  * profiler: NULL, or a sfseg_profiler that records CUDA events around every pass launch
- * (benchmark instrumentation). */
+ * (benchmark instrumentation).
+ * binarize: NULL, or the soft-binarisation of Alg.1 STEP 3 (SURVEY §8(f) row f2,
+ * reading A21): after the normalisation of every iteration k > n_cont,
+ *   x_k <- sigma(kappa_k (x_k - theta_k)),  theta_k = mean of the positive entries of x_k,
+ *   kappa_k = kappa0 * growth^(k - n_cont - 1),
+ * and the binarised x_k is the next iterate as is (not renormalised).  When K > n_cont the
+ * output x_out is the last binarised iterate (values in (0,1), not unit norm).  With a tape,
+ * sfseg_power_iterate_backward_ex (same options) differentiates through it ("trainable by
+ * using a soft-binarization between iterations").  Forces the two-pass iteration. */
 #define SFSEG_ALGO_AUTO 0
 #define SFSEG_ALGO_TWO_PASS 1
 #define SFSEG_ALGO_TWO_PASS_FP32 3
 typedef struct sfseg_profiler sfseg_profiler;
 typedef struct {
+  int32_t n_cont;   /* continuous iterations before binarisation starts (>= 0) */
+  float kappa0;     /* steepness of the first binarised iteration (> 0) */
+  float growth;     /* geometric growth of the steepness per iteration (> 0) */
+} sfseg_binarize;
+typedef struct {
   int32_t algo;
   sfseg_profiler* profiler;
+  const sfseg_binarize* binarize;
 } sfseg_options;
 
 /* Per-kernel timing object (owned by the caller).  sfseg_profiler_read syncs the
@@ -218,11 +232,6 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
  *     K > n_cont x_out is the last binarised iterate (values in (0,1), not unit norm; hard
  *     mask: sfseg_threshold with SFSEG_THR_ABSOLUTE, tau = 0.5).  NULL: no binarisation.
  *   ws: >= sfseg_workspace_bytes_full(...), 256-byte aligned.  Asynchronous. */
-typedef struct {
-  int32_t n_cont;   /* continuous iterations before binarisation starts (>= 0) */
-  float kappa0;     /* steepness of the first binarised iteration (> 0) */
-  float growth;     /* geometric growth of the steepness per iteration (> 0) */
-} sfseg_binarize;
 sfseg_status sfseg_workspace_bytes_full(sfseg_shape shape, int32_t Cs, int32_t Cf, sfseg_gauss gauss,
                                         int32_t K, size_t* ws_bytes_host);
 sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float* ws_host, float bs,
@@ -327,6 +336,18 @@ sfseg_status sfseg_slabs_sync_status(sfseg_shape shape, int32_t C, sfseg_gauss g
 typedef struct { double lr, beta1, beta2, eps, weight_decay; int32_t amsgrad; } sfseg_adamw;
 sfseg_status sfseg_adamw_step(double* w, const double* grad, double* state, int32_t n, int64_t t,
                               const sfseg_adamw* hp, void* stream);
+
+/* Focal-Dice loss of Eq.12 (reading A24) and its gradient, on the device:
+ * per training frame i = (volume, frame) the soft Dice overlap
+ *   D_i = 2 sum(x t) / (sum(x) + sum(t))
+ * of the prediction x (e.g. the soft-binarised output of sfseg_power_iterate_ex) and the binary
+ * ground truth t (mask: uint8 0/1), J = sum_i (1 - D_i)^gamma (gamma = 0.75 in the paper),
+ * dL_dx = dJ/dx.  x, dL_dx [B][T][H][W] fp32, mask [B][T][H][W] uint8; loss: ONE DEVICE double.
+ * A frame with sum(x) + sum(t) == 0 contributes 0.  Sums in fp64, fixed order (deterministic).
+ * ws: >= sfseg_focal_dice_ws_bytes(shape), 256-byte aligned.  Asynchronous. */
+size_t sfseg_focal_dice_ws_bytes(sfseg_shape shape);
+sfseg_status sfseg_focal_dice(const float* x, const uint8_t* mask, sfseg_shape shape, double gamma,
+                              double* loss, float* dL_dx, void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -56,8 +56,12 @@ class DistC(C.Structure):
     _fields_ = [("comm", C.c_void_p), ("T_global", C.c_int64), ("t_offset", C.c_int64)]
 
 
+class BinarizeC(C.Structure):
+    _fields_ = [("n_cont", C.c_int32), ("kappa0", C.c_float), ("growth", C.c_float)]
+
+
 class OptionsC(C.Structure):
-    _fields_ = [("algo", C.c_int32), ("profiler", C.c_void_p)]
+    _fields_ = [("algo", C.c_int32), ("profiler", C.c_void_p), ("binarize", C.c_void_p)]
 
 
 class AdamwC(C.Structure):
@@ -99,6 +103,8 @@ _SIGS = {
     "sfseg_profiler_destroy": (C.c_int, [_P]),
     "sfseg_profiler_read": (C.c_int, [_P, _P, _P]),
     "sfseg_adamw_step": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
+    "sfseg_focal_dice_ws_bytes": (C.c_size_t, [Shape]),
+    "sfseg_focal_dice": (C.c_int, [_P, _P, Shape, C.c_double, _P, _P, _P, C.c_size_t, _P]),
     "sfseg_threshold_ws_bytes": (C.c_size_t, [Shape]),
     "sfseg_threshold": (C.c_int, [_P, Shape, C.c_float, C.c_int32, _P, _P, C.c_size_t, _P]),
     "sfseg_sync_status": (C.c_int, [_P, _P]),
@@ -218,8 +224,14 @@ PATH_TWO_PASS_TC = 1
 PATH_FUSED_3D = 2
 
 
-def _options(algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None) -> OptionsC:
-    return OptionsC(int(algo), profiler.handle if profiler is not None else None)
+def _options(algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None, binarize=None) -> OptionsC:
+    """sfseg_options; binarize = (n_cont, kappa0, growth) or None (the BinarizeC is kept alive
+    on the returned object for the duration of the call)."""
+    o = OptionsC(int(algo), profiler.handle if profiler is not None else None, None)
+    if binarize is not None:
+        o._bz = BinarizeC(int(binarize[0]), float(binarize[1]), float(binarize[2]))
+        o.binarize = C.cast(C.pointer(o._bz), C.c_void_p)
+    return o
 
 
 def forward_path(shape, gauss, algo: int = ALGO_AUTO) -> tuple:
@@ -270,7 +282,7 @@ class Solver:
     """
 
     def __init__(self, shape, C_: int, gauss: Gauss, K: int, device="cuda", want_tape: bool = False,
-                 algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None):
+                 algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None, binarize=None):
         self.shape = tuple(int(v) for v in shape)
         self.C, self.gauss, self.K = int(C_), gauss, int(K)
         self.device = torch.device(device)
@@ -278,6 +290,7 @@ class Solver:
             self.device = torch.device("cuda", torch.cuda.current_device())
         self.want_tape = bool(want_tape)
         self.algo, self.profiler = int(algo), profiler
+        self.binarize = None if binarize is None else (int(binarize[0]), float(binarize[1]), float(binarize[2]))
         ws, tape = workspace_bytes(self.shape, self.C, gauss, self.K, want_tape)
         thr = lib().sfseg_threshold_ws_bytes(Shape(*self.shape))
         self.ws_bytes = ws
@@ -287,7 +300,8 @@ class Solver:
         self.stats = torch.zeros((self.shape[0], self.K, 3), dtype=torch.float64, device=self.device)
 
     def _opt(self):
-        return C.byref(_options(self.algo, self.profiler))
+        self._o = _options(self.algo, self.profiler, self.binarize)
+        return C.byref(self._o)
 
     def forward(self, ch: torch.Tensor, w, b: float = 0.0, act: int = ACT_IDENTITY, x0=None,
                 x_out: Optional[torch.Tensor] = None, want_rayleigh: bool = False, F_out=None,
@@ -476,10 +490,6 @@ class HostStream:
         self.solver.sync(s_cmp)
 
 
-class BinarizeC(C.Structure):
-    _fields_ = [("n_cont", C.c_int32), ("kappa0", C.c_float), ("growth", C.c_float)]
-
-
 class FullSolver:
     """The full SFSeg / SFSeg++ operator (Eq.7 / Eq.10 with
     unary exponent p, pairwise map F and alpha) through sfseg_power_iterate_full."""
@@ -565,29 +575,62 @@ class AdamWState:
                                       C.byref(self.hp), _stream(stream)), "sfseg_adamw_step")
 
 
+class FocalDice:
+    """Eq.12 Focal-Dice loss and dJ/dx on the device (sfseg_focal_dice) for one shape."""
+
+    def __init__(self, shape, gamma: float = 0.75, device="cuda"):
+        self.shape = tuple(int(v) for v in shape)
+        self.gamma = float(gamma)
+        self.device = torch.device(device)
+        n = lib().sfseg_focal_dice_ws_bytes(Shape(*self.shape))
+        self.ws_bytes = n
+        self.ws = _alloc_bytes(n, self.device)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+
+    def __call__(self, x: torch.Tensor, mask: torch.Tensor, grad: Optional[torch.Tensor] = None, stream=None):
+        """Returns (loss: 1-element float64 device tensor, dJ/dx)."""
+        _require(x, "x", 4, shape=self.shape, device=x.device)
+        _require(mask, "mask", 4, dtype=torch.uint8, shape=self.shape, device=x.device)
+        if grad is None:
+            grad = torch.empty(self.shape, dtype=torch.float32, device=x.device)
+        _require(grad, "grad", 4, shape=self.shape, device=x.device)
+        _check(lib().sfseg_focal_dice(_ptr(x), _ptr(mask), Shape(*self.shape), self.gamma, _ptr(self.loss),
+                                      _ptr(grad), _ptr(self.ws), self.ws_bytes, _stream(stream)), "sfseg_focal_dice")
+        return self.loss, grad
+
+
 def train_weights(ch: torch.Tensor, mask: torch.Tensor, w0, b0: float, act: int, gauss: Gauss, K: int, steps: int,
-                  lr: float, weight_decay: float = 0.0):
+                  lr: float, weight_decay: float = 0.0, loss: str = "mse", binarize=None, gamma: float = 0.75):
     """Learn the Eq.9 weights end to end: each step runs
-    sfseg_power_iterate with a tape, the MSE loss of reading A13 against the
-    unit-normalised mask (harness-side elementwise gradient), then
-    sfseg_power_iterate_backward for dL/dw, dL/db, and sfseg_adamw_step.
-    Returns (w, b, losses)."""
+    sfseg_power_iterate_ex with a tape (and, with ``binarize``, the soft-binarised
+    iterations of Alg.1 STEP 3), the loss -- "focal_dice": Eq.12 on the device
+    (sfseg_focal_dice); "mse": reading A13 against the unit-normalised mask (harness-side
+    elementwise gradient) -- then sfseg_power_iterate_backward_ex for dL/dw, dL/db and
+    sfseg_adamw_step.  Returns (w, b, losses)."""
     _require(ch, "ch", 5)
     B, Cn, T, H, W = ch.shape
-    solver = Solver((B, T, H, W), Cn, gauss, K, device=ch.device, want_tape=True)
-    m = mask.to(torch.float32)
-    mn = torch.linalg.vector_norm(m.reshape(B, -1).double(), dim=1).float().clamp_min(1e-30)
-    mh = m / mn.view(B, 1, 1, 1)
+    solver = Solver((B, T, H, W), Cn, gauss, K, device=ch.device, want_tape=True, binarize=binarize)
+    if loss == "focal_dice":
+        fd = FocalDice((B, T, H, W), gamma, device=ch.device)
+        m8 = mask.to(torch.uint8).contiguous()
+    else:
+        m = mask.to(torch.float32)
+        mn = torch.linalg.vector_norm(m.reshape(B, -1).double(), dim=1).float().clamp_min(1e-30)
+        mh = m / mn.view(B, 1, 1, 1)
     opt = AdamWState(list(w0) + [float(b0)], lr, weight_decay=weight_decay, device=ch.device)
     losses = []
     for _ in range(steps):
         p = opt.w.cpu().tolist()
         w, b = [float(v) for v in p[:-1]], float(p[-1])
         x = solver.forward(ch, w, b, act)
-        d = x - mh
-        losses.append(float((d.double() ** 2).mean()))
-        g = (2.0 / x.numel()) * d
-        dw, db = solver.backward(ch, w, g.contiguous(), b, act)
+        if loss == "focal_dice":
+            Lt, g = fd(x, m8)
+            losses.append(float(Lt.item()))
+        else:
+            d = x - mh
+            losses.append(float((d.double() ** 2).mean()))
+            g = ((2.0 / x.numel()) * d).contiguous()
+        dw, db = solver.backward(ch, w, g, b, act)
         opt.step(torch.tensor(list(dw) + [db], dtype=torch.float64, device=ch.device))
     p = opt.w.cpu().tolist()
     return p[:-1], float(p[-1]), losses

@@ -33,6 +33,7 @@ enum ScalSlot : int {
   SC_INV_NU_PREV = 4,  // backward: 1 / nu_{k-1}
   SC_NU = 5,           // last nu
   SC_THETA = 6,        // soft-binarisation: mean of the positive entries of y_k (y units)
+  SC_CORR = 7,         // backward through a binarised iteration: sum(g) / n_pos (the centre's adjoint)
 };
 
 enum ErrBits : unsigned { ERR_DEGENERATE = 1u, ERR_NONFINITE = 2u };

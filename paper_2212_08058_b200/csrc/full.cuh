@@ -162,6 +162,8 @@ struct BinParams {
   unsigned* err;
   int B, T, H, W, Wp, gx;
   float kappa;
+  double* tape_bin;     // hot-path tape [B][K][2] (theta_k in x units, n_pos) or null
+  int K, k;             // iteration recorded in tape_bin
 };
 
 __global__ void __launch_bounds__(kEwThreads) pos_stats_kernel(const __grid_constant__ BinParams P) {
@@ -190,7 +192,14 @@ __global__ void __launch_bounds__(kEwThreads) pos_stats_kernel(const __grid_cons
   for (int v = 0; v < P.B; ++v) {
     const double tot = block_sum_array<kEwThreads>(P.partials + (long)v * nper, nper, 1, red);
     const double cnt = block_sum_array<kEwThreads>(P.partials + (long)(P.B + v) * nper, nper, 1, red);
-    if (threadIdx.x == 0) P.sc[v * kScal + SC_THETA] = cnt > 0.0 ? tot / cnt : 0.0;
+    if (threadIdx.x == 0) {
+      P.sc[v * kScal + SC_THETA] = cnt > 0.0 ? tot / cnt : 0.0;
+      if (P.tape_bin) {
+        double* tb = P.tape_bin + ((long)v * P.K + (P.k - 1)) * 2;
+        tb[0] = cnt > 0.0 ? tot / cnt / P.sc[v * kScal + SC_NU] : 0.0;
+        tb[1] = cnt;
+      }
+    }
   }
   if (threadIdx.x == 0) *P.counter = 0u;
 }

@@ -284,9 +284,14 @@ struct BwdInitParams {
   double* sc;
   double* partials;
   unsigned* counter;
+  const double* tape_bin;  // [B][K][2] of the binarised iterations (row f2)
+  float kappa;             // steepness of iteration K (0: not binarised; then g is dL/dx_K)
   int B, T, H, W, Wp, K, gx;
 };
 
+// x_bar_K = dL/dx_K, c_K = <x_K, x_bar_K>.  When iteration K was soft-binarised the output is
+// b_K = sigma(kappa (x_K - theta)) and g is its adjoint: x_bar holds kappa sigma' g and the
+// finalize forms corr and c_K as in bwd_epi_kernel (bwd.cuh).
 __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_constant__ BwdInitParams P) {
   __shared__ double red[kEwThreads / 32];
   __shared__ int flag;
@@ -294,7 +299,10 @@ __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_const
   const int b = bt / P.T, t = bt - b * P.T;
   const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
   const float* gf = P.g + ((long)b * P.T + t) * HW;
-  double acc = 0.0;
+  const bool bin = P.kappa > 0.f;
+  const float inv_nuK = (float)(1.0 / P.tape_nu[(long)b * P.K + (P.K - 1)]);
+  const float theta = bin ? (float)P.tape_bin[((long)b * P.K + (P.K - 1)) * 2] : 0.f;
+  double acc = 0.0, acc2 = 0.0;
   // row-parallel (see combine_kernel): no per-element index division
   for (int y = blockIdx.x; y < P.H; y += P.gx) {
     for (int c0 = 0; c0 < P.Wp; c0 += kEwThreads * kCols) {
@@ -313,22 +321,44 @@ __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_const
         const int x = c0 + i * kEwThreads + threadIdx.x;
         if (x >= P.Wp) continue;
         const long po = (long)bt * HWp + (long)y * P.Wp + x;
-        acc += (double)gv[i] * (double)fv[i] * (double)uv[i];
-        P.xbar[po] = gv[i];
+        if (bin) {
+          const float xk = fv[i] * uv[i] * inv_nuK;
+          const float sg = 1.f / (1.f + expf(-P.kappa * (xk - theta)));
+          const float gg = (x < P.W) ? P.kappa * sg * (1.f - sg) * gv[i] : 0.f;
+          acc += (double)xk * (double)gg;
+          acc2 += (double)gg;
+          P.xbar[po] = gg;
+        } else {
+          acc += (double)gv[i] * (double)fv[i] * (double)uv[i];
+          P.xbar[po] = gv[i];
+        }
         P.Fbar[po] = 0.f;
       }
     }
   }
   const double s = block_sum<kEwThreads>(acc, red);
+  const double s2 = bin ? block_sum<kEwThreads>(acc2, red) : 0.0;
   const long nper = (long)P.T * P.gx;
-  if (threadIdx.x == 0) P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = s;
+  if (threadIdx.x == 0) {
+    P.partials[(long)b * nper + (long)t * P.gx + blockIdx.x] = s;
+    if (bin) P.partials[(long)(P.B + b) * nper + (long)t * P.gx + blockIdx.x] = s2;
+  }
   if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
   for (int bb = 0; bb < P.B; ++bb) {
     const double tot = block_sum_array<kEwThreads>(P.partials + (long)bb * nper, nper, 1, red);
+    const double sg = bin ? block_sum_array<kEwThreads>(P.partials + (long)(P.B + bb) * nper, nper, 1, red) : 0.0;
     if (threadIdx.x == 0) {
       const double nuK = P.tape_nu[(long)bb * P.K + (P.K - 1)];
-      // c_K = <x_K, x_bar_K> = sum(g F u_{K-1}) / nu_K ; cn = c_K / nu_K
-      P.sc[bb * kScal + SC_CN] = tot / (nuK * nuK);
+      if (bin) {
+        // c_K = <x_K, g - [x_K > 0] corr> = sum(x g) - theta sum(g); cn = c_K / nu_K
+        const double* tb = P.tape_bin + ((long)bb * P.K + (P.K - 1)) * 2;
+        P.sc[bb * kScal + SC_CN] = (tot - tb[0] * sg) / nuK;
+        P.sc[bb * kScal + SC_CORR] = tb[1] > 0.0 ? sg / tb[1] : 0.0;
+      } else {
+        // c_K = <x_K, x_bar_K> = sum(g F u_{K-1}) / nu_K ; cn = c_K / nu_K
+        P.sc[bb * kScal + SC_CN] = tot / (nuK * nuK);
+        P.sc[bb * kScal + SC_CORR] = 0.0;
+      }
       P.sc[bb * kScal + SC_INV_NU] = 1.0 / nuK;
       P.sc[bb * kScal + SC_INV_NU_PREV] = (P.K >= 2) ? 1.0 / P.tape_nu[(long)bb * P.K + (P.K - 2)] : 0.0;
     }

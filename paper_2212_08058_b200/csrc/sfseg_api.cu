@@ -246,10 +246,16 @@ struct Plan {
   int G3;             // f3d grid
   int algo;           // SFSEG_ALGO_* of this call (sfseg_options; no process-global switch)
   Profiler* prof;     // per-launch event timing (nullable)
+  bool bin;           // soft-binarisation (row f2) of iterations k > binv.n_cont
+  sfseg_binarize binv;
   // workspace offsets
   size_t off_sc, off_part, off_out, off_F, off_p, off_v, off_p2, off_xbar, off_Fbar, off_x0p, ws_fwd, ws_bwd;
   size_t n_part;
-  size_t tape_nu_bytes, tape_bytes;
+  size_t tape_nu_bytes, tape_hdr_bytes, tape_bytes;  // tape: nu [B][K], bin stats [B][K][2], K x u
+  float kappa(int k) const {  // steepness of iteration k (1-based); 0 when not binarised
+    if (!bin || k <= binv.n_cont) return 0.f;
+    return (float)(binv.kappa0 * std::pow((double)binv.growth, (double)(k - binv.n_cont - 1)));
+  }
 };
 
 bool valid_algo(int32_t algo) {
@@ -262,6 +268,14 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   if (!valid_algo(algo)) return SFSEG_ERR_INVALID_ARGUMENT;
   P->algo = algo;
   P->prof = opt ? opt->profiler : nullptr;
+  P->bin = opt && opt->binarize;
+  if (P->bin) {
+    const sfseg_binarize& bz = *opt->binarize;
+    if (bz.n_cont < 0 || !(bz.kappa0 > 0.f) || !std::isfinite(bz.kappa0) || !(bz.growth > 0.f) ||
+        !std::isfinite(bz.growth))
+      return SFSEG_ERR_INVALID_ARGUMENT;
+    P->binv = bz;
+  }
   if (C < 1 || C > kMaxC) return C < 1 ? SFSEG_ERR_INVALID_ARGUMENT : SFSEG_ERR_UNSUPPORTED;
   if (K < 1) return SFSEG_ERR_INVALID_ARGUMENT;
   if (!(g.sigma_t > 0.0) || !(g.sigma_s > 0.0) || !std::isfinite(g.sigma_t) || !std::isfinite(g.sigma_s))
@@ -292,7 +306,7 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->gx = ew_gx(P->H, P->BT);
   P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
   P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * spass_tc_occupancy(P->RS), P->U / 4));
-  P->f3d = algo == SFSEG_ALGO_AUTO && f3d_supported(P->RT, P->RS);
+  P->f3d = algo == SFSEG_ALGO_AUTO && !P->bin && f3d_supported(P->RT, P->RS);
   P->TX = (int)((sh.W + kF3dTW - 1) / kF3dTW);
   P->TY = (int)((sh.H + f3d_th(std::min(P->RS, kF3dMaxR)) - 1) / f3d_th(std::min(P->RS, kF3dMaxR)));
   P->U3 = P->B * P->TY * P->TX * P->T;
@@ -330,7 +344,8 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   off += vb;
   P->ws_bwd = off;
   P->tape_nu_bytes = align_up(sizeof(double) * P->B * K);
-  P->tape_bytes = P->tape_nu_bytes + (size_t)K * vb;
+  P->tape_hdr_bytes = P->tape_nu_bytes + align_up(sizeof(double) * 2 * P->B * K);
+  P->tape_bytes = P->tape_hdr_bytes + (size_t)K * vb;
   return SFSEG_OK;
 }
 
@@ -802,7 +817,7 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
   float* v = at<float>(ws, P.off_v);
   double* tape_nu = tape ? static_cast<double*>(tape) : nullptr;
   auto tape_u = [&](int i) -> float* {
-    return reinterpret_cast<float*>(static_cast<char*>(tape) + P.tape_nu_bytes +
+    return reinterpret_cast<float*>(static_cast<char*>(tape) + P.tape_hdr_bytes +
                                     (size_t)i * align_up(sizeof(float) * (size_t)P.vol_elems));
   };
 
@@ -884,17 +899,48 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
       SF_CUDA(after_launch("tpass_fwd", st));
     }
     // (a4)-(a7) u = G_y G_x v ; y_k = F u ; p_k = F y_k ; ||y_k||, <p_{k-1}, u>
+    const float kap = P.kappa(k);
     sp.out = p;
     sp.pprev = want_rayleigh ? p : nullptr;
     sp.tape_u = tape ? tape_u(k - 1) : nullptr;
     sp.k = k;
-    sp.last = (k == K) ? 1 : 0;
+    sp.last = (k == K || kap > 0.f) ? 1 : 0;   // a binarised iteration stores y_k itself
     {
       ProfScope ps(P.prof, st, PC_SPASS);
       SF_CUDA(launch_spass_forward(P, sp, st));
       SF_CUDA(after_launch("spass_fwd", st));
     }
+    if (kap > 0.f) {
+      // Alg.1 STEP 3 (row f2): theta_k, then x_k = sigma(kappa (y_k / nu_k - theta_k)) and the
+      // next stored iterate p_k = F x_k (scale 1); the output itself after the last iteration
+      BinParams bp;
+      std::memset(&bp, 0, sizeof(bp));
+      bp.y = p;
+      bp.U = F;
+      bp.a = (k == K) ? nullptr : p;
+      bp.x_dense = (k == K) ? x_out : nullptr;
+      bp.sc = at<double>(ws, P.off_sc);
+      bp.partials = at<double>(ws, P.off_part);
+      bp.counter = &at<WsHeader>(ws, 0)->counter[1];
+      bp.err = &at<WsHeader>(ws, 0)->err;
+      bp.B = (int)P.B;
+      bp.T = (int)P.T;
+      bp.H = (int)P.H;
+      bp.W = (int)P.W;
+      bp.Wp = (int)P.Wp;
+      bp.gx = P.gx;
+      bp.kappa = kap;
+      bp.tape_bin = tape ? reinterpret_cast<double*>(static_cast<char*>(tape) + P.tape_nu_bytes) : nullptr;
+      bp.K = K;
+      bp.k = k;
+      ProfScope ps(P.prof, st, PC_ONCE);
+      pos_stats_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(bp);
+      SF_CUDA(after_launch("pos_stats", st));
+      binarize_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(bp);
+      SF_CUDA(after_launch("binarize", st));
+    }
   }
+  if (P.kappa(K) > 0.f) return SFSEG_OK;   // x_out = the last binarised iterate (values in (0,1))
   // (a8) x_K = y_K / nu_K (dense output)
   {
     dim3 grid((unsigned)P.gx, (unsigned)P.BT);
@@ -937,7 +983,7 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   float* x0p = x0 ? at<float>(ws, P.off_x0p) : nullptr;
   const double* tape_nu = static_cast<const double*>(tape);
   auto tape_u = [&](int i) -> const float* {
-    return reinterpret_cast<const float*>(static_cast<const char*>(tape) + P.tape_nu_bytes +
+    return reinterpret_cast<const float*>(static_cast<const char*>(tape) + P.tape_hdr_bytes +
                                           (size_t)i * align_up(sizeof(float) * (size_t)P.vol_elems));
   };
 
@@ -960,6 +1006,8 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   ip.sc = at<double>(ws, P.off_sc);
   ip.partials = at<double>(ws, P.off_part);
   ip.counter = &at<WsHeader>(ws, 0)->counter[2];
+  ip.tape_bin = reinterpret_cast<const double*>(static_cast<const char*>(tape) + P.tape_nu_bytes);
+  ip.kappa = P.kappa(K);
   ip.B = (int)P.B;
   ip.T = (int)P.T;
   ip.H = (int)P.H;
@@ -1002,6 +1050,7 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   be.Wp = (int)P.Wp;
   be.gx = P.gx;
   be.K = K;
+  be.tape_bin = ip.tape_bin;
   TpassParams tp;
   std::memset(&tp, 0, sizeof(tp));
   fill_tpass_common(tp, P, ws);
@@ -1018,7 +1067,9 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
     sp.u1 = tape_u(k - 1);
     sp.u2 = (k >= 2) ? tape_u(k - 2) : nullptr;
     sp.k = k;
-    if (P.tc) {
+    // plain spatial pass + streaming epilogue: always with the tensor-core pass, and on the FP32
+    // plan when an iteration is binarised (the fused FP32 epilogue has no binarisation adjoint)
+    if (P.tc || P.bin) {
       SpassParams pl = sp;
       pl.plain = 1;
       pl.out = ubuf;
@@ -1030,6 +1081,7 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
       be.u1 = sp.u1;
       be.u2 = sp.u2;
       be.k = k;
+      be.kappa_prev = P.kappa(k - 1);
       {
         ProfScope ps(P.prof, st, PC_BWD);
         bwd_epi_kernel<<<dim3((unsigned)P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(be);
@@ -1657,6 +1709,39 @@ sfseg_status sfseg_adamw_step(double* w, const double* grad, double* state, int3
   P.amsgrad = hp->amsgrad ? 1 : 0;
   adamw_kernel<<<(unsigned)((n + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(P);
   return map_cuda(cudaGetLastError());
+}
+
+size_t sfseg_focal_dice_ws_bytes(sfseg_shape sh) {
+  if (sh.B < 1 || sh.T < 1) return 0;
+  const size_t BT = (size_t)(sh.B * sh.T);
+  return align_up(sizeof(WsHeader)) + align_up(sizeof(double) * 3 * BT * kFdGx) + align_up(sizeof(double) * BT);
+}
+
+sfseg_status sfseg_focal_dice(const float* x, const uint8_t* mask, sfseg_shape sh, double gamma, double* loss,
+                              float* dL_dx, void* ws, size_t ws_bytes, void* stream) {
+  if (!x || !mask || !loss || !dL_dx || !(gamma > 0.0) || !std::isfinite(gamma)) return SFSEG_ERR_INVALID_ARGUMENT;
+  if (sh.B < 1 || sh.T < 1 || sh.H < 1 || sh.W < 1) return SFSEG_ERR_SHAPE;
+  sfseg_status s = check_ws(ws, ws_bytes, sfseg_focal_dice_ws_bytes(sh));
+  if (s != SFSEG_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  FocalDiceParams P;
+  P.x = x;
+  P.t = mask;
+  P.grad = dL_dx;
+  P.counter = &at<WsHeader>(ws, 0)->counter[0];
+  P.part = at<double>(ws, align_up(sizeof(WsHeader)));
+  P.frame_loss = at<double>(ws, align_up(sizeof(WsHeader)) + align_up(sizeof(double) * 3 * (size_t)(sh.B * sh.T) * kFdGx));
+  P.loss = loss;
+  P.HW = (long)(sh.H * sh.W);
+  P.BT = (int)(sh.B * sh.T);
+  P.gamma = gamma;
+  SF_CUDA(cudaMemsetAsync(ws, 0, align_up(sizeof(WsHeader)), st));
+  const dim3 grid(kFdGx, (unsigned)(sh.B * sh.T));
+  focal_dice_sums_kernel<<<grid, kEwThreads, 0, st>>>(P);
+  SF_CUDA(after_launch("focal_dice_sums", st));
+  focal_dice_grad_kernel<<<grid, kEwThreads, 0, st>>>(P);
+  SF_CUDA(after_launch("focal_dice_grad", st));
+  return SFSEG_OK;
 }
 
 }  // extern "C"

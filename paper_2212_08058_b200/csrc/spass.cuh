@@ -116,8 +116,12 @@ __device__ __forceinline__ void fwd_finalize(double* sc, double* stats, double* 
   sc[SC_NU] = nu;
 }
 
-// Backward step k produced x_bar_{k-1}; s0 = c_{k-1} = <x_{k-1}, x_bar_{k-1}>.
-__device__ __forceinline__ void bwd_finalize(double* sc, const double* tape_nu, int K, int k, int b, double s0) {
+// Backward step k produced x_bar_{k-1}; s0 = c_{k-1} = <x_{k-1}, x_bar_{k-1}>.  When iteration
+// k-1 was soft-binarised, x_bar holds g = kappa sigma' b_bar and the caller passes
+// s0 = sum(x g) - theta sum(g) (= <x, g - [x > 0] sum(g)/n_pos>) and corr = sum(g) / n_pos.
+__device__ __forceinline__ void bwd_finalize(double* sc, const double* tape_nu, int K, int k, int b, double s0,
+                                             double corr = 0.0) {
+  sc[SC_CORR] = corr;
   if (k >= 2) {
     const double nu1 = tape_nu[(long)b * K + (k - 2)];
     sc[SC_CN] = s0 / nu1;

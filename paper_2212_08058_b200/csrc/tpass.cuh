@@ -16,7 +16,8 @@ constexpr int kMaxRT = 16;
 
 enum TpassMode : int {
   TP_FWD = 0,   // src = p (stored iterate), out = s_{k-1} * G_t * p
-  TP_BWD = 1,   // src = F * y_bar_k, y_bar_k = (x_bar_k - F u_{k-1} cn) * inv_nu  (Appendix A)
+  TP_BWD = 1,   // src = F * y_bar_k, y_bar_k = (x_bar_k - [x_k > 0] corr - F u_{k-1} cn) * inv_nu (Appendix A;
+                //   corr != 0 only after a soft-binarised iteration, reading A21)
   TP_FWDF = 2,  // full SFSeg operator (f1): src = F^fexp * a, out = s_{k-1} * G_t * src  (Eq.7's three inputs)
 };
 
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   const float4* src = reinterpret_cast<const float4*>(P.src) + b * vol4 + ec;
   const float4* Fp = nullptr;
   const float4* U1 = nullptr;
-  float cn = 0.f, inv_nu = 0.f, scale = 1.f;
+  float cn = 0.f, inv_nu = 0.f, corr = 0.f, scale = 1.f;
   if (MODE == TP_FWD) {
     scale = (float)P.sc[b * kScal + SC_S];
   } else if (MODE == TP_FWDF) {
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
     U1 = reinterpret_cast<const float4*>(P.u1) + b * vol4 + ec;
     cn = (float)P.sc[b * kScal + SC_CN];
     inv_nu = (float)P.sc[b * kScal + SC_INV_NU];
+    corr = (float)P.sc[b * kScal + SC_CORR];  // 0 unless iteration k was soft-binarised
   }
   const float4* hlo = P.halo_lo ? reinterpret_cast<const float4*>(P.halo_lo) + (long)b * RT * P.frame4 + ec : nullptr;
   const float4* hhi = P.halo_hi ? reinterpret_cast<const float4*>(P.halo_hi) + (long)b * RT * P.frame4 + ec : nullptr;
@@ -128,10 +130,10 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
       }
     } else if (j >= 0 && j < T) {
       const float4 xb = sq[sl][0][tid], f = sq[sl][1][tid], u = sq[sl][2][tid];
-      val.x = f.x * ((xb.x - f.x * u.x * cn) * inv_nu);
-      val.y = f.y * ((xb.y - f.y * u.y * cn) * inv_nu);
-      val.z = f.z * ((xb.z - f.z * u.z * cn) * inv_nu);
-      val.w = f.w * ((xb.w - f.w * u.w * cn) * inv_nu);
+      val.x = f.x * ((xb.x - (f.x * u.x > 0.f ? corr : 0.f) - f.x * u.x * cn) * inv_nu);
+      val.y = f.y * ((xb.y - (f.y * u.y > 0.f ? corr : 0.f) - f.y * u.y * cn) * inv_nu);
+      val.z = f.z * ((xb.z - (f.z * u.z > 0.f ? corr : 0.f) - f.z * u.z * cn) * inv_nu);
+      val.w = f.w * ((xb.w - (f.w * u.w > 0.f ? corr : 0.f) - f.w * u.w * cn) * inv_nu);
     } else if (HALO) {
       // backward halos arrive pre-multiplied (F * y_bar of the neighbour slab)
       const float4* g = frame_src(jp, 0);
