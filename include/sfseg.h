@@ -284,6 +284,19 @@ sfseg_status sfseg_solve_host(const float* ch_host, int32_t C, const float* w_ho
                               uint8_t* d_mask, float* x_out_host, uint8_t* mask_out_host,
                               void* ws, size_t ws_bytes, void* stream);
 
+/* End-to-end over a BATCH of host volumes, pipelined inside the library: the H2D copy of
+ * volume i+1 (stream_h2d) and the D2H copy of volume i-1 (stream_d2h) overlap the solve and
+ * threshold of volume i (stream), one cudaMemcpyAsync per copy, two device slots ordered by
+ * events (created and destroyed inside the call).  ch_host[i]: [B][C][T][H][W] (pinned for
+ * overlap); x_out_host[i] / mask_out_host[i] (either array or entry may be NULL).  d_ch
+ * [2][B][C][T][H][W], d_x [2][B][T][H][W], d_mask [2][B][T][H][W]: caller-owned device slots.
+ * Streams are the caller's.  Syncs; returns the first device error of any volume. */
+sfseg_status sfseg_solve_host_batch(const float* const* ch_host, int32_t n, int32_t C, const float* w_host,
+                                    float b, int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
+                                    float tau, int32_t thr_mode, float* d_ch, float* d_x, uint8_t* d_mask,
+                                    float* const* x_out_host, uint8_t* const* mask_out_host, void* ws,
+                                    size_t ws_bytes, void* stream, void* stream_h2d, void* stream_d2h);
+
 /* ---- plan introspection ----
  * The forward path sfseg_power_iterate_ex takes for this shape, Gaussian and algo on
  * one GPU without a tape (a tape forces the two-pass iteration): info_host[0] =

@@ -65,7 +65,7 @@ class ParallelFilter:
         self._b = shared_memory.SharedMemory(create=True, size=n)
         self.vin = np.ndarray(self.shape, np.float64, buffer=self._a.buf)
         self.vout = np.ndarray(self.shape, np.float64, buffer=self._b.buf)
-        ctx = mp.get_context("fork")
+        ctx = mp.get_context("spawn")   # no fork of a multi-threaded (CUDA) parent
         self.pool = ctx.Pool(self.procs, initializer=_attach, initargs=(self._a.name, self._b.name, self.shape))
 
     def close(self):

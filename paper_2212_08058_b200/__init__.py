@@ -111,6 +111,9 @@ _SIGS = {
     "sfseg_solve_host": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                    C.c_float, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "sfseg_forward_path": (C.c_int, [Shape, GaussC, C.c_int32, C.POINTER(C.c_int32)]),
+    "sfseg_solve_host_batch": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC,
+                                         C.c_int32, C.c_float, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_size_t,
+                                         _P, _P, _P]),
     "sfseg_workspace_bytes_online": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
     "sfseg_power_iterate_online": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
                                              C.c_int32, C.c_int32, _P, _P, C.c_size_t, _P]),
@@ -434,6 +437,46 @@ def solve_host(ch_host: torch.Tensor, w, gauss: Gauss, K: int, tau: float, solve
         None if x_out_host is None else C.c_void_p(x_out_host.data_ptr()),
         None if mask_out_host is None else C.c_void_p(mask_out_host.data_ptr()),
         _ptr(solver.ws), solver.ws.numel(), _stream(stream)), "sfseg_solve_host")
+
+
+class HostBatch:
+    """End to end over HOST buffers through ONE library call (sfseg_solve_host_batch): the
+    library pipelines H2D of volume i+1 and D2H of volume i-1 under the solve of volume i on
+    the caller's streams.  Holds the two device slots and the copy streams."""
+
+    def __init__(self, solver: "Solver"):
+        self.solver = solver
+        dev = solver.device
+        B, T, H, W = solver.shape
+        self.d_ch = torch.empty((2, B, solver.C, T, H, W), dtype=torch.float32, device=dev)
+        self.d_x = torch.empty((2, B, T, H, W), dtype=torch.float32, device=dev)
+        self.d_m = torch.empty((2, B, T, H, W), dtype=torch.uint8, device=dev)
+        self.s_h2d = torch.cuda.Stream(dev)
+        self.s_d2h = torch.cuda.Stream(dev)
+
+    def run(self, ch_hosts, w, tau: float, x_hosts=None, mask_hosts=None, b: float = 0.0, act: int = ACT_IDENTITY,
+            thr_mode: int = THR_PER_FRAME_MAX, stream=None) -> None:
+        s = self.solver
+        B, T, H, W = s.shape
+        n = len(ch_hosts)
+        for t in ch_hosts:
+            if t.is_cuda or t.dtype != torch.float32 or tuple(t.shape) != (B, s.C, T, H, W) or not t.is_contiguous():
+                raise ValueError("ch_hosts must be contiguous float32 host tensors of the solver's shape")
+        for arr, dt in ((x_hosts, torch.float32), (mask_hosts, torch.uint8)):
+            if arr is not None:
+                if len(arr) != n:
+                    raise ValueError("one output per input volume")
+                for t in arr:
+                    if t.is_cuda or t.dtype != dt or tuple(t.shape) != s.shape or not t.is_contiguous():
+                        raise ValueError(f"outputs must be contiguous {dt} host tensors of shape {s.shape}")
+        chp = (C.c_void_p * n)(*[t.data_ptr() for t in ch_hosts])
+        xp = None if x_hosts is None else (C.c_void_p * n)(*[t.data_ptr() for t in x_hosts])
+        mp = None if mask_hosts is None else (C.c_void_p * n)(*[t.data_ptr() for t in mask_hosts])
+        _check(lib().sfseg_solve_host_batch(
+            chp, n, s.C, _weights(w, s.C), float(b), int(act), Shape(*s.shape), s.gauss.c(), s.K, float(tau),
+            int(thr_mode), _ptr(self.d_ch), _ptr(self.d_x), _ptr(self.d_m), xp, mp, _ptr(s.ws), s.ws.numel(),
+            _stream(stream), C.c_void_p(self.s_h2d.cuda_stream), C.c_void_p(self.s_d2h.cuda_stream)),
+            "sfseg_solve_host_batch")
 
 
 class HostStream:

@@ -25,6 +25,9 @@ SOURCES = ["sfseg_api.cu", "spass_fwd.cu", "spass_bwd.cu", "tpass.cu", "f3d.cu",
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+# A/B builds of compile-time kernel variants (tools/gpu_variants.sh), e.g. "-DSPTC_MIN_CTAS=2";
+# part of the build digest, empty for the product build
+FLAGS += os.environ.get("SFSEG_NVCC_DEFS", "").split()
 
 
 def _nvcc() -> str:

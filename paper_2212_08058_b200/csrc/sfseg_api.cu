@@ -1506,6 +1506,70 @@ sfseg_status sfseg_solve_host(const float* ch_host, int32_t C, const float* w_ho
   return sfseg_sync_status(ws, stream);
 }
 
+sfseg_status sfseg_solve_host_batch(const float* const* ch_host, int32_t n, int32_t C, const float* w_host, float b,
+                                    int32_t act, sfseg_shape sh, sfseg_gauss gauss, int32_t K, float tau,
+                                    int32_t thr_mode, float* d_ch, float* d_x, uint8_t* d_mask,
+                                    float* const* x_out_host, uint8_t* const* mask_out_host, void* ws,
+                                    size_t ws_bytes, void* stream, void* stream_h2d, void* stream_d2h) {
+  if (!ch_host || n < 1 || !d_ch || !d_x || !d_mask || !w_host || !stream_h2d || !stream_d2h ||
+      !validate_act(act) || !std::isfinite(tau) || thr_mode < 0 || thr_mode > 2)
+    return SFSEG_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < n; ++i)
+    if (!ch_host[i]) return SFSEG_ERR_INVALID_ARGUMENT;
+  Plan P;
+  sfseg_status s = make_plan(sh, C, gauss, K, &P);
+  if (s != SFSEG_OK) return s;
+  if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
+  const size_t thr_ws = sfseg_threshold_ws_bytes(sh);
+  if ((s = check_ws(ws, ws_bytes, P.ws_fwd + thr_ws)) != SFSEG_OK) return s;
+  cudaStream_t sc = static_cast<cudaStream_t>(stream), si = static_cast<cudaStream_t>(stream_h2d),
+               so = static_cast<cudaStream_t>(stream_d2h);
+  const size_t nvox = (size_t)(sh.B * sh.T * sh.H * sh.W);
+  cudaEvent_t ev[3][2] = {};
+  for (auto& row : ev)
+    for (auto& e : row) SF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  auto destroy = [&]() {
+    for (auto& row : ev)
+      for (auto& e : row)
+        if (e) cudaEventDestroy(e);
+  };
+  cudaError_t ce = cudaSuccess;
+  for (int i = 0; i < n && s == SFSEG_OK && ce == cudaSuccess; ++i) {
+    const int sl = i & 1;
+    float* dch = d_ch + (size_t)sl * nvox * C;
+    float* dx = d_x + (size_t)sl * nvox;
+    uint8_t* dm = d_mask + (size_t)sl * nvox;
+    // H2D of volume i while volume i-1 solves: its slot's previous solve must be done reading
+    if (i >= 2 && (ce = cudaStreamWaitEvent(si, ev[1][sl], 0)) != cudaSuccess) break;
+    if ((ce = cudaMemcpyAsync(dch, ch_host[i], sizeof(float) * nvox * C, cudaMemcpyHostToDevice, si)) != cudaSuccess) break;
+    if ((ce = cudaEventRecord(ev[0][sl], si)) != cudaSuccess) break;
+    if ((ce = cudaStreamWaitEvent(sc, ev[0][sl], 0)) != cudaSuccess) break;
+    // the slot's x / mask of volume i-2 must be copied out before they are overwritten
+    if (i >= 2 && (ce = cudaStreamWaitEvent(sc, ev[2][sl], 0)) != cudaSuccess) break;
+    s = sfseg_power_iterate(dch, C, w_host, b, act, sh, gauss, K, nullptr, dx, nullptr, nullptr, 0, nullptr, ws,
+                            P.ws_fwd, nullptr, stream);
+    if (s != SFSEG_OK) break;
+    s = sfseg_threshold(dx, sh, tau, thr_mode, dm, static_cast<char*>(ws) + P.ws_fwd, thr_ws, stream);
+    if (s != SFSEG_OK) break;
+    if ((ce = cudaEventRecord(ev[1][sl], sc)) != cudaSuccess) break;
+    // D2H of volume i while volume i+1 solves
+    if ((ce = cudaStreamWaitEvent(so, ev[1][sl], 0)) != cudaSuccess) break;
+    if (x_out_host && x_out_host[i] &&
+        (ce = cudaMemcpyAsync(x_out_host[i], dx, sizeof(float) * nvox, cudaMemcpyDeviceToHost, so)) != cudaSuccess)
+      break;
+    if (mask_out_host && mask_out_host[i] &&
+        (ce = cudaMemcpyAsync(mask_out_host[i], dm, nvox, cudaMemcpyDeviceToHost, so)) != cudaSuccess)
+      break;
+    if ((ce = cudaEventRecord(ev[2][sl], so)) != cudaSuccess) break;
+  }
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(so);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(si);
+  destroy();
+  if (ce != cudaSuccess) return map_cuda(ce);
+  if (s != SFSEG_OK) return s;
+  return sfseg_sync_status(ws, stream);   // first device error of any volume (sticky)
+}
+
 sfseg_status sfseg_get_unique_id(uint8_t id_host[128]) {
   if (!id_host) return SFSEG_ERR_INVALID_ARGUMENT;
   NcclApi& api = nccl();

@@ -51,3 +51,30 @@ def test_online_c2_recipe_multichannel(sf):
     F, _ = O.combine(wl.ch, wl.w)
     xo = O.power_iterate_online(F, O.gaussian_taps(2.0, 6), O.gaussian_taps(8.0, 24), 6, 14, 7)
     assert _rel(x, xo) <= 1e-4
+
+
+def test_online_zero_window_error_is_not_wiped(sf):
+    """an all-zero F window in the MIDDLE of the video (stride == q, so windows
+    are disjoint) makes that window's solve degenerate; later windows must not clear the
+    workspace's error word (sticky until sfseg_sync_status), so the call reports it."""
+    rng = np.random.default_rng(5)
+    ch = (rng.random((1, 1, 15, 20, 30)) * 0.8 + 0.1).astype(np.float32)
+    ch[:, :, 5:10] = 0.0   # window [5, 10) is all zero
+    with pytest.raises(sf.SfsegError) as e:
+        sf.power_iterate_online(torch.from_numpy(ch).cuda(), [1.0], sf.Gauss(1.0, 2.0, 2, 6), 4, 5, 5)
+    assert e.value.status == 4   # SFSEG_ERR_DEGENERATE
+
+
+def test_sticky_error_survives_later_solves(sf):
+    """Two solves on one workspace, the first degenerate (F == 0), the second fine: the
+    error is reported at the sync after the second (sticky), then cleared."""
+    g = sf.Gauss(1.0, 2.0, 2, 6)
+    s = sf.Solver((1, 4, 16, 24), 1, g, 3)
+    z = torch.zeros((1, 1, 4, 16, 24), dtype=torch.float32, device="cuda")
+    ok = torch.rand((1, 1, 4, 16, 24), dtype=torch.float32, device="cuda") + 0.1
+    s.forward(z, [1.0], check=False)
+    s.forward(ok, [1.0], check=False)
+    with pytest.raises(sf.SfsegError) as e:
+        s.sync()
+    assert e.value.status == 4
+    s.forward(ok, [1.0])   # cleared by the sync that reported it

@@ -443,68 +443,6 @@ def test_backward_user_x0(sf):
     assert abs(db - dbo) <= G_TOL * max(abs(dbo), np.abs(dwo).max())
 
 
-# --------------------------------------------------------------------------- full BASELINE sizes
-@pytest.mark.slow
-def test_c2_full_size_parity(sf):
-    """configs[1] at full size in the bench's launch configuration, against the full oracle."""
-    wl = WL.generate("c2")
-    c = wl.cfg
-    xg, xo, stg = _check_forward(sf, wl.ch, wl.w, c.sigma_t, c.sigma_s, c.radius_t, c.radius_s, c.K)
-    assert (xg >= 0).all()
-    g = stg[0, :, 1]
-    assert (np.diff(g) >= -1e-6 * g[1:]).all()
-
-
-@pytest.mark.slow
-def test_c4_full_size_sampled_volumes(sf):
-    """configs[3] at full size (64 volumes of 32x256x256, C=4) in the bench's launch
-    configuration; the volumes are independent, so the oracle solves a sample of them."""
-    wl = WL.generate("c4", with_mask=False)
-    c = wl.cfg
-    dev = torch.device("cuda")
-    B, C, T, H, W = wl.ch.shape
-    s = sf.Solver((B, T, H, W), C, sf.Gauss(c.sigma_t, c.sigma_s, c.radius_t, c.radius_s), c.K)
-    x = s.forward(torch.from_numpy(wl.ch).to(dev), wl.w).cpu().numpy()
-    gains = s.stats.cpu().numpy()[..., 1]
-    for v in (0, 17, 63):
-        xo, sto = _oracle_solve(wl.ch[v:v + 1], wl.w, (c.sigma_t, c.sigma_s, c.radius_t, c.radius_s), c.K)
-        assert _rel(x[v], xo[0]) <= X_TOL, f"volume {v}: {_rel(x[v], xo[0]):.3e}"
-        np.testing.assert_allclose(gains[v], sto["gain"][0], rtol=GAIN_TOL)
-    # every volume: unit norm, non-negative, monotone gain (properties at any size)
-    n = np.linalg.norm(x.reshape(B, -1).astype(np.float64), axis=1)
-    assert np.abs(n - 1.0).max() < 1e-5
-    assert (x >= 0).all()
-    assert (np.diff(gains, axis=1) >= -1e-6 * gains[:, 1:]).all()
-
-
-@pytest.mark.slow
-def test_c5_full_size_properties_and_crop(sf):
-    """configs[4] at full size (512x1080x1920, C=2, r = (9, 36), K = 20) on one GPU: the
-    oracle cannot solve 1.06 G voxels, so the full solve is checked by properties (unit norm,
-    non-negativity, monotone gain, time-reversal equivariance) and the same kernels against
-    the oracle on a T=24 crop of the same recipe."""
-    wl = WL.generate("c5", with_mask=False)
-    c = wl.cfg
-    dev = torch.device("cuda")
-    B, C, T, H, W = wl.ch.shape
-    g = sf.Gauss(c.sigma_t, c.sigma_s, c.radius_t, c.radius_s)
-    s = sf.Solver((B, T, H, W), C, g, c.K)
-    ch = torch.from_numpy(wl.ch).to(dev)
-    x = s.forward(ch, wl.w)
-    gains = s.stats.cpu().numpy()[0, :, 1]
-    assert abs(float(torch.linalg.vector_norm(x.double())) - 1.0) < 1e-5
-    assert float(x.min()) >= 0.0
-    assert (np.diff(gains) >= -1e-6 * gains[1:]).all()
-    # mirror in time: M commutes with the time reversal, so x_K(flip ch) == flip x_K(ch)
-    xr = s.forward(torch.flip(ch, dims=[2]).contiguous(), wl.w)
-    assert float(torch.linalg.vector_norm((torch.flip(xr, dims=[1]) - x).double())) <= 1e-4
-    del x, xr, ch, s
-    torch.cuda.empty_cache()
-    cfg = WL.get_config("c5", T=24, H=120, W=300)
-    crop = WL.generate("c5", cfg=cfg, with_mask=False)
-    _check_forward(sf, crop.ch, crop.w, c.sigma_t, c.sigma_s, c.radius_t, c.radius_s, 6)
-
-
 @pytest.mark.parametrize("algo,radii,expect", [
     ("auto", (6, 24), "tc"), ("auto", (1, 3), "f3d"), ("fp32", (6, 24), "fp32"), ("two", (1, 3), "fp32"),
 ])

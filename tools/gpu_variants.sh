@@ -1,0 +1,23 @@
+#!/bin/bash
+# A/B of compile-time variants of the kernels on the c2 bench (rebuilds per variant, then
+# restores the product build).  gpurun -- 'bash tools/gpu_variants.sh <tag> "<defs1>" "<defs2>" ...'
+TAG=$1; shift
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+i=0
+for DEFS in "$@"; do
+  export SFSEG_NVCC_DEFS="$DEFS"
+  python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$i.log 2>&1
+  timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 10 --warmup 3 > $OUT/bench_$i.json 2> $OUT/bench_$i.err
+  python - "$DEFS" $OUT/bench_$i.json <<'PY' >> $OUT/summary.txt
+import json, sys
+d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
+r = d["roofline"]
+print(f"{sys.argv[1] or 'default':40s} ms/step {d['ms_per_step']:.3f}  spass {r['launch_ms']*1e3:.1f} us  "
+      f"tpass {r.get('tpass', {}).get('launch_ms', 0)*1e3:.1f} us  value {d['value']:.3e}")
+PY
+  i=$((i+1))
+done
+unset SFSEG_NVCC_DEFS
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build_restore.log 2>&1
+cat $OUT/summary.txt
