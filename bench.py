@@ -3,19 +3,21 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 
-A "step" is one pass of the whole hot path over one synthetic volume:
-fused channel combine + K_iter power iterations (temporal pass, fused spatial
-pass with F multiplies and norm -- on the bf16 tensor pipe for r_s >= 8, or the
-fused single-pass 3D kernel for small radii) + final normalisation + per-frame
-threshold, captured once and replayed as one CUDA
-graph per step (--graph 0: stream launches).  At N=1 the workload is BASELINE.json configs[1]
-("c2": 1x70x480x854, C=1, sigma_t=2, sigma_s=8, 15 iterations, tau=0.5).
-For N>1 (torchrun, one rank per GPU) every rank solves its own c2 volume
-(data-parallel over independent volumes, weak scaling, no data-path collective);
-with --shard slab the ranks split ONE volume into time slabs (NCCL halo
-exchange of r_t frames + fp64 norm allreduce every iteration, strong scaling).
+A "step" is one pass of the whole hot path over one synthetic volume (batch):
+fused channel combine + K power iterations (temporal pass, fused spatial pass with
+the F multiplies and the norm -- on the tensor pipe in fp32-class six-product split
+bf16 for r_s >= 8 (A23), or the fused single-pass 3D kernel for small
+radii) + final normalisation + per-frame threshold,
+captured once and replayed as one CUDA graph per step (--graph 0: stream launches).
 
-metric: voxel-iterations/s = B*T*H*W*K_iter per step, whole job.
+N=1: BASELINE.json configs[1] ("c2": 1x70x480x854, C=1, sigma_t=2, sigma_s=8,
+15 iterations, tau=0.5).  N>1 (one process per GPU; `--gpus N` without torchrun
+re-launches itself under torch.distributed.run): configs[4] ("c5": 1x512x1080x1920,
+C=2, K=20) in time slabs of 512/N frames (NCCL halo exchange of r_t frames + fp64
+norm allreduce every iteration, strong scaling); `--shard volume` runs configs[3]
+("c4") with 64/N of its volumes per rank (no data-path collective, strong scaling).
+
+metric: voxel-iterations/s = B*T*H*W*K per step, whole job.
 """
 from __future__ import annotations
 
@@ -37,8 +39,9 @@ ALU_PEAK_FMA_PER_CLK_PER_SM = 128     # FP32 lanes per SM (B200_PROFILING.md / b
 SM_COUNT = 148
 # legacy warp-level HMMA (mma.sync m16n8k16 bf16, fp32 accumulate) full-chip rate measured by
 # tools/mma_microbench.cu on this pool's B200 (profiles/mma/mma.log): the ceiling of the
-# tensor-core spatial pass's instruction choice (a third of the tcgen05 dense bf16 peak)
+# tensor-core spatial pass's instruction choice
 MMA_SYNC_BF16_TFLOPS = 555.6
+TC_PRODUCTS = 6                       # bf16 products per tap (three planes per operand, A23)
 
 
 def _peaks():
@@ -49,6 +52,17 @@ def _peaks():
         return d, "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.lower().startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -116,59 +130,114 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_oracle_sample(cfg_name: str, t_crop: int = 0):
-    """Time the oracle (as it stands) on a bounded sample: one power iteration of
-    the workload (optionally on the first t_crop frames).  Returns (vox_iter_per_s, secs, sample)."""
+def _default_config(args, world: int) -> str:
+    if args.config:
+        return args.config
+    if world > 1:
+        return "c4" if args.shard == "volume" else "c5"
+    return "c2"
+
+
+def cpu_oracle_baseline(cfg_name: str, full_iters: bool = True, single_core: bool = True):
+    """The oracle as it stands (oracle/: plain numpy f64), timed on this host's cores.
+
+    multi-core: oracle.parallel (the serial oracle's filter split into independent frame /
+      row pieces on every core -- bitwise the serial result) over ALL K iterations of the
+      workload (c2: 15 iterations of 1x70x480x854), or over the first iteration(s) for the
+      configs whose full solve exceeds ~30 s (c4: 1 of 10, c5: 1 iteration of a T=64 crop);
+    single-core: one iteration of the serial oracle on the first 16 frames.
+    Returns the cpu_baseline dict of the JSON line."""
     import numpy as np
     import oracle as O
+    from oracle import parallel as OP
     import workloads as WL
     cfg = WL.get_config(cfg_name)
-    if t_crop:
-        wl = WL.generate(cfg_name, t_range=(0, min(t_crop, cfg.T)))
-    else:
-        wl = WL.generate(cfg_name)
     gt, gs = O.gaussian_taps(cfg.sigma_t, cfg.radius_t), O.gaussian_taps(cfg.sigma_s, cfg.radius_s)
-    if cfg_name == "c2f":   # full SFSeg operator (f1): three convolutions per iteration
+    cores = OP.host_cores()
+    out = {"unit": UNIT, "cores": cores, "cpu_model": _cpu_model(), "kind": "oracle"}
+    if cfg_name == "c5":
+        wl = WL.generate(cfg_name, t_range=(0, 64), with_mask=False)
+        iters, what = 1, "1 of 20 iterations of a 1x64x1080x1920 crop of c5"
+    elif cfg_name == "c4":
+        wl = WL.generate(cfg_name, volumes=range(16), with_mask=False)
+        iters, what = 1, "1 of 10 iterations of 16 of the 64 c4 volumes"
+    else:
+        wl = WL.generate(cfg_name, with_mask=False)
+        iters = cfg.K if full_iters else 1
+        what = f"{iters} of {cfg.K} iterations of {cfg_name} {'x'.join(map(str, wl.ch.shape[:1] + wl.ch.shape[2:]))}"
+    if cfg_name == "c2f":
         e = wl.extra
         S, U, F = O.combine_full(wl.ch, wl.w, wl.b, 0, e["f_ch"], e["wf"], 0.0, 0, e["p"])
         t0 = time.perf_counter()
         O.power_iterate_full(S, U, F, e["alpha"], gt, gs, 1)
-    else:
-        F, _ = O.combine(wl.ch, wl.w, wl.b, cfg.act)
-        t0 = time.perf_counter()
-        O.power_iterate(F, gt, gs, 1)
+        dt = time.perf_counter() - t0
+        out.update(value=F.size / dt, cores=1, sample=f"1 of {cfg.K} iterations of the full operator (serial)",
+                   seconds=dt)
+        return out
+    F, _ = O.combine(wl.ch, wl.w, wl.b, cfg.act)
+    OP.power_iterate(F[:1, :min(F.shape[1], 8)], gt, gs, 1, procs=cores)   # pool start-up, imports
+    t0 = time.perf_counter()
+    OP.power_iterate(F, gt, gs, cfg.K, procs=cores, iters=iters)
     dt = time.perf_counter() - t0
-    nvox = F.size
-    sample = (f"1 of {cfg.K} power iterations (combine excluded) of {cfg_name} "
-              f"{'x'.join(str(s) for s in F.shape)} in numpy float64, single thread")
-    return nvox / dt, dt, sample
+    out.update(value=F.size * iters / dt, seconds=dt,
+               sample=f"{what}, multi-process oracle (oracle/parallel.py) on {cores} cores; combine excluded")
+    if single_core:
+        crop = F[:1, :min(F.shape[1], 16)]
+        t0 = time.perf_counter()
+        O.power_iterate(crop, gt, gs, 1)
+        d1 = time.perf_counter() - t0
+        out["single_core"] = {"value": crop.size / d1, "seconds": d1,
+                              "sample": f"1 iteration of the serial oracle on {'x'.join(map(str, crop.shape))}"}
+    return out
 
 
 def run_reference(args):
+    """--impl reference: the oracle (the paper's method as plain f64 numpy) on the host cores,
+    each step one power iteration of the workload (multi-process oracle), rank 0 only."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
+    import numpy as np
+    import oracle as O
+    from oracle import parallel as OP
     import workloads as WL
-    cfg = WL.get_config(args.config)
-    t_crop = 16 if args.config in ("c2", "c3", "probe", "c2f") else 8
-    for _ in range(args.warmup):
-        cpu_oracle_sample(args.config, t_crop)
-    total_t, total_units = 0.0, 0
-    sample = ""
-    for _ in range(args.steps):
-        v, dt, sample = cpu_oracle_sample(args.config, t_crop)
-        total_t += dt
-        total_units += v * dt
-    value = total_units / total_t
+    cfg_name = _default_config(args, ws)
+    cfg = WL.get_config(cfg_name)
+    if cfg_name == "c5":
+        wl = WL.generate(cfg_name, t_range=(0, 64), with_mask=False)
+        what = "one power iteration of a 1x64x1080x1920 crop of c5"
+    elif cfg_name == "c4":
+        wl = WL.generate(cfg_name, volumes=range(8), with_mask=False)
+        what = "one power iteration of 8 of the 64 c4 volumes"
+    else:
+        wl = WL.generate(cfg_name if cfg_name != "c2f" else "c2", with_mask=False)
+        what = f"one of the {cfg.K} power iterations of {cfg_name}"
+    gt, gs = O.gaussian_taps(cfg.sigma_t, cfg.radius_t), O.gaussian_taps(cfg.sigma_s, cfg.radius_s)
+    F, _ = O.combine(wl.ch, wl.w, wl.b, cfg.act)
+    cores = OP.host_cores()
+    total_t = 0.0
+    with OP.ParallelFilter(F.shape[1:], cores) as filt:
+        def one():   # y_1 = F * G(F * x_0), x_0 = F, and its norm (Eq.4/7/8)
+            for b in range(F.shape[0]):
+                y = F[b] * filt(F[b] * F[b], gt, gs, gs)
+                float(np.sum(y * y))
+        for _ in range(args.warmup):
+            one()
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            one()
+            total_t += time.perf_counter() - t0
+    value = F.size * args.steps / total_t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (workloads/ generator; DAVIS-2016-shaped blobs)",
-        "config": {"workload": f"{args.config}: {cfg.note}", "shape": [cfg.B, cfg.T, cfg.H, cfg.W], "C": cfg.C,
+        "config": {"workload": f"{cfg_name}: {cfg.note}", "shape": [cfg.B, cfg.T, cfg.H, cfg.W], "C": cfg.C,
                    "sigma_t": cfg.sigma_t, "sigma_s": cfg.sigma_s, "radius_t": cfg.radius_t,
                    "radius_s": cfg.radius_s, "iters": cfg.K},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu_model": _cpu_model(), "kind": "oracle",
+                         "sample": f"each step: {what} (multi-process oracle, oracle/parallel.py)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -190,8 +259,11 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     sf.lib()
 
-    cfg = WL.get_config(args.config)
-    slab = world > 1 and args.shard == "slab"
+    cfg_name = _default_config(args, world)
+    args.config = cfg_name
+    cfg = WL.get_config(cfg_name)
+    slab = world > 1 and args.shard == "slab" and cfg_name != "c4"
+    vshard = world > 1 and not slab      # independent volumes split across ranks (c4: 64/N each)
     K = cfg.K
     gauss = sf.Gauss(cfg.sigma_t, cfg.sigma_s, cfg.radius_t, cfg.radius_s)
     if slab:
@@ -200,6 +272,11 @@ def run_ours(args):
         wl = WL.generate(args.config, t_range=(t0, t1), with_mask=False)
         uid = broadcast_unique_id(rank)
         comm = Comm(world, rank, local, uid)
+    elif vshard:
+        if cfg.B % world:
+            raise SystemExit(f"{cfg_name}: {cfg.B} volumes do not split over {world} ranks")
+        per = cfg.B // world
+        wl = WL.generate(args.config, volumes=range(rank * per, (rank + 1) * per), with_mask=False)
     else:
         # c3 (SFSeg++ ensemble) times forward + backward (dL/dw for the MSE loss, reading A13)
         wl = WL.generate(args.config, with_mask=(args.config == "c3"))
@@ -428,19 +505,19 @@ def run_ours(args):
     # ---------------------------------------------------------------- e2e through the C ABI with host buffers
     e2e = None
     if not args.no_e2e and not slab and not full:
-        # end to end over pinned HOST buffers through the public API: HostStream pipelines the
-        # H2D copy of volume i+1 and the D2H copy of volume i-1 under the solve of volume i
-        # (three streams); every step copies its full input in and its x + mask out.
-        x_hosts = [torch.empty((B, T, H, W), dtype=torch.float32).pin_memory() for _ in range(2)]
-        m_hosts = [torch.empty((B, T, H, W), dtype=torch.uint8).pin_memory() for _ in range(2)]
+        # end to end over pinned HOST buffers through ONE library call per batch of volumes
+        # (sfseg_solve_host_batch): the library pipelines the H2D copy of volume i+1 and the D2H
+        # copy of volume i-1 under the solve of volume i (one cudaMemcpyAsync per copy, caller's
+        # copy streams); every volume copies its full input in and its x + mask out.
         e2e_steps = max(2, min(args.steps, 10))
-        hs = sf.HostStream(solver, device=dev)
-        hs.run([ch_host] * 2, wl.w, cfg.tau, x_hosts, m_hosts, wl.b, cfg.act)
+        x_hosts = [torch.empty((B, T, H, W), dtype=torch.float32).pin_memory() for _ in range(e2e_steps)]
+        m_hosts = [torch.empty((B, T, H, W), dtype=torch.uint8).pin_memory() for _ in range(e2e_steps)]
+        hb = sf.HostBatch(solver)
+        hb.run([ch_host] * 2, wl.w, cfg.tau, x_hosts[:2], m_hosts[:2], wl.b, cfg.act)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        hs.run([ch_host] * e2e_steps, wl.w, cfg.tau, [x_hosts[i % 2] for i in range(e2e_steps)],
-               [m_hosts[i % 2] for i in range(e2e_steps)], wl.b, cfg.act)
+        hb.run([ch_host] * e2e_steps, wl.w, cfg.tau, x_hosts, m_hosts, wl.b, cfg.act)
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
@@ -448,8 +525,9 @@ def run_ours(args):
                "h2d_bytes_per_step": int(ch_host.numel() * 4),
                "d2h_bytes_per_step": int(x_hosts[0].numel() * 4 + m_hosts[0].numel()),
                "steps": e2e_steps,
-               "api": "HostStream.run: sfseg_power_iterate + sfseg_threshold per volume, H2D/D2H of pinned "
-                      "host buffers on copy streams overlapped with the previous/next solve"}
+               "api": "sfseg_solve_host_batch (C ABI): H2D of pinned host channels, solve, threshold, D2H of "
+                      "x_K and the mask per volume, copies pipelined inside the library on two copy streams"}
+        del hb
         # the unpipelined single call (sfseg_solve_host: H2D, solve, threshold, D2H, sync) for reference
         d_ch = torch.empty_like(ch)
         sf.solve_host(ch_host, wl.w, gauss, K, cfg.tau, solver, d_ch, x, mask, x_hosts[0], m_hosts[0])
@@ -457,24 +535,30 @@ def run_ours(args):
         for _ in range(2):
             sf.solve_host(ch_host, wl.w, gauss, K, cfg.tau, solver, d_ch, x, mask, x_hosts[0], m_hosts[0])
         e2e["unpipelined_value"] = units_per_step * 2 / (time.perf_counter() - t0)
+        del x_hosts, m_hosts, d_ch
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, sample = cpu_oracle_sample(args.config)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, "seconds": dt}
+        cpu = cpu_oracle_baseline(args.config)
 
     if rank == 0:
         ck = clocks.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if (slab or vshard) else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (workloads/ generator; DAVIS-2016-shaped blobs, seed 0)",
             "config": {"workload": f"{args.config}: {cfg.note}", "shape": [B, T, H, W], "C": Cn,
                        "sigma_t": cfg.sigma_t, "sigma_s": cfg.sigma_s, "radius_t": r_t, "radius_s": r_s,
                        "iters": K, "tau": cfg.tau,
-                       "parallelism": (f"time-slab x{world} (NCCL halo r_t frames + fp64 norm allreduce / iter)"
-                                       if slab else f"dp{world} (one volume per GPU)"),
+                       "parallelism": (f"time-slab x{world} (NCCL halo r_t frames + fp64 norm allreduce / iter; "
+                                       f"NCCL communicator of {comm.nranks} ranks)" if slab else
+                                       f"volume shards x{world} ({B} of {cfg.B} volumes per rank, no collective)"
+                                       if vshard else "one GPU"),
+                       "arithmetic": ("fp32 FFMA everywhere except the spatial pass of r_s >= 8, which runs on the "
+                                      "tensor pipe with each operand and tap split into three bf16 planes and six "
+                                      "products per tap (fp32-class; x_K error vs the f64 oracle 1.4x the FP32-FMA "
+                                      "pass's at full c2, tests/test_gpu_fullsize.py)"),
                        "l2": "inputs > L2 (ch 115 MB + F/p/v 344 MB vs 126 MB L2); no flush",
                        "launch": "one CUDA graph per step" if graph is not None else "stream launches"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
@@ -504,7 +588,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "probe", "c2f"])
+    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4", "c5", "probe", "c2f"],
+                    help="default: c2 at N=1, c5 (time slabs) at N>1, c4 with --shard volume")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -512,9 +597,22 @@ def main():
                     help="1 (default): replay the step as one captured CUDA graph (measured 2-3 %% faster than "
                          "stream launches at c2/probe/c2f, profiles/tc/ab_graph.txt); 0: stream launches. "
                          "Multi-rank time slabs and the training step (c3) always use stream launches")
-    ap.add_argument("--shard", default="volume", choices=["volume", "slab"],
-                    help="N>1: one volume per GPU (weak scaling) or time slabs of one volume with NCCL halos (strong)")
+    ap.add_argument("--shard", default="slab", choices=["volume", "slab"],
+                    help="N>1: time slabs of one volume with NCCL halos (default, c5) or the c4 batch split by "
+                         "volume (64/N per rank, no collective)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run (rendezvous on 127.0.0.1)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != ws and args.impl == "ours":
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; using {ws}", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
