@@ -261,6 +261,8 @@ def run_ours(args):
 
     cfg_name = _default_config(args, world)
     args.config = cfg_name
+    algo = {"auto": sf.ALGO_AUTO, "tcgen05": sf.ALGO_TWO_PASS_TCGEN05, "mma": sf.ALGO_TWO_PASS_MMA_SYNC,
+            "fp32": sf.ALGO_TWO_PASS_FP32}[args.algo]
     cfg = WL.get_config(cfg_name)
     slab = world > 1 and args.shard == "slab" and cfg_name != "c4"
     vshard = world > 1 and not slab      # independent volumes split across ranks (c4: 64/N each)
@@ -286,7 +288,7 @@ def run_ours(args):
     if slab:
         solver = SlabSolver(comm, (B, T, H, W), cfg.T, t0, Cn, gauss, K, device=dev)
     else:
-        solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev, want_tape=(args.config == "c3"))
+        solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev, want_tape=(args.config == "c3"), algo=algo)
     full = args.config == "c2f" and not slab
     if full:   # the full SFSeg operator replaces the hot-path solve
         fsolver = sf.FullSolver((B, T, H, W), Cn, 2, gauss, K, device=dev)
@@ -296,8 +298,9 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     # the per-frame threshold (a9) is frame-local: each rank thresholds its own slab
-    path_info = sf.forward_path((B, T, H, W), gauss)
-    path_tc = path_info[0] == sf.PATH_TWO_PASS_TC
+    path_info = sf.forward_path((B, T, H, W), gauss, algo)
+    path_tc = path_info[0] in (sf.PATH_TWO_PASS_TC, sf.PATH_TWO_PASS_TCGEN05)
+    path_t5 = path_info[0] == sf.PATH_TWO_PASS_TCGEN05
     thr_solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev) if slab else solver
 
     train = args.config == "c3" and not slab
@@ -449,10 +452,25 @@ def run_ours(args):
         # write p = 53 us at c2) rather than by the tensor pipe (its banded bf16x3 products
         # take 13.5 us at the measured dense bf16 peak); both reported
         RSc = path_info[2]
-        ra = (RSc + 3) // 4 * 4
-        nkx, nky = (16 + ra + RSc + 15) // 16, (16 + 2 * RSc + 15) // 16
-        S_, NB_ = -(-W // 64), -(-H // 32)
-        tc_flops = float(B * T * S_ * NB_) * 48 * (nkx + nky) * 4096   # HMMA m16n8k16 = 4096 flop
+        NB_ = -(-H // 32)
+        if path_t5:
+            # tcgen05: per (frame, 80-column strip, 32-row block): 6 products x (NKY + 8) MMAs of
+            # M=128, N=32, K=16 (131072 flop each) -- y-pass window steps + the 8 x-pass steps
+            nky5 = (32 + RSc + 15) // 16 + (RSc + 15) // 16
+            tc_flops = float(B * T * (-(-W // 80)) * NB_) * TC_PRODUCTS * (nky5 + 8) * 131072
+            kname = (f"spass_tc5_kernel<R={RSc}> (tcgen05.mma kind::f16, operands in TMEM / smem, accumulators in "
+                     f"TMEM; x/y Gaussian as banded Toeplitz products, three bf16 planes x six products per tap "
+                     f"(fp32-class) + F multiplies + norm)")
+            tc_ceiling = float(peaks.get("bf16_tflops", 2250.0))
+        else:
+            ra = (RSc + 3) // 4 * 4
+            nkx, nky = (16 + ra + RSc + 15) // 16, (16 + 2 * RSc + 15) // 16
+            S_ = -(-W // 64)
+            # mma.sync m16n8k16 (4096 flop): 16 x 6 HMMA per k step and warp, 4 warps per 32 x 64 block
+            tc_flops = float(B * T * S_ * NB_) * 16 * TC_PRODUCTS * (nkx + nky) * 4096
+            kname = (f"spass_tc_kernel<R={RSc}> (mma.sync m16n8k16; x/y Gaussian as banded Toeplitz products, "
+                     f"three bf16 planes x six products per tap (fp32-class) + F multiplies + norm)")
+            tc_ceiling = MMA_SYNC_BF16_TFLOPS
         # read v (+ F unless the full operator's plain pass), write p (+ the tape u for training)
         sp_bytes = (8.0 + (0.0 if full else 4.0) + (4.0 if args.config == "c3" else 0.0)) * vox
         bf16_peak = float(peaks.get("bf16_tflops", 2250.0))
@@ -461,8 +479,7 @@ def run_ours(args):
         except Exception:
             tc_traffic = None
         roofline = {
-            "kernel": f"spass_tc_kernel<R={RSc}> (x/y Gaussian as banded bf16x3 Toeplitz products on the "
-                      f"tensor pipe + F multiplies + norm)",
+            "kernel": kname,
             "bound": "hbm", "achieved": sp_bytes / sp_avg_s / 1e9 if sp_n else None, "peak": hbm_peak,
             "unit": "GB/s", "frac": (sp_bytes / sp_avg_s / 1e9 / hbm_peak) if sp_n else None,
             "traffic": tc_traffic,
@@ -474,7 +491,8 @@ def run_ours(args):
                        "achieved_TFLOPs": tc_flops / sp_avg_s / 1e12 if sp_n else None,
                        "peak_bf16_TFLOPs": bf16_peak, "peak_source": f"{peaks_src} bf16_tflops",
                        "frac": (tc_flops / sp_avg_s / 1e12 / bf16_peak) if sp_n else None,
-                       "mma_sync_ceiling_TFLOPs": MMA_SYNC_BF16_TFLOPS,
+                       "instruction_ceiling_TFLOPs": tc_ceiling,
+                       "instruction_frac": (tc_flops / sp_avg_s / 1e12 / tc_ceiling) if sp_n else None,
                        "useful_fp32_TFLOPs": flops_per_launch / sp_avg_s / 1e12 if sp_n else None},
             "tpass": {"launch_ms": tp_avg_s * 1e3, "launches": tp_n,
                       "achieved_GBps": tp_bytes / tp_avg_s / 1e9 if tp_n else None, "peak_GBps": hbm_peak,
@@ -591,6 +609,9 @@ def main():
     ap.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4", "c5", "probe", "c2f"],
                     help="default: c2 at N=1, c5 (time slabs) at N>1, c4 with --shard volume")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "tcgen05", "mma", "fp32"],
+                    help="forward path (sfseg_options.algo): auto, the tcgen05/TMEM spatial pass, the mma.sync "
+                         "one, or the FP32-FMA one")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", type=int, default=1,

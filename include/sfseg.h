@@ -118,6 +118,10 @@ const char* sfseg_last_cuda_error(void);
 #define SFSEG_ALGO_AUTO 0
 #define SFSEG_ALGO_TWO_PASS 1
 #define SFSEG_ALGO_TWO_PASS_FP32 3
+/* the two-pass iteration with the warp-level (mma.sync) tensor-core spatial pass */
+#define SFSEG_ALGO_TWO_PASS_MMA_SYNC 4
+/* the two-pass iteration with the tcgen05 / TMEM spatial pass (spatial radii <= 24; else as TWO_PASS) */
+#define SFSEG_ALGO_TWO_PASS_TCGEN05 5
 typedef struct sfseg_profiler sfseg_profiler;
 typedef struct {
   int32_t n_cont;   /* continuous iterations before binarisation starts (>= 0) */
@@ -305,6 +309,7 @@ sfseg_status sfseg_solve_host_batch(const float* const* ch_host, int32_t n, int3
 #define SFSEG_PATH_TWO_PASS_FP32 0
 #define SFSEG_PATH_TWO_PASS_TC 1
 #define SFSEG_PATH_FUSED_3D 2
+#define SFSEG_PATH_TWO_PASS_TCGEN05 4
 sfseg_status sfseg_forward_path(sfseg_shape shape, sfseg_gauss gauss, int32_t algo, int32_t* info_host /*[3]*/);
 
 /* ---- multi-GPU communicator (NCCL, loaded at run time with dlopen) ---- */

@@ -221,10 +221,13 @@ class Profiler:
 ALGO_AUTO = 0
 ALGO_TWO_PASS = 1
 ALGO_TWO_PASS_FP32 = 3
+ALGO_TWO_PASS_MMA_SYNC = 4
+ALGO_TWO_PASS_TCGEN05 = 5
 
 PATH_TWO_PASS_FP32 = 0
 PATH_TWO_PASS_TC = 1
 PATH_FUSED_3D = 2
+PATH_TWO_PASS_TCGEN05 = 4
 
 
 def _options(algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None, binarize=None) -> OptionsC:

@@ -17,6 +17,9 @@ bool spass_tc_supported(int R);
 int spass_tc_occupancy(int R);
 int spass_tc_boxw(int R);
 cudaError_t launch_spass_tc(int R, const SpassParams& P, int grid, cudaStream_t st);
+// tcgen05 / TMEM spatial pass (spass_tc5.cuh): strips of 80 output columns, 128-column TMA boxes
+bool spass_tc5_supported(int R);
+cudaError_t launch_spass_tc5(int R, const SpassParams& P, int grid, cudaStream_t st);
 bool f3d_supported(int RT, int R);
 int f3d_occupancy(int RT, int R);
 cudaError_t launch_f3d(int RT, int R, const F3dParams& P, int grid, cudaStream_t st);

@@ -28,6 +28,7 @@
 #include "bwd.cuh"
 #include "learn.cuh"
 #include "launch.h"
+#include "spass_tc5.cuh"
 
 using namespace sfseg;
 
@@ -239,6 +240,10 @@ struct Plan {
   int G;              // spass grid
   bool tc;            // forward spatial pass on the tensor cores (spass_tc_kernel)
   int Gtc;            // its grid
+  bool tc5;           // ... on tcgen05 / TMEM (spass_tc5_kernel): 80-column strips
+  int S5;             // its strips
+  int64_t U5;         // its units = BT * S5 * NB
+  int G5;             // its grid (one CTA per SM: all 512 TMEM columns)
   int gx;             // elementwise grid.x per frame
   bool f3d;           // single-pass fused 3D kernel (small radii) for the single-GPU forward
   int TX, TY;         // f3d tiles per frame (64 columns x f3d_th(RS) rows)
@@ -259,7 +264,8 @@ struct Plan {
 };
 
 bool valid_algo(int32_t algo) {
-  return algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_FP32;
+  return algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_FP32 ||
+         algo == SFSEG_ALGO_TWO_PASS_MMA_SYNC || algo == SFSEG_ALGO_TWO_PASS_TCGEN05;
 }
 
 sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan* P,
@@ -305,6 +311,10 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 4));
   P->gx = ew_gx(P->H, P->BT);
   P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
+  P->tc5 = P->tc && algo == SFSEG_ALGO_TWO_PASS_TCGEN05 && spass_tc5_supported(P->RS);
+  P->S5 = (int)((sh.W + k5OW - 1) / k5OW);
+  P->U5 = P->BT * P->S5 * P->NB;
+  P->G5 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(), P->U5));
   P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * spass_tc_occupancy(P->RS), P->U / 4));
   P->f3d = algo == SFSEG_ALGO_AUTO && !P->bin && f3d_supported(P->RT, P->RS);
   P->TX = (int)((sh.W + kF3dTW - 1) / kF3dTW);
@@ -418,9 +428,16 @@ void fill_spass_common(SpassParams& sp, const Plan& P, void* ws) {
 // Forward spatial pass: the tensor-core kernel when the plan selected it, else the FP32 one.
 // Input descriptor of the forward spatial pass over v (box width of the selected kernel).
 bool make_spass_fwd_tmap(CUtensorMap* map, const Plan& P, const float* v) {
+  if (P.tc5) return make_volume_tmap(map, v, P.W, P.H, P.BT, P.Wp, k5Lanes, k5NR);
   return make_volume_tmap(map, v, P.W, P.H, P.BT, P.Wp, P.tc ? spass_tc_boxw(P.RS) : spass_boxw(P.RS));
 }
 cudaError_t launch_spass_forward(const Plan& P, SpassParams& sp, cudaStream_t st) {
+  if (P.tc5) {
+    sp.S = P.S5;
+    sp.U = P.U5;
+    sp.G = P.G5;
+    return launch_spass_tc5(P.RS, sp, P.G5, st);
+  }
   if (P.tc) {
     sp.G = P.Gtc;
     return launch_spass_tc(P.RS, sp, P.Gtc, st);
@@ -733,7 +750,8 @@ sfseg_status sfseg_forward_path(sfseg_shape sh, sfseg_gauss g, int32_t algo, int
   const sfseg_options opt{algo, nullptr};
   sfseg_status s = make_plan(sh, 1, g, 1, &P, &opt);
   if (s != SFSEG_OK) return s;
-  info[0] = P.f3d ? SFSEG_PATH_FUSED_3D : P.tc ? SFSEG_PATH_TWO_PASS_TC : SFSEG_PATH_TWO_PASS_FP32;
+  info[0] = P.f3d ? SFSEG_PATH_FUSED_3D : P.tc5 ? SFSEG_PATH_TWO_PASS_TCGEN05 : P.tc ? SFSEG_PATH_TWO_PASS_TC
+                                                                               : SFSEG_PATH_TWO_PASS_FP32;
   info[1] = P.RT;
   info[2] = P.RS;
   return SFSEG_OK;
