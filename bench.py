@@ -454,10 +454,9 @@ def run_ours(args):
         RSc = path_info[2]
         NB_ = -(-H // 32)
         if path_t5:
-            # tcgen05: per (frame, 80-column strip, 32-row block): 6 products x (NKY + 8) MMAs of
-            # M=128, N=32, K=16 (131072 flop each) -- y-pass window steps + the 8 x-pass steps
-            nky5 = (32 + RSc + 15) // 16 + (RSc + 15) // 16
-            tc_flops = float(B * T * (-(-W // 80)) * NB_) * TC_PRODUCTS * (nky5 + 8) * 131072
+            # per (frame, 80-column strip, 64-row block): 6 products x (NKY + 8) MMAs, M=128 N=64 K=16
+            nky5 = (64 + RSc + 15) // 16 + (RSc + 15) // 16
+            tc_flops = float(B * T * (-(-W // 80)) * (-(-H // 64))) * TC_PRODUCTS * (nky5 + 8) * 262144
             kname = (f"spass_tc5_kernel<R={RSc}> (tcgen05.mma kind::f16, operands in TMEM / smem, accumulators in "
                      f"TMEM; x/y Gaussian as banded Toeplitz products, three bf16 planes x six products per tap "
                      f"(fp32-class) + F multiplies + norm)")

@@ -242,7 +242,8 @@ struct Plan {
   int Gtc;            // its grid
   bool tc5;           // ... on tcgen05 / TMEM (spass_tc5_kernel): 80-column strips
   int S5;             // its strips
-  int64_t U5;         // its units = BT * S5 * NB
+  int NB5;            // its 64-row blocks per column
+  int64_t U5;         // its units = BT * S5 * NB5
   int G5;             // its grid (one CTA per SM: all 512 TMEM columns)
   int gx;             // elementwise grid.x per frame
   bool f3d;           // single-pass fused 3D kernel (small radii) for the single-GPU forward
@@ -313,7 +314,8 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
   P->tc5 = P->tc && algo == SFSEG_ALGO_TWO_PASS_TCGEN05 && spass_tc5_supported(P->RS);
   P->S5 = (int)((sh.W + k5OW - 1) / k5OW);
-  P->U5 = P->BT * P->S5 * P->NB;
+  P->NB5 = (int)((sh.H + k5NR - 1) / k5NR);
+  P->U5 = P->BT * P->S5 * P->NB5;
   P->G5 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(), P->U5));
   P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * spass_tc_occupancy(P->RS), P->U / 4));
   P->f3d = algo == SFSEG_ALGO_AUTO && !P->bin && f3d_supported(P->RT, P->RS);
@@ -428,12 +430,13 @@ void fill_spass_common(SpassParams& sp, const Plan& P, void* ws) {
 // Forward spatial pass: the tensor-core kernel when the plan selected it, else the FP32 one.
 // Input descriptor of the forward spatial pass over v (box width of the selected kernel).
 bool make_spass_fwd_tmap(CUtensorMap* map, const Plan& P, const float* v) {
-  if (P.tc5) return make_volume_tmap(map, v, P.W, P.H, P.BT, P.Wp, k5Lanes, k5NR);
+  if (P.tc5) return make_volume_tmap(map, v, P.W, P.H, P.BT, P.Wp, k5Lanes, k5IR);
   return make_volume_tmap(map, v, P.W, P.H, P.BT, P.Wp, P.tc ? spass_tc_boxw(P.RS) : spass_boxw(P.RS));
 }
 cudaError_t launch_spass_forward(const Plan& P, SpassParams& sp, cudaStream_t st) {
   if (P.tc5) {
     sp.S = P.S5;
+    sp.NB = P.NB5;
     sp.U = P.U5;
     sp.G = P.G5;
     return launch_spass_tc5(P.RS, sp, P.G5, st);
