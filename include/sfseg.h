@@ -319,7 +319,10 @@ sfseg_status sfseg_forward_path(sfseg_shape shape, sfseg_gauss gauss, int32_t al
  * are the rank's LOCAL slab [B][C][T_local][H][W] / [B][T_local][H][W].
  * Workspace from sfseg_workspace_bytes(..., dist, ...).  Every iteration:
  * r_t-frame halo send/recv with ranks +-1 and an fp64 allreduce of the norm
- * partials (NCCL, enqueued on `stream`).  Tape / F_out: SFSEG_ERR_UNSUPPORTED.
+ * partials (NCCL, enqueued on `stream`).  With a tape (each rank its own: nu_k global, u_k of
+ * its frames) sfseg_power_iterate_backward with the same sfseg_dist runs the time-slab backward
+ * (halo of F y_bar_k per step, allreduces of the step scalars and of dw, db; x_0 = F, no
+ * binarisation).  F_out / binarisation: SFSEG_ERR_UNSUPPORTED.
  * 128-byte NCCL unique id into id_host (call on rank 0, broadcast it). */
 sfseg_status sfseg_get_unique_id(uint8_t id_host[128]);
 sfseg_status sfseg_comm_create(const uint8_t id_host[128], int32_t nranks, int32_t rank,
@@ -337,8 +340,22 @@ sfseg_status sfseg_slabs_workspace_bytes(sfseg_shape shape, int32_t C, sfseg_gau
 sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* w_host, float b,
                                        int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
                                        int32_t nslabs, const float* x0_or_null, float* x_out,
-                                       double* stats_or_null, int32_t want_rayleigh, void* ws,
-                                       size_t ws_bytes, const sfseg_options* opt_or_null, void* stream);
+                                       double* stats_or_null, int32_t want_rayleigh,
+                                       void* tape_or_null, void* ws, size_t ws_bytes,
+                                       const sfseg_options* opt_or_null, void* stream);
+/* Tape of the emulated slabs (one per slab, concatenated) and the time-slab BACKWARD emulated
+ * the same way (per step an r_t-frame halo of F y_bar_k exchanged with
+ * the neighbour slabs, an allreduce of <x_{k-1}, x_bar_{k-1}>, and a final allreduce of the C + 1
+ * weight-gradient sums): the per-rank phases of sfseg_power_iterate_backward with a
+ * sfseg_dist.  x_0 = F only, no binarisation (SFSEG_ERR_UNSUPPORTED).  Syncs (host outputs). */
+sfseg_status sfseg_slabs_tape_bytes(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K, int32_t nslabs,
+                                    size_t* tape_bytes_host);
+sfseg_status sfseg_power_iterate_slabs_backward(const float* ch, int32_t C, const float* w_host, float b,
+                                                int32_t act, sfseg_shape shape, sfseg_gauss gauss, int32_t K,
+                                                int32_t nslabs, const void* tape, const float* dL_dx,
+                                                double* dL_dw_host, double* dL_db_host, void* ws,
+                                                size_t ws_bytes, const sfseg_options* opt_or_null,
+                                                void* stream);
 /* Syncs `stream`; returns the first device-detected error of any slab. */
 sfseg_status sfseg_slabs_sync_status(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K,
                                      int32_t nslabs, void* ws, void* stream);

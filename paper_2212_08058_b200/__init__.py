@@ -123,7 +123,11 @@ _SIGS = {
                                            _P, _P, _P, C.c_size_t, _P, _P]),
     "sfseg_slabs_workspace_bytes": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
     "sfseg_power_iterate_slabs": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC, C.c_int32,
-                                            C.c_int32, _P, _P, _P, C.c_int32, _P, C.c_size_t, _P, _P]),
+                                            C.c_int32, _P, _P, _P, C.c_int32, _P, _P, C.c_size_t, _P, _P]),
+    "sfseg_slabs_tape_bytes": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P]),
+    "sfseg_power_iterate_slabs_backward": (C.c_int, [_P, C.c_int32, _P, C.c_float, C.c_int32, Shape, GaussC,
+                                                     C.c_int32, C.c_int32, _P, _P, _P, _P, _P, C.c_size_t, _P,
+                                                     _P]),
     "sfseg_slabs_sync_status": (C.c_int, [Shape, C.c_int32, GaussC, C.c_int32, C.c_int32, _P, _P]),
     "sfseg_get_unique_id": (C.c_int, [_P]),
     "sfseg_comm_create": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P]),
@@ -384,9 +388,10 @@ def power_iterate_backward(ch, w, gauss: Gauss, K: int, dL_dx, b: float = 0.0, a
 
 def power_iterate_slabs(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, b: float = 0.0,
                         act: int = ACT_IDENTITY, x0=None, want_rayleigh: bool = False, stream=None,
-                        algo: int = ALGO_AUTO):
+                        algo: int = ALGO_AUTO, want_tape: bool = False):
     """Time-slab decomposition of the solve emulated on ONE GPU (sfseg_power_iterate_slabs):
-    the per-rank phases of the multi-GPU path with in-process halo copies and reduction."""
+    the per-rank phases of the multi-GPU path with in-process halo copies and reduction.
+    Returns (x, stats) or, with want_tape, (x, stats, tape) for power_iterate_slabs_backward."""
     _require(ch, "ch", 5)
     B, Cn, T, H, W = ch.shape
     shp, g = Shape(B, T, H, W), gauss.c()
@@ -395,17 +400,44 @@ def power_iterate_slabs(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, 
            "sfseg_slabs_workspace_bytes")
     ws = torch.zeros(max(n.value, 256), dtype=torch.uint8, device=ch.device)  # every slab header zeroed
     nsl = int(nslabs)
+    tape = None
+    if want_tape:
+        tb = C.c_size_t(0)
+        _check(lib().sfseg_slabs_tape_bytes(shp, Cn, g, int(K), nsl, C.byref(tb)), "sfseg_slabs_tape_bytes")
+        tape = _alloc_bytes(tb.value, ch.device)
     x = torch.empty((B, T, H, W), dtype=torch.float32, device=ch.device)
     stats = torch.zeros((B, int(K), 3), dtype=torch.float64, device=ch.device)
     if x0 is not None:
         _require(x0, "x0", 4, shape=(B, T, H, W), device=ch.device)
     _check(lib().sfseg_power_iterate_slabs(_ptr(ch), Cn, _weights(w, Cn), float(b), int(act), shp, g, int(K),
-                                           nsl, _ptr(x0), _ptr(x), _ptr(stats), int(want_rayleigh),
+                                           nsl, _ptr(x0), _ptr(x), _ptr(stats), int(want_rayleigh), _ptr(tape),
                                            _ptr(ws), n.value, C.byref(_options(algo)), _stream(stream)),
            "sfseg_power_iterate_slabs")
     _check(lib().sfseg_slabs_sync_status(shp, Cn, g, int(K), nsl, _ptr(ws), _stream(stream)),
            "sfseg_power_iterate_slabs (device)")
-    return x, stats
+    return (x, stats, tape) if want_tape else (x, stats)
+
+
+def power_iterate_slabs_backward(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, tape: torch.Tensor,
+                                 dL_dx: torch.Tensor, b: float = 0.0, act: int = ACT_IDENTITY, stream=None,
+                                 algo: int = ALGO_AUTO):
+    """The time-slab backward emulated on ONE GPU (sfseg_power_iterate_slabs_backward) on the tape
+    of power_iterate_slabs(want_tape=True).  Returns (dw, db)."""
+    _require(ch, "ch", 5)
+    B, Cn, T, H, W = ch.shape
+    _require(dL_dx, "dL_dx", 4, shape=(B, T, H, W), device=ch.device)
+    shp, g = Shape(B, T, H, W), gauss.c()
+    n = C.c_size_t(0)
+    _check(lib().sfseg_slabs_workspace_bytes(shp, Cn, g, int(K), int(nslabs), C.byref(n)),
+           "sfseg_slabs_workspace_bytes")
+    ws = torch.zeros(max(n.value, 256), dtype=torch.uint8, device=ch.device)
+    dw = (C.c_double * Cn)()
+    db = C.c_double(0.0)
+    _check(lib().sfseg_power_iterate_slabs_backward(_ptr(ch), Cn, _weights(w, Cn), float(b), int(act), shp, g,
+                                                    int(K), int(nslabs), _ptr(tape), _ptr(dL_dx), dw, C.byref(db),
+                                                    _ptr(ws), n.value, C.byref(_options(algo)), _stream(stream)),
+           "sfseg_power_iterate_slabs_backward")
+    return [dw[i] for i in range(Cn)], db.value
 
 
 def threshold(x: torch.Tensor, tau: float, mode: int = THR_PER_FRAME_MAX) -> torch.Tensor:

@@ -33,6 +33,7 @@ struct BwdEpiParams {
   unsigned* counter;
   const double* tape_bin;  // [B][K][2] (theta in x units, n_pos) of the binarised iterations
   float kappa_prev;        // steepness of iteration k-1 (0: not binarised)
+  double* loc;             // time slabs: per-volume local sums [B][2] (finalized after the allreduce)
   int B, T, H, W, Wp, gx, K, k;
 };
 
@@ -104,7 +105,13 @@ __global__ void __launch_bounds__(kEwThreads) bwd_epi_kernel(const __grid_consta
   if (!last_block_arrive(P.counter, gridDim.x * gridDim.y, &flag)) return;
   for (int v = 0; v < P.B; ++v) {
     const double tot = block_sum_array<kEwThreads>(P.partials + (long)v * nper, nper, 1, red);
-    if (bin) {
+    if (P.loc) {
+      const double sg = bin ? block_sum_array<kEwThreads>(P.partials + (long)(P.B + v) * nper, nper, 1, red) : 0.0;
+      if (threadIdx.x == 0) {
+        P.loc[2 * v] = tot;
+        P.loc[2 * v + 1] = sg;
+      }
+    } else if (bin) {
       const double sg = block_sum_array<kEwThreads>(P.partials + (long)(P.B + v) * nper, nper, 1, red);
       if (threadIdx.x == 0) {
         const double* tb = P.tape_bin + ((long)v * P.K + (P.k - 2)) * 2;
@@ -115,6 +122,27 @@ __global__ void __launch_bounds__(kEwThreads) bwd_epi_kernel(const __grid_consta
     }
   }
   if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+// Time slabs: the bwd_epi finalize from the allreduced sums glob[B][2].
+struct BwdStepFinParams {
+  const double* glob;
+  double* sc;
+  const double* tape_nu;
+  const double* tape_bin;
+  float kappa_prev;
+  int B, K, k;
+};
+__global__ void bwd_step_finalize_kernel(const __grid_constant__ BwdStepFinParams P) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= P.B) return;
+  const double tot = P.glob[2 * v], sg = P.glob[2 * v + 1];
+  if (P.kappa_prev > 0.f) {
+    const double* tb = P.tape_bin + ((long)v * P.K + (P.k - 2)) * 2;
+    bwd_finalize(P.sc + v * kScal, P.tape_nu, P.K, P.k, v, tot - tb[0] * sg, tb[1] > 0.0 ? sg / tb[1] : 0.0);
+  } else {
+    bwd_finalize(P.sc + v * kScal, P.tape_nu, P.K, P.k, v, tot);
+  }
 }
 
 }  // namespace sfseg

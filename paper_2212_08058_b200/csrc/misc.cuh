@@ -286,7 +286,9 @@ struct BwdInitParams {
   unsigned* counter;
   const double* tape_bin;  // [B][K][2] of the binarised iterations (row f2)
   float kappa;             // steepness of iteration K (0: not binarised; then g is dL/dx_K)
+  double* loc;             // time slabs: per-volume local sums [B][2] (finalized after the allreduce)
   int B, T, H, W, Wp, K, gx;
+  int g_T, g_t0;           // dL/dx buffer frames per volume and this slab's first frame in it
 };
 
 // x_bar_K = dL/dx_K, c_K = <x_K, x_bar_K>.  When iteration K was soft-binarised the output is
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_const
   const int bt = blockIdx.y;
   const int b = bt / P.T, t = bt - b * P.T;
   const long HWp = (long)P.H * P.Wp, HW = (long)P.H * P.W;
-  const float* gf = P.g + ((long)b * P.T + t) * HW;
+  const float* gf = P.g + ((long)b * P.g_T + P.g_t0 + t) * HW;
   const bool bin = P.kappa > 0.f;
   const float inv_nuK = (float)(1.0 / P.tape_nu[(long)b * P.K + (P.K - 1)]);
   const float theta = bin ? (float)P.tape_bin[((long)b * P.K + (P.K - 1)) * 2] : 0.f;
@@ -347,7 +349,10 @@ __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_const
   for (int bb = 0; bb < P.B; ++bb) {
     const double tot = block_sum_array<kEwThreads>(P.partials + (long)bb * nper, nper, 1, red);
     const double sg = bin ? block_sum_array<kEwThreads>(P.partials + (long)(P.B + bb) * nper, nper, 1, red) : 0.0;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && P.loc) {
+      P.loc[2 * bb] = tot;
+      P.loc[2 * bb + 1] = sg;
+    } else if (threadIdx.x == 0) {
       const double nuK = P.tape_nu[(long)bb * P.K + (P.K - 1)];
       if (bin) {
         // c_K = <x_K, g - [x_K > 0] corr> = sum(x g) - theta sum(g); cn = c_K / nu_K
@@ -366,6 +371,61 @@ __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_const
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
+// Time slabs: the bwd_init finalize from the allreduced sums glob[B][2] = (sum(x g) or
+// sum(g F u_{K-1}), sum(g) of a binarised iteration K).
+struct BwdInitFinParams {
+  const double* glob;
+  double* sc;
+  const double* tape_nu;
+  const double* tape_bin;
+  float kappa;
+  int B, K;
+};
+__global__ void bwd_init_finalize_kernel(const __grid_constant__ BwdInitFinParams P) {
+  const int bb = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bb >= P.B) return;
+  const double tot = P.glob[2 * bb], sg = P.glob[2 * bb + 1];
+  const double nuK = P.tape_nu[(long)bb * P.K + (P.K - 1)];
+  if (P.kappa > 0.f) {
+    const double* tb = P.tape_bin + ((long)bb * P.K + (P.K - 1)) * 2;
+    P.sc[bb * kScal + SC_CN] = (tot - tb[0] * sg) / nuK;
+    P.sc[bb * kScal + SC_CORR] = tb[1] > 0.0 ? sg / tb[1] : 0.0;
+  } else {
+    P.sc[bb * kScal + SC_CN] = tot / (nuK * nuK);
+    P.sc[bb * kScal + SC_CORR] = 0.0;
+  }
+  P.sc[bb * kScal + SC_INV_NU] = 1.0 / nuK;
+  P.sc[bb * kScal + SC_INV_NU_PREV] = (P.K >= 2) ? 1.0 / P.tape_nu[(long)bb * P.K + (P.K - 2)] : 0.0;
+}
+
+// Time slabs, backward halos: the temporal pass of backward step k at a slab boundary needs
+// the neighbour's F y_bar_k on r_t frames (tpass TP_BWD reads halos pre-multiplied).  This
+// kernel forms F y_bar_k = F (x_bar_k - [F u_{k-1} > 0] corr - F u_{k-1} cn) inv_nu on the
+// first and last RT frames of every volume into send_lo / send_hi [B][RT][H][Wp].
+struct BwdHaloParams {
+  const float* xbar;
+  const float* F;
+  const float* u1;
+  const double* sc;
+  float* send_lo;
+  float* send_hi;
+  long frame;   // H * Wp
+  int T, RT;
+};
+__global__ void __launch_bounds__(kEwThreads) bwd_halo_kernel(const __grid_constant__ BwdHaloParams P) {
+  const int b = blockIdx.z, j = blockIdx.y;   // j < RT: first frames (send_lo), else last frames (send_hi)
+  const bool hi = j >= P.RT;
+  const int t = hi ? P.T - 2 * P.RT + j : j;
+  const float cn = (float)P.sc[b * kScal + SC_CN], inv_nu = (float)P.sc[b * kScal + SC_INV_NU];
+  const float corr = (float)P.sc[b * kScal + SC_CORR];
+  const long src = ((long)b * P.T + t) * P.frame;
+  float* dst = (hi ? P.send_hi : P.send_lo) + ((long)b * P.RT + (hi ? j - P.RT : j)) * P.frame;
+  for (long e = (long)blockIdx.x * kEwThreads + threadIdx.x; e < P.frame; e += (long)gridDim.x * kEwThreads) {
+    const float f = P.F[src + e], fu = f * P.u1[src + e];
+    dst[e] = f * ((P.xbar[src + e] - (fu > 0.f ? corr : 0.f) - fu * cn) * inv_nu);
+  }
+}
+
 // ------------------------------------------------------------------ backward contraction dw, db
 struct ContractParams {
   const float* ch;      // dense [B][C][T][H][W]
@@ -375,6 +435,7 @@ struct ContractParams {
   double* out;          // [C+1] : dw_0..dw_{C-1}, db
   unsigned* counter;
   int B, C, T, H, W, Wp, act;
+  int in_T, in_t0;      // channel buffer frames per volume and this slab's first frame in it
   float bias;
   float w[kMaxC];
 };
@@ -389,8 +450,8 @@ __global__ void __launch_bounds__(kEwThreads) contract_kernel(const __grid_const
   for (int c = 0; c <= CMAX; ++c) acc[c] = 0.0;
   const int bt = blockIdx.y;
   const int b = bt / P.T, t = bt - b * P.T;
-  const long HW = (long)P.H * P.W, vol = (long)P.T * HW, HWp = (long)P.H * P.Wp;
-  const float* chf = P.ch + (long)b * P.C * vol + (long)t * HW;
+  const long HW = (long)P.H * P.W, vol = (long)P.in_T * HW, HWp = (long)P.H * P.Wp;
+  const float* chf = P.ch + (long)b * P.C * vol + (long)(P.in_t0 + t) * HW;
   for (int y = blockIdx.x; y < P.H; y += gridDim.x) {
 #pragma unroll 2
     for (int x = threadIdx.x; x < P.W; x += kEwThreads) {

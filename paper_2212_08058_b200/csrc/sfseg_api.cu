@@ -475,17 +475,23 @@ bool finite_weights(const float* w, int C, float b) {
 // one GPU (halo copies + a rank-ordered reduction kernel) used to test the
 // decomposition on a single device.
 struct SlabOffsets {
-  size_t off_hlo, off_hhi, off_loc, off_glob, total;
+  size_t off_hlo, off_hhi, off_slo, off_shi, off_loc, off_glob, total;
 };
+// after the single-GPU backward region (x_bar, F_bar, x_0): receive halos, send halos (backward),
+// local / global sums (2 per volume, or the C + 1 weight-gradient sums)
 SlabOffsets slab_offsets(const Plan& P) {
   SlabOffsets o;
-  size_t off = P.ws_fwd;
+  size_t off = P.ws_bwd;
   const size_t hb = align_up(sizeof(float) * (size_t)P.B * P.RT * P.H * P.Wp);
   o.off_hlo = off;
   off += hb;
   o.off_hhi = off;
   off += hb;
-  const size_t lb = align_up(sizeof(double) * 2 * P.B);
+  o.off_slo = off;
+  off += hb;
+  o.off_shi = off;
+  off += hb;
+  const size_t lb = align_up(sizeof(double) * std::max<size_t>(2 * (size_t)P.B, (size_t)kMaxC + 1));
   o.off_loc = off;
   off += lb;
   o.off_glob = off;
@@ -503,6 +509,7 @@ struct Rank {
   int out_T = 0, out_t0 = 0;
   double* stats = nullptr;
   int rayleigh = 0;
+  void* tape = nullptr;     // this rank's tape (nu_k global, u_k local frames) or null
   void* ws = nullptr;
   SlabOffsets so;
   bool has_lo = false, has_hi = false;
@@ -528,6 +535,7 @@ sfseg_status rank_setup(Rank& r, cudaStream_t st) {
   fill_spass_common(r.sp, P, r.ws);
   r.sp.stats = r.stats;
   r.sp.loc = r.loc;
+  r.sp.tape_nu = nullptr;   // nu_k is written by the post-allreduce finalize
   std::memset(&r.tp, 0, sizeof(r.tp));
   fill_tpass_common(r.tp, P, r.ws);
   r.tp.src = r.p;
@@ -556,7 +564,7 @@ sfseg_status ph_finalize(Rank& r, int k, cudaStream_t st) {
   fp.glob = r.glob;
   fp.sc = at<double>(r.ws, r.P.off_sc);
   fp.stats = r.stats;
-  fp.tape_nu = nullptr;
+  fp.tape_nu = (k >= 1 && r.tape) ? static_cast<double*>(r.tape) : nullptr;
   fp.err = &at<WsHeader>(r.ws, 0)->err;
   fp.B = (int)r.P.B;
   fp.K = r.P.K;
@@ -577,6 +585,9 @@ sfseg_status ph_T(Rank& r, cudaStream_t st) {
 sfseg_status ph_S(Rank& r, int k, cudaStream_t st) {
   r.sp.out = r.p;
   r.sp.pprev = r.rayleigh ? r.p : nullptr;
+  r.sp.tape_u = r.tape ? reinterpret_cast<float*>(static_cast<char*>(r.tape) + r.P.tape_hdr_bytes +
+                                                 (size_t)(k - 1) * align_up(sizeof(float) * (size_t)r.P.vol_elems))
+                       : nullptr;
   r.sp.k = k;
   r.sp.last = (k == r.P.K) ? 1 : 0;
   ProfScope ps(r.P.prof, st, PC_SPASS);
@@ -616,8 +627,8 @@ sfseg_status nccl_exchange(Rank& r, sfseg_comm* c, cudaStream_t st) {
   return SFSEG_OK;
 }
 
-sfseg_status nccl_allreduce(Rank& r, sfseg_comm* c, cudaStream_t st) {
-  if (nccl().AllReduce(r.loc, r.glob, 2 * (size_t)r.P.B, ncclFloat64, ncclSum, c->comm, st) != ncclSuccess)
+sfseg_status nccl_allreduce(Rank& r, sfseg_comm* c, cudaStream_t st, size_t n = 0) {
+  if (nccl().AllReduce(r.loc, r.glob, n ? n : 2 * (size_t)r.P.B, ncclFloat64, ncclSum, c->comm, st) != ncclSuccess)
     return SFSEG_ERR_NCCL;
   return SFSEG_OK;
 }
@@ -643,17 +654,254 @@ sfseg_status local_exchange(std::vector<Rank>& R, cudaStream_t st) {
   return SFSEG_OK;
 }
 
-sfseg_status local_allreduce(std::vector<Rank>& R, cudaStream_t st) {
+sfseg_status local_allreduce(std::vector<Rank>& R, cudaStream_t st, int n = 0) {
   LocalReduceParams lp;
   std::memset(&lp, 0, sizeof(lp));
   lp.nranks = (int)R.size();
-  lp.n = 2 * (int)R[0].P.B;
+  lp.n = n ? n : 2 * (int)R[0].P.B;
   for (int i = 0; i < lp.nranks; ++i) {
     lp.loc[i] = R[i].loc;
     lp.glob[i] = R[i].glob;
   }
   local_allreduce_kernel<<<(unsigned)((lp.n + 127) / 128), 128, 0, st>>>(lp);
   SF_CUDA(after_launch("local_allreduce", st));
+  return SFSEG_OK;
+}
+
+// ---------------------------------------------------------------------- time-slab backward
+// (SURVEY.md §8(e) c2/c3 row): the single-GPU backward's steps (Appendix A) per slab, with
+// (1) the backward temporal pass's r_t-frame halos of F y_bar_k exchanged with ranks +-1
+// before every step (bwd_halo_kernel fills the send buffers), (2) the per-step scalars
+// <x_{k-1}, x_bar_{k-1}> (and the binarisation sums) allreduced before their finalize, and
+// (3) the C + 1 weight-gradient sums allreduced at the end.
+struct BwdRank {
+  Rank* r = nullptr;
+  const float* g = nullptr;   // dL/dx buffer [B][g_T][H][W]
+  int g_T = 0, g_t0 = 0;
+  float* xbar = nullptr;
+  float* Fbar = nullptr;
+  float* ubuf = nullptr;
+  float* slo = nullptr;
+  float* shi = nullptr;
+  SpassParams sp;
+  TpassParams tp;
+  BwdEpiParams be;
+};
+
+const float* slab_tape_u(const Rank& r, int i) {
+  return reinterpret_cast<const float*>(static_cast<const char*>(r.tape) + r.P.tape_hdr_bytes +
+                                        (size_t)i * align_up(sizeof(float) * (size_t)r.P.vol_elems));
+}
+
+sfseg_status bw_setup(BwdRank& q, cudaStream_t st) {
+  Rank& r = *q.r;
+  const Plan& P = r.P;
+  q.xbar = at<float>(r.ws, P.off_xbar);
+  q.Fbar = at<float>(r.ws, P.off_Fbar);
+  q.ubuf = at<float>(r.ws, P.off_p2);
+  q.slo = at<float>(r.ws, r.so.off_slo);
+  q.shi = at<float>(r.ws, r.so.off_shi);
+  std::memset(&q.sp, 0, sizeof(q.sp));
+  if (!make_spass_fwd_tmap(&q.sp.tmap, P, r.v)) return SFSEG_ERR_CUDA;
+  fill_spass_common(q.sp, P, r.ws);
+  q.sp.plain = 1;
+  q.sp.out = q.ubuf;
+  std::memset(&q.tp, 0, sizeof(q.tp));
+  fill_tpass_common(q.tp, P, r.ws);
+  q.tp.src = q.xbar;
+  q.tp.F = r.F;
+  q.tp.out = r.v;
+  q.tp.halo_lo = r.has_lo ? r.hlo : nullptr;
+  q.tp.halo_hi = r.has_hi ? r.hhi : nullptr;
+  std::memset(&q.be, 0, sizeof(q.be));
+  q.be.u = q.ubuf;
+  q.be.F = r.F;
+  q.be.xbar = q.xbar;
+  q.be.Fbar = q.Fbar;
+  q.be.sc = at<double>(r.ws, P.off_sc);
+  q.be.tape_nu = static_cast<const double*>(r.tape);
+  q.be.tape_bin = reinterpret_cast<const double*>(static_cast<const char*>(r.tape) + P.tape_nu_bytes);
+  q.be.partials = at<double>(r.ws, P.off_part);
+  q.be.counter = &at<WsHeader>(r.ws, 0)->counter[0];
+  q.be.loc = r.loc;
+  q.be.B = (int)P.B;
+  q.be.T = (int)P.T;
+  q.be.H = (int)P.H;
+  q.be.W = (int)P.W;
+  q.be.Wp = (int)P.Wp;
+  q.be.gx = P.gx;
+  q.be.K = P.K;
+  return SFSEG_OK;
+}
+
+sfseg_status bw_init(BwdRank& q, cudaStream_t st) {
+  Rank& r = *q.r;
+  const Plan& P = r.P;
+  BwdInitParams ip;
+  std::memset(&ip, 0, sizeof(ip));
+  ip.g = q.g;
+  ip.F = r.F;
+  ip.uK1 = slab_tape_u(r, P.K - 1);
+  ip.xbar = q.xbar;
+  ip.Fbar = q.Fbar;
+  ip.tape_nu = static_cast<const double*>(r.tape);
+  ip.tape_bin = q.be.tape_bin;
+  ip.sc = at<double>(r.ws, P.off_sc);
+  ip.partials = at<double>(r.ws, P.off_part);
+  ip.counter = &at<WsHeader>(r.ws, 0)->counter[2];
+  ip.loc = r.loc;
+  ip.B = (int)P.B;
+  ip.T = (int)P.T;
+  ip.H = (int)P.H;
+  ip.W = (int)P.W;
+  ip.Wp = (int)P.Wp;
+  ip.K = P.K;
+  ip.gx = P.gx;
+  ip.g_T = q.g_T;
+  ip.g_t0 = q.g_t0;
+  bwd_init_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ip);
+  SF_CUDA(after_launch("bwd_init(slab)", st));
+  return SFSEG_OK;
+}
+
+sfseg_status bw_init_fin(BwdRank& q, cudaStream_t st) {
+  Rank& r = *q.r;
+  BwdInitFinParams fp;
+  fp.glob = r.glob;
+  fp.sc = at<double>(r.ws, r.P.off_sc);
+  fp.tape_nu = static_cast<const double*>(r.tape);
+  fp.tape_bin = q.be.tape_bin;
+  fp.kappa = 0.f;
+  fp.B = (int)r.P.B;
+  fp.K = r.P.K;
+  bwd_init_finalize_kernel<<<(unsigned)((r.P.B + 127) / 128), 128, 0, st>>>(fp);
+  SF_CUDA(after_launch("bwd_init_finalize", st));
+  return SFSEG_OK;
+}
+
+sfseg_status bw_halo(BwdRank& q, int k, cudaStream_t st) {
+  Rank& r = *q.r;
+  const Plan& P = r.P;
+  if (!(r.has_lo || r.has_hi) || P.RT == 0) return SFSEG_OK;
+  BwdHaloParams hp;
+  hp.xbar = q.xbar;
+  hp.F = r.F;
+  hp.u1 = slab_tape_u(r, k - 1);
+  hp.sc = at<double>(r.ws, P.off_sc);
+  hp.send_lo = q.slo;
+  hp.send_hi = q.shi;
+  hp.frame = P.H * P.Wp;
+  hp.T = (int)P.T;
+  hp.RT = P.RT;
+  bwd_halo_kernel<<<dim3(8, (unsigned)(2 * P.RT), (unsigned)P.B), kEwThreads, 0, st>>>(hp);
+  SF_CUDA(after_launch("bwd_halo", st));
+  return SFSEG_OK;
+}
+
+sfseg_status bw_step(BwdRank& q, int k, cudaStream_t st) {
+  Rank& r = *q.r;
+  const Plan& P = r.P;
+  q.tp.u1 = slab_tape_u(r, k - 1);
+  {
+    ProfScope ps(P.prof, st, PC_BWD);
+    SF_CUDA(launch_tpass_bwd(P.RT, q.tp, (int)P.B, st));
+    SF_CUDA(after_launch("tpass_bwd(slab)", st));
+  }
+  q.sp.k = k;
+  {
+    ProfScope ps(P.prof, st, PC_BWD);
+    SF_CUDA(launch_spass_forward(P, q.sp, st));
+    SF_CUDA(after_launch("spass(plain, slab bwd)", st));
+  }
+  q.be.u1 = slab_tape_u(r, k - 1);
+  q.be.u2 = k >= 2 ? slab_tape_u(r, k - 2) : nullptr;
+  q.be.k = k;
+  q.be.kappa_prev = 0.f;
+  {
+    ProfScope ps(P.prof, st, PC_BWD);
+    bwd_epi_kernel<<<dim3((unsigned)P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(q.be);
+    SF_CUDA(after_launch("bwd_epi(slab)", st));
+  }
+  return SFSEG_OK;
+}
+
+sfseg_status bw_step_fin(BwdRank& q, int k, cudaStream_t st) {
+  Rank& r = *q.r;
+  BwdStepFinParams fp;
+  fp.glob = r.glob;
+  fp.sc = at<double>(r.ws, r.P.off_sc);
+  fp.tape_nu = static_cast<const double*>(r.tape);
+  fp.tape_bin = q.be.tape_bin;
+  fp.kappa_prev = 0.f;
+  fp.B = (int)r.P.B;
+  fp.K = r.P.K;
+  fp.k = k;
+  bwd_step_finalize_kernel<<<(unsigned)((r.P.B + 127) / 128), 128, 0, st>>>(fp);
+  SF_CUDA(after_launch("bwd_step_finalize", st));
+  return SFSEG_OK;
+}
+
+// dw, db of this slab into loc[0..C] (the caller allreduces them into glob)
+sfseg_status bw_contract(BwdRank& q, const float* w_host, float b, int act, cudaStream_t st) {
+  Rank& r = *q.r;
+  const Plan& P = r.P;
+  ContractParams cc;
+  std::memset(&cc, 0, sizeof(cc));
+  cc.ch = r.ch;
+  cc.Fbar = q.Fbar;
+  cc.xbar0 = q.xbar;   // x_0 = F
+  cc.partials = at<double>(r.ws, P.off_part);
+  cc.out = r.loc;
+  cc.counter = &at<WsHeader>(r.ws, 0)->counter[3];
+  cc.B = (int)P.B;
+  cc.C = P.C;
+  cc.T = (int)P.T;
+  cc.H = (int)P.H;
+  cc.W = (int)P.W;
+  cc.Wp = (int)P.Wp;
+  cc.in_T = r.in_T;
+  cc.in_t0 = r.in_t0;
+  cc.act = act;
+  cc.bias = b;
+  for (int c = 0; c < P.C; ++c) cc.w[c] = w_host[c];
+  const dim3 G2((unsigned)P.gx, (unsigned)P.BT);
+  const int C = P.C;
+  if (C <= 1) contract_kernel<1><<<G2, kEwThreads, 0, st>>>(cc);
+  else if (C <= 2) contract_kernel<2><<<G2, kEwThreads, 0, st>>>(cc);
+  else if (C <= 4) contract_kernel<4><<<G2, kEwThreads, 0, st>>>(cc);
+  else if (C <= 8) contract_kernel<8><<<G2, kEwThreads, 0, st>>>(cc);
+  else if (C <= 16) contract_kernel<16><<<G2, kEwThreads, 0, st>>>(cc);
+  else contract_kernel<kMaxC><<<G2, kEwThreads, 0, st>>>(cc);
+  SF_CUDA(after_launch("contract(slab)", st));
+  return SFSEG_OK;
+}
+
+// in-process halo exchange of the backward send buffers (emulated ranks)
+sfseg_status local_bwd_exchange(std::vector<Rank>& R, std::vector<BwdRank>& Q, cudaStream_t st) {
+  for (size_t i = 0; i < R.size(); ++i) {
+    const Plan& P = R[i].P;
+    const size_t n = sizeof(float) * (size_t)P.B * P.RT * P.H * P.Wp;
+    if (R[i].has_lo) SF_CUDA(cudaMemcpyAsync(R[i].hlo, Q[i - 1].shi, n, cudaMemcpyDeviceToDevice, st));
+    if (R[i].has_hi) SF_CUDA(cudaMemcpyAsync(R[i].hhi, Q[i + 1].slo, n, cudaMemcpyDeviceToDevice, st));
+  }
+  return SFSEG_OK;
+}
+
+sfseg_status nccl_bwd_exchange(Rank& r, BwdRank& q, sfseg_comm* c, cudaStream_t st) {
+  NcclApi& api = nccl();
+  const Plan& P = r.P;
+  const size_t n = (size_t)P.B * P.RT * P.H * P.Wp;
+  if (n == 0) return SFSEG_OK;
+  if (api.GroupStart() != ncclSuccess) return SFSEG_ERR_NCCL;
+  if (r.has_lo) {
+    if (api.Send(q.slo, n, ncclFloat32, c->rank - 1, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
+    if (api.Recv(r.hlo, n, ncclFloat32, c->rank - 1, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
+  }
+  if (r.has_hi) {
+    if (api.Send(q.shi, n, ncclFloat32, c->rank + 1, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
+    if (api.Recv(r.hhi, n, ncclFloat32, c->rank + 1, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
+  }
+  if (api.GroupEnd() != ncclSuccess) return SFSEG_ERR_NCCL;
   return SFSEG_OK;
 }
 
@@ -686,7 +934,8 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
   if (!ch || !w_host || !x_out || !validate_act(act)) s = SFSEG_ERR_INVALID_ARGUMENT;
   else if ((s = make_plan(sh, C, gauss, K, &P, opt)) != SFSEG_OK) {
   } else if (!finite_weights(w_host, C, b)) s = SFSEG_ERR_INVALID_ARGUMENT;
-  else if (tape || F_out) s = SFSEG_ERR_UNSUPPORTED;  // backward / F export are single-GPU only
+  else if (F_out || P.bin) s = SFSEG_ERR_UNSUPPORTED;  // F export / binarisation: single-GPU only
+  else if (tape && (reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) s = SFSEG_ERR_WORKSPACE;
   else if (dist->t_offset < 0 || dist->t_offset + P.T > dist->T_global) s = SFSEG_ERR_SHAPE;
   else if (c->nranks > 1 && P.T < P.RT) s = SFSEG_ERR_SHAPE;  // the halo must come from one neighbour
   else s = check_ws(ws, ws_bytes, slab_offsets(P).total);
@@ -703,6 +952,7 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
   r.stats = stats;
   r.rayleigh = want_rayleigh;
   r.ws = ws;
+  r.tape = tape;
   r.has_lo = dist->t_offset > 0 && c->rank > 0;
   r.has_hi = dist->t_offset + P.T < dist->T_global && c->rank < c->nranks - 1;
   if ((s = rank_setup(r, st)) != SFSEG_OK) return s;
@@ -718,6 +968,63 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
     if (k < P.K && (s = nccl_exchange(r, c, st)) != SFSEG_OK) return s;
   }
   return ph_final(r, st);
+}
+
+// One rank of an NCCL-connected time-slab backward (the tape from a dist forward).
+sfseg_status dist_power_iterate_backward(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
+                                         sfseg_shape sh, sfseg_gauss gauss, int32_t K, const float* x0,
+                                         const void* tape, const float* dL_dx, double* dL_dw_host,
+                                         double* dL_db_host, void* ws, size_t ws_bytes, const sfseg_dist* dist,
+                                         const sfseg_options* opt, void* stream) {
+  if (!dist->comm || !dist->comm->comm) return SFSEG_ERR_INVALID_ARGUMENT;
+  sfseg_comm* c = dist->comm;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Plan P;
+  sfseg_status s = SFSEG_OK;
+  if (!ch || !w_host || !tape || !dL_dx || !dL_dw_host || !validate_act(act)) s = SFSEG_ERR_INVALID_ARGUMENT;
+  else if ((s = make_plan(sh, C, gauss, K, &P, opt)) != SFSEG_OK) {
+  } else if (!finite_weights(w_host, C, b)) s = SFSEG_ERR_INVALID_ARGUMENT;
+  else if (x0 || P.bin) s = SFSEG_ERR_UNSUPPORTED;   // user x_0 / binarisation: single-GPU backward only
+  else if (dist->t_offset < 0 || dist->t_offset + P.T > dist->T_global) s = SFSEG_ERR_SHAPE;
+  else if (c->nranks > 1 && P.T < P.RT) s = SFSEG_ERR_SHAPE;
+  else if ((reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) s = SFSEG_ERR_WORKSPACE;
+  else s = check_ws(ws, ws_bytes, slab_offsets(P).total);
+  const sfseg_status agreed = dist_agree(c, s, st);
+  if (s != SFSEG_OK) return s;
+  if (agreed != SFSEG_OK) return agreed;
+  Rank r;
+  r.P = P;
+  r.ch = ch;
+  r.in_T = (int)P.T;
+  r.ws = ws;
+  r.tape = const_cast<void*>(tape);
+  r.has_lo = dist->t_offset > 0 && c->rank > 0;
+  r.has_hi = dist->t_offset + P.T < dist->T_global && c->rank < c->nranks - 1;
+  if ((s = rank_setup(r, st)) != SFSEG_OK) return s;
+  BwdRank q;
+  q.r = &r;
+  q.g = dL_dx;
+  q.g_T = (int)P.T;
+  if ((s = bw_setup(q, st)) != SFSEG_OK) return s;
+  if ((s = ph_combine(r, w_host, b, act, st)) != SFSEG_OK) return s;
+  if ((s = bw_init(q, st)) != SFSEG_OK) return s;
+  if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) return s;
+  if ((s = bw_init_fin(q, st)) != SFSEG_OK) return s;
+  for (int k = K; k >= 1; --k) {
+    if ((s = bw_halo(q, k, st)) != SFSEG_OK) return s;
+    if ((s = nccl_bwd_exchange(r, q, c, st)) != SFSEG_OK) return s;
+    if ((s = bw_step(q, k, st)) != SFSEG_OK) return s;
+    if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) return s;
+    if ((s = bw_step_fin(q, k, st)) != SFSEG_OK) return s;
+  }
+  if ((s = bw_contract(q, w_host, b, act, st)) != SFSEG_OK) return s;
+  if ((s = nccl_allreduce(r, c, st, (size_t)C + 1)) != SFSEG_OK) return s;
+  std::vector<double> out(C + 1);
+  SF_CUDA(cudaMemcpyAsync(out.data(), r.glob, sizeof(double) * (C + 1), cudaMemcpyDeviceToHost, st));
+  s = sfseg_sync_status(ws, stream);
+  for (int i = 0; i < C; ++i) dL_dw_host[i] = out[i];
+  if (dL_db_host) *dL_db_host = out[C];
+  return s;
 }
 
 // Slab boundaries: slab i of n covers frames [i*T/n, (i+1)*T/n) (uneven when n does not divide T).
@@ -986,12 +1293,13 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
                                              const void* tape, const float* dL_dx, double* dL_dw_host,
                                              double* dL_db_host, void* ws, size_t ws_bytes, const sfseg_dist* dist,
                                              const sfseg_options* opt, void* stream) {
+  if (dist) return dist_power_iterate_backward(ch, C, w_host, b, act, sh, gauss, K, x0, tape, dL_dx, dL_dw_host,
+                                               dL_db_host, ws, ws_bytes, dist, opt, stream);
   if (!ch || !w_host || !tape || !dL_dx || !dL_dw_host || !validate_act(act)) return SFSEG_ERR_INVALID_ARGUMENT;
   Plan P;
   sfseg_status s = make_plan(sh, C, gauss, K, &P, opt);
   if (s != SFSEG_OK) return s;
   if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
-  if (dist) return SFSEG_ERR_UNSUPPORTED;
   if ((s = check_ws(ws, ws_bytes, P.ws_bwd)) != SFSEG_OK) return s;
   if ((reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) return SFSEG_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1035,6 +1343,8 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   ip.W = (int)P.W;
   ip.Wp = (int)P.Wp;
   ip.K = K;
+  ip.g_T = (int)P.T;
+  ip.g_t0 = 0;
   ip.gx = P.gx;
   bwd_init_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ip);
   SF_CUDA(after_launch("bwd_init", st));
@@ -1129,6 +1439,8 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   cc.H = (int)P.H;
   cc.W = (int)P.W;
   cc.Wp = (int)P.Wp;
+  cc.in_T = (int)P.T;
+  cc.in_t0 = 0;
   cc.act = act;
   cc.bias = b;
   for (int c = 0; c < C; ++c) cc.w[c] = w_host[c];
@@ -1696,12 +2008,31 @@ sfseg_status sfseg_slabs_workspace_bytes(sfseg_shape sh, int32_t C, sfseg_gauss 
   return SFSEG_OK;
 }
 
+sfseg_status sfseg_slabs_tape_bytes(sfseg_shape sh, int32_t C, sfseg_gauss gauss, int32_t K, int32_t nslabs,
+                                     size_t* tape_bytes_host) {
+  if (!tape_bytes_host || nslabs < 1 || nslabs > kMaxLocalRanks) return SFSEG_ERR_INVALID_ARGUMENT;
+  size_t tot = 0;
+  for (int i = 0; i < nslabs; ++i) {
+    sfseg_shape ls = sh;
+    ls.T = slab_start(sh.T, nslabs, i + 1) - slab_start(sh.T, nslabs, i);
+    Plan P;
+    sfseg_status s = make_plan(ls, C, gauss, K, &P);
+    if (s != SFSEG_OK) return s;
+    tot += align_up(P.tape_bytes);
+  }
+  *tape_bytes_host = tot;
+  return SFSEG_OK;
+}
+
 sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* w_host, float b, int32_t act,
                                        sfseg_shape sh, sfseg_gauss gauss, int32_t K, int32_t nslabs,
                                        const float* x0, float* x_out, double* stats, int32_t want_rayleigh,
-                                       void* ws, size_t ws_bytes, const sfseg_options* opt, void* stream) {
+                                       void* tape, void* ws, size_t ws_bytes, const sfseg_options* opt,
+                                       void* stream) {
   if (!ch || !w_host || !x_out || !validate_act(act) || nslabs < 1 || nslabs > kMaxLocalRanks)
     return SFSEG_ERR_INVALID_ARGUMENT;
+  if (opt && opt->binarize) return SFSEG_ERR_UNSUPPORTED;
+  if (tape && (reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) return SFSEG_ERR_WORKSPACE;
   if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
   size_t need = 0;
   sfseg_status s = sfseg_slabs_workspace_bytes(sh, C, gauss, K, nslabs, &need);
@@ -1709,12 +2040,16 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
   if ((s = check_ws(ws, ws_bytes, need)) != SFSEG_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   std::vector<Rank> R(nslabs);
-  size_t off = 0;
+  size_t off = 0, toff = 0;
   for (int i = 0; i < nslabs; ++i) {
     const int64_t t0 = slab_start(sh.T, nslabs, i), t1 = slab_start(sh.T, nslabs, i + 1);
     sfseg_shape ls = sh;
     ls.T = t1 - t0;
     if ((s = make_plan(ls, C, gauss, K, &R[i].P, opt)) != SFSEG_OK) return s;
+    if (tape) {
+      R[i].tape = static_cast<char*>(tape) + toff;
+      toff += align_up(R[i].P.tape_bytes);
+    }
     if (nslabs > 1 && R[i].P.T < R[i].P.RT) return SFSEG_ERR_SHAPE;
     R[i].ch = ch;
     R[i].x0 = x0;
@@ -1751,6 +2086,79 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
   for (auto& r : R)
     if ((s = ph_final(r, st)) != SFSEG_OK) return s;
   return SFSEG_OK;
+}
+
+// The time-slab backward emulated on one GPU (the per-rank phases of the NCCL path with
+// in-process halo copies and rank-ordered reductions), on the tape of sfseg_power_iterate_slabs.
+sfseg_status sfseg_power_iterate_slabs_backward(const float* ch, int32_t C, const float* w_host, float b,
+                                                int32_t act, sfseg_shape sh, sfseg_gauss gauss, int32_t K,
+                                                int32_t nslabs, const void* tape, const float* dL_dx,
+                                                double* dL_dw_host, double* dL_db_host, void* ws, size_t ws_bytes,
+                                                const sfseg_options* opt, void* stream) {
+  if (!ch || !w_host || !tape || !dL_dx || !dL_dw_host || !validate_act(act) || nslabs < 1 ||
+      nslabs > kMaxLocalRanks)
+    return SFSEG_ERR_INVALID_ARGUMENT;
+  if (opt && opt->binarize) return SFSEG_ERR_UNSUPPORTED;
+  if (!finite_weights(w_host, C, b)) return SFSEG_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(tape) % kAlign) != 0) return SFSEG_ERR_WORKSPACE;
+  size_t need = 0;
+  sfseg_status s = sfseg_slabs_workspace_bytes(sh, C, gauss, K, nslabs, &need);
+  if (s != SFSEG_OK) return s;
+  if ((s = check_ws(ws, ws_bytes, need)) != SFSEG_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<Rank> R(nslabs);
+  std::vector<BwdRank> Q(nslabs);
+  size_t off = 0, toff = 0;
+  for (int i = 0; i < nslabs; ++i) {
+    const int64_t t0 = slab_start(sh.T, nslabs, i), t1 = slab_start(sh.T, nslabs, i + 1);
+    sfseg_shape ls = sh;
+    ls.T = t1 - t0;
+    if ((s = make_plan(ls, C, gauss, K, &R[i].P, opt)) != SFSEG_OK) return s;
+    if (nslabs > 1 && R[i].P.T < R[i].P.RT) return SFSEG_ERR_SHAPE;
+    R[i].ch = ch;
+    R[i].in_T = (int)sh.T;
+    R[i].in_t0 = (int)t0;
+    R[i].ws = static_cast<char*>(ws) + off;
+    R[i].tape = const_cast<char*>(static_cast<const char*>(tape)) + toff;
+    R[i].has_lo = i > 0;
+    R[i].has_hi = i < nslabs - 1;
+    off += align_up(slab_offsets(R[i].P).total);
+    toff += align_up(R[i].P.tape_bytes);
+    Q[i].r = &R[i];
+    Q[i].g = dL_dx;
+    Q[i].g_T = (int)sh.T;
+    Q[i].g_t0 = (int)t0;
+  }
+  for (int i = 0; i < nslabs; ++i) {
+    if ((s = rank_setup(R[i], st)) != SFSEG_OK) return s;
+    if ((s = bw_setup(Q[i], st)) != SFSEG_OK) return s;
+  }
+  for (auto& r : R)
+    if ((s = ph_combine(r, w_host, b, act, st)) != SFSEG_OK) return s;
+  for (auto& q : Q)
+    if ((s = bw_init(q, st)) != SFSEG_OK) return s;
+  if ((s = local_allreduce(R, st)) != SFSEG_OK) return s;
+  for (auto& q : Q)
+    if ((s = bw_init_fin(q, st)) != SFSEG_OK) return s;
+  for (int k = K; k >= 1; --k) {
+    for (auto& q : Q)
+      if ((s = bw_halo(q, k, st)) != SFSEG_OK) return s;
+    if ((s = local_bwd_exchange(R, Q, st)) != SFSEG_OK) return s;
+    for (auto& q : Q)
+      if ((s = bw_step(q, k, st)) != SFSEG_OK) return s;
+    if ((s = local_allreduce(R, st)) != SFSEG_OK) return s;
+    for (auto& q : Q)
+      if ((s = bw_step_fin(q, k, st)) != SFSEG_OK) return s;
+  }
+  for (auto& q : Q)
+    if ((s = bw_contract(q, w_host, b, act, st)) != SFSEG_OK) return s;
+  if ((s = local_allreduce(R, st, C + 1)) != SFSEG_OK) return s;
+  std::vector<double> out(C + 1);
+  SF_CUDA(cudaMemcpyAsync(out.data(), R[0].glob, sizeof(double) * (C + 1), cudaMemcpyDeviceToHost, st));
+  s = sfseg_slabs_sync_status(sh, C, gauss, K, nslabs, ws, stream);
+  for (int i = 0; i < C; ++i) dL_dw_host[i] = out[i];
+  if (dL_db_host) *dL_db_host = out[C];
+  return s;
 }
 
 // Device error word of slab i inside a sfseg_power_iterate_slabs workspace.

@@ -13,7 +13,7 @@ from typing import Optional, Tuple
 
 import torch
 
-from . import (DistC, Gauss, Shape, _alloc_ws, _check, _ptr, _require, _stream, _weights, lib,
+from . import (DistC, Gauss, Shape, _alloc_bytes, _alloc_ws, _check, _ptr, _require, _stream, _weights, lib,
                ACT_IDENTITY)
 
 
@@ -61,13 +61,15 @@ class SlabSolver:
     """One rank of a time-slab sharded solve (ch / x are this rank's local slab)."""
 
     def __init__(self, comm: Comm, local_shape, T_global: int, t_offset: int, C_: int, gauss: Gauss, K: int,
-                 device="cuda"):
+                 device="cuda", want_tape: bool = False):
         self.comm, self.shape = comm, tuple(int(v) for v in local_shape)
         self.C, self.gauss, self.K = int(C_), gauss, int(K)
         self.dist = DistC(comm.handle, int(T_global), int(t_offset))
         n = C.c_size_t(0)
-        _check(lib().sfseg_workspace_bytes(Shape(*self.shape), self.C, gauss.c(), self.K, 0, C.byref(self.dist),
-                                           C.byref(n), None), "sfseg_workspace_bytes(dist)")
+        tb = C.c_size_t(0)
+        _check(lib().sfseg_workspace_bytes(Shape(*self.shape), self.C, gauss.c(), self.K, int(want_tape),
+                                           C.byref(self.dist), C.byref(n), C.byref(tb)), "sfseg_workspace_bytes(dist)")
+        self.tape = _alloc_bytes(tb.value, device) if want_tape else None
         self.ws_bytes = n.value
         self.ws = _alloc_ws(n.value, device)
         self.device = self.ws.device
@@ -82,11 +84,28 @@ class SlabSolver:
         _require(x_out, "x_out", 4, shape=self.shape, device=self.device)
         _check(lib().sfseg_power_iterate(
             _ptr(ch), self.C, _weights(w, self.C), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
-            None, _ptr(x_out), None, _ptr(self.stats), 0, None, _ptr(self.ws), self.ws_bytes,
+            None, _ptr(x_out), None, _ptr(self.stats), 0, _ptr(self.tape), _ptr(self.ws), self.ws_bytes,
             C.byref(self.dist), _stream(stream)), "sfseg_power_iterate(dist)")
         if check:
             self.sync(stream)
         return x_out
+
+    def backward(self, ch: torch.Tensor, w, dL_dx: torch.Tensor, b: float = 0.0, act: int = ACT_IDENTITY,
+                 stream=None):
+        """Time-slab backward on this rank's tape (sfseg_power_iterate_backward with the sfseg_dist):
+        returns the GLOBAL (dw, db) -- the ranks allreduce them."""
+        if self.tape is None:
+            raise RuntimeError("SlabSolver was built without want_tape")
+        B, T, H, W = self.shape
+        _require(ch, "ch", 5, shape=(B, self.C, T, H, W), device=self.device)
+        _require(dL_dx, "dL_dx", 4, shape=self.shape, device=self.device)
+        dw = (C.c_double * self.C)()
+        db = C.c_double(0.0)
+        _check(lib().sfseg_power_iterate_backward(
+            _ptr(ch), self.C, _weights(w, self.C), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
+            None, _ptr(self.tape), _ptr(dL_dx), dw, C.byref(db), _ptr(self.ws), self.ws_bytes, C.byref(self.dist),
+            _stream(stream)), "sfseg_power_iterate_backward(dist)")
+        return [dw[i] for i in range(self.C)], db.value
 
     def sync(self, stream=None) -> None:
         _check(lib().sfseg_sync_status(_ptr(self.ws), _stream(stream)), "sfseg_power_iterate(dist, device)")

@@ -81,5 +81,46 @@ def test_nccl_single_rank_dist_path(sf):
         x1 = ref.forward(ch, wl.w).cpu().numpy()
         assert _rel(xd, x1.astype(np.float64)) < 1e-6
         np.testing.assert_allclose(s.stats.cpu().numpy(), ref.stats.cpu().numpy(), rtol=1e-6)
+        # the NCCL backward path (agreement, bwd phases, allreduces) with one rank
+        sb = SlabSolver(comm, (1, 12, 60, 100), 12, 0, 1, g, 6, want_tape=True)
+        sb.forward(ch, [1.3], 0.1, 1)
+        gr = torch.from_numpy(np.random.default_rng(2).normal(size=(1, 12, 60, 100)).astype(np.float32)).cuda()
+        dwd, dbd = sb.backward(ch, [1.3], gr, 0.1, 1)
+        _, dw1, db1 = sf.power_iterate_backward(ch, [1.3], g, 6, gr, 0.1, 1)
+        assert abs(dwd[0] - dw1[0]) <= 1e-5 * abs(dw1[0]) and abs(dbd - db1) <= 1e-5 * abs(db1)
+        # a bad argument on a rank is agreed on before any data-path collective (returns, no hang)
+        with pytest.raises(sf.SfsegError):
+            sb.backward(ch, [float("nan")], gr, 0.1, 1)
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("name,shape,nslabs,act", [
+    ("c3", dict(T=26, H=56, W=120), 2, 1),
+    ("c3", dict(T=26, H=56, W=120), 4, 0),     # uneven slabs 6,7,6,7 with r_t = 6
+    ("c4", dict(B=2, T=23, H=48, W=70), 3, 1), # B > 1, r_t = 5
+])
+def test_slab_backward_matches_single_gpu_and_oracle(sf, name, shape, nslabs, act):
+    """Time-slab backward (per step: halo of F y_bar_k with the neighbour slabs, allreduce of
+    <x_{k-1}, x_bar_{k-1}>; final allreduce of dw, db) on the slab forward's tapes == the
+    single-GPU backward and the oracle's dL/dw."""
+    cfg = WL.get_config(name, **shape)
+    wl = WL.generate(name, cfg=cfg)
+    B, C, T, H, W = wl.ch.shape
+    w = wl.w if act == 0 else (np.arange(C, dtype=np.float32) * 0.3 - 0.2)
+    b = 0.0 if act == 0 else 0.15
+    K = 5
+    g = sf.Gauss(cfg.sigma_t, cfg.sigma_s, cfg.radius_t, cfg.radius_s)
+    ch = torch.from_numpy(wl.ch).cuda()
+    rng = np.random.default_rng(9)
+    gr = rng.normal(size=(B, T, H, W)).astype(np.float32)
+    grt = torch.from_numpy(gr).cuda()
+    xs, _, tape = sf.power_iterate_slabs(ch, w, g, K, nslabs, b, act, want_tape=True)
+    dws, dbs = sf.power_iterate_slabs_backward(ch, w, g, K, nslabs, tape, grt, b, act)
+    x1, dw1, db1 = sf.power_iterate_backward(ch, w, g, K, grt, b, act)
+    dwo, dbo = O.power_iterate_backward(wl.ch, w, b, act, O.gaussian_taps(cfg.sigma_t, cfg.radius_t),
+                                        O.gaussian_taps(cfg.sigma_s, cfg.radius_s), K, gr.astype(np.float64))
+    assert _rel(dws, np.array(dwo)) <= 1e-3
+    assert _rel(dws, np.array(dw1)) <= 1e-5     # same arithmetic, different reduction order
+    assert abs(dbs - dbo) <= 1e-3 * max(abs(dbo), np.abs(dwo).max())
+    assert _rel(xs.cpu().numpy(), x1.cpu().numpy()) <= 1e-6
