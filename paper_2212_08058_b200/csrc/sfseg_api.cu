@@ -605,13 +605,19 @@ sfseg_status ph_final(Rank& r, cudaStream_t st) {
   return SFSEG_OK;
 }
 
-sfseg_status nccl_exchange(Rank& r, sfseg_comm* c, cudaStream_t st) {
+// The r_t boundary frames of p with ranks +-1; with_allreduce: the norm partials' fp64
+// allreduce goes into the SAME NCCL group (both depend only on the spatial pass just run):
+// one grouped launch per iteration instead of two, the sends overlapping the reduction.
+sfseg_status nccl_exchange(Rank& r, sfseg_comm* c, cudaStream_t st, bool with_allreduce = false) {
   NcclApi& api = nccl();
   const Plan& P = r.P;
   const size_t fr = (size_t)P.H * P.Wp, n = (size_t)P.RT * fr;
-  if (n == 0) return SFSEG_OK;
+  if (n == 0 && !with_allreduce) return SFSEG_OK;
   if (api.GroupStart() != ncclSuccess) return SFSEG_ERR_NCCL;
-  for (int64_t b = 0; b < P.B; ++b) {
+  if (with_allreduce &&
+      api.AllReduce(r.loc, r.glob, 2 * (size_t)P.B, ncclFloat64, ncclSum, c->comm, st) != ncclSuccess)
+    return SFSEG_ERR_NCCL;
+  for (int64_t b = 0; b < P.B && n > 0; ++b) {
     float* base = r.p + (size_t)b * P.T * fr;
     if (r.has_lo) {
       if (api.Send(base, n, ncclFloat32, c->rank - 1, c->comm, st) != ncclSuccess) return SFSEG_ERR_NCCL;
@@ -963,9 +969,12 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
   for (int k = 1; k <= P.K; ++k) {
     if ((s = ph_T(r, st)) != SFSEG_OK) return s;
     if ((s = ph_S(r, k, st)) != SFSEG_OK) return s;
-    if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) return s;
+    if (k < P.K) {
+      if ((s = nccl_exchange(r, c, st, /*with_allreduce=*/true)) != SFSEG_OK) return s;
+    } else if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) {
+      return s;
+    }
     if ((s = ph_finalize(r, k, st)) != SFSEG_OK) return s;
-    if (k < P.K && (s = nccl_exchange(r, c, st)) != SFSEG_OK) return s;
   }
   return ph_final(r, st);
 }
