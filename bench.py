@@ -262,7 +262,8 @@ def run_ours(args):
     cfg_name = _default_config(args, world)
     args.config = cfg_name
     algo = {"auto": sf.ALGO_AUTO, "tcgen05": sf.ALGO_TWO_PASS_TCGEN05, "mma": sf.ALGO_TWO_PASS_MMA_SYNC,
-            "fp32": sf.ALGO_TWO_PASS_FP32}[args.algo]
+            "fp32": sf.ALGO_TWO_PASS_FP32,
+            "f16": sf.ALGO_TWO_PASS_MMA_F16}[args.algo]
     cfg = WL.get_config(cfg_name)
     slab = world > 1 and args.shard == "slab" and cfg_name != "c4"
     vshard = world > 1 and not slab      # independent volumes split across ranks (c4: 64/N each)
@@ -299,7 +300,8 @@ def run_ours(args):
 
     # the per-frame threshold (a9) is frame-local: each rank thresholds its own slab
     path_info = sf.forward_path((B, T, H, W), gauss, algo)
-    path_tc = path_info[0] in (sf.PATH_TWO_PASS_TC, sf.PATH_TWO_PASS_TCGEN05)
+    path_tc = path_info[0] in (sf.PATH_TWO_PASS_TC, sf.PATH_TWO_PASS_TCGEN05, sf.PATH_TWO_PASS_TC_F16)
+    path_f16 = path_info[0] == sf.PATH_TWO_PASS_TC_F16
     path_t5 = path_info[0] == sf.PATH_TWO_PASS_TCGEN05
     thr_solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev) if slab else solver
 
@@ -466,9 +468,12 @@ def run_ours(args):
             nkx, nky = (16 + ra + RSc + 15) // 16, (16 + 2 * RSc + 15) // 16
             S_ = -(-W // 64)
             # mma.sync m16n8k16 (4096 flop): 16 x 6 HMMA per k step and warp, 4 warps per 32 x 64 block
-            tc_flops = float(B * T * S_ * NB_) * 16 * TC_PRODUCTS * (nkx + nky) * 4096
+            nprod = 3 if path_f16 else TC_PRODUCTS
+            tc_flops = float(B * T * S_ * NB_) * 16 * nprod * (nkx + nky) * 4096
             kname = (f"spass_tc_kernel<R={RSc}> (mma.sync m16n8k16; x/y Gaussian as banded Toeplitz products, "
-                     f"three bf16 planes x six products per tap (fp32-class) + F multiplies + norm)")
+                     + ("two fp16 planes x three products per tap, per-volume power-of-two range scaling"
+                        if path_f16 else "three bf16 planes x six products per tap (fp32-class)")
+                     + " + F multiplies + norm)")
             tc_ceiling = MMA_SYNC_BF16_TFLOPS
         # read v (+ F unless the full operator's plain pass), write p (+ the tape u for training)
         sp_bytes = (8.0 + (0.0 if full else 4.0) + (4.0 if args.config == "c3" else 0.0)) * vox
@@ -558,6 +563,18 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(args.config)
 
+    if path_f16:
+        arith = ("fp32 FFMA everywhere except the forward spatial pass of r_s >= 8, which runs on the tensor "
+                 "pipe with each operand and tap split into two fp16 planes (22 significant bits, per-volume "
+                 "power-of-two range scaling) and three products per tap, fp32 accumulation (fp32-class: x_K "
+                 "error vs the f64 oracle within 2x the FP32-FMA pass's at full c2, tests/test_gpu_fullsize.py; "
+                 "DESIGN.md A25)")
+    elif path_tc:
+        arith = ("fp32 FFMA everywhere except the forward spatial pass of r_s >= 8, which runs on the tensor "
+                 "pipe with each operand and tap split into three bf16 planes and six products per tap "
+                 "(fp32-class; DESIGN.md A23)")
+    else:
+        arith = "fp32 FFMA throughout"
     if rank == 0:
         ck = clocks.summary()
         line = {
@@ -572,10 +589,7 @@ def run_ours(args):
                                        f"NCCL communicator of {comm.nranks} ranks)" if slab else
                                        f"volume shards x{world} ({B} of {cfg.B} volumes per rank, no collective)"
                                        if vshard else "one GPU"),
-                       "arithmetic": ("fp32 FFMA everywhere except the spatial pass of r_s >= 8, which runs on the "
-                                      "tensor pipe with each operand and tap split into three bf16 planes and six "
-                                      "products per tap (fp32-class; x_K error vs the f64 oracle 1.4x the FP32-FMA "
-                                      "pass's at full c2, tests/test_gpu_fullsize.py)"),
+                       "arithmetic": arith,
                        "l2": "inputs > L2 (ch 115 MB + F/p/v 344 MB vs 126 MB L2); no flush",
                        "launch": "one CUDA graph per step" if graph is not None else "stream launches"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
@@ -608,7 +622,7 @@ def main():
     ap.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4", "c5", "probe", "c2f"],
                     help="default: c2 at N=1, c5 (time slabs) at N>1, c4 with --shard volume")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algo", default="auto", choices=["auto", "tcgen05", "mma", "fp32"],
+    ap.add_argument("--algo", default="auto", choices=["auto", "tcgen05", "mma", "fp32", "f16"],
                     help="forward path (sfseg_options.algo): auto, the tcgen05/TMEM spatial pass, the mma.sync "
                          "one, or the FP32-FMA one")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -101,9 +101,11 @@ const char* sfseg_last_cuda_error(void);
  *     (r_t <= 3, r_s <= 8; PAPER.md:319's 3x7x7 support is such a case), otherwise
  *     one temporal pass + one fused spatial pass per iteration.
  *   SFSEG_ALGO_TWO_PASS: always the two-pass iteration.  Its spatial pass runs on the
- *     tensor pipe for compiled spatial radii 8..48: each operand and tap split into three
- *     bf16 planes (the full fp32 significand) and six products per tap (A23),
- *     fp32 accumulation: fp32-class arithmetic.
+ *     tensor pipe for compiled spatial radii 8..48: each operand and tap split into two
+ *     fp16 planes (22 significant bits; the data scaled per volume by a power of two into
+ *     fp16's range) and three products per tap, fp32 accumulation: fp32-class arithmetic
+ *     (A25; x_K error within 2x the FP32-FMA pass's).  The same for the two-pass
+ *     fallback of SFSEG_ALGO_AUTO.
  *   SFSEG_ALGO_TWO_PASS_FP32: the two-pass iteration with the FP32-FMA spatial pass.
  * profiler: NULL, or a sfseg_profiler that records CUDA events around every pass launch
  * (benchmark instrumentation).
@@ -118,10 +120,17 @@ const char* sfseg_last_cuda_error(void);
 #define SFSEG_ALGO_AUTO 0
 #define SFSEG_ALGO_TWO_PASS 1
 #define SFSEG_ALGO_TWO_PASS_FP32 3
-/* the two-pass iteration with the warp-level (mma.sync) tensor-core spatial pass */
+/* the two-pass iteration with the warp-level (mma.sync) tensor-core spatial pass in three bf16
+ * planes and six products per tap (|a - a1 - a2 - a3| <= 2^-27 |a|; A23) */
 #define SFSEG_ALGO_TWO_PASS_MMA_SYNC 4
 /* the two-pass iteration with the tcgen05 / TMEM spatial pass (spatial radii <= 24; else as TWO_PASS) */
 #define SFSEG_ALGO_TWO_PASS_TCGEN05 5
+/* the two-pass iteration with the mma.sync spatial pass in two fp16 planes and three products
+ * per tap (22 significant bits per operand; A25): half the tensor work of the
+ * bf16 format (what SFSEG_ALGO_TWO_PASS runs).  The forward temporal pass records max |v| per volume, and the data are
+ * scaled by a power of two into fp16's normal range; entries below 2^-24 of a volume's
+ * max |v| lose relative precision (absolute error <= 2^-39 max |v|). */
+#define SFSEG_ALGO_TWO_PASS_MMA_F16 6
 typedef struct sfseg_profiler sfseg_profiler;
 typedef struct {
   int32_t n_cont;   /* continuous iterations before binarisation starts (>= 0) */
@@ -310,6 +319,7 @@ sfseg_status sfseg_solve_host_batch(const float* const* ch_host, int32_t n, int3
 #define SFSEG_PATH_TWO_PASS_TC 1
 #define SFSEG_PATH_FUSED_3D 2
 #define SFSEG_PATH_TWO_PASS_TCGEN05 4
+#define SFSEG_PATH_TWO_PASS_TC_F16 5
 sfseg_status sfseg_forward_path(sfseg_shape shape, sfseg_gauss gauss, int32_t algo, int32_t* info_host /*[3]*/);
 
 /* ---- multi-GPU communicator (NCCL, loaded at run time with dlopen) ---- */

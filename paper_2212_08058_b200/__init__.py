@@ -227,11 +227,13 @@ ALGO_TWO_PASS = 1
 ALGO_TWO_PASS_FP32 = 3
 ALGO_TWO_PASS_MMA_SYNC = 4
 ALGO_TWO_PASS_TCGEN05 = 5
+ALGO_TWO_PASS_MMA_F16 = 6
 
 PATH_TWO_PASS_FP32 = 0
 PATH_TWO_PASS_TC = 1
 PATH_FUSED_3D = 2
 PATH_TWO_PASS_TCGEN05 = 4
+PATH_TWO_PASS_TC_F16 = 5
 
 
 def _options(algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None, binarize=None) -> OptionsC:

@@ -22,7 +22,7 @@ constexpr int kSpassWarps = kSpassThreads / 32;
 constexpr int kSpassPartSlots = 1;    // norm partial slots per CTA
 constexpr int kRingStride = kTW + 4;  // ring row stride in floats (== 4 mod 32: conflict-free)
 constexpr int kMaxC = 64;       // channels passed by value in kernel parameters
-constexpr int kScal = 8;        // doubles of per-volume scalars
+constexpr int kScal = 10;       // doubles of per-volume scalars
 
 // per-volume scalar slots (double sc[B][kScal])
 enum ScalSlot : int {
@@ -34,6 +34,8 @@ enum ScalSlot : int {
   SC_NU = 5,           // last nu
   SC_THETA = 6,        // soft-binarisation: mean of the positive entries of y_k (y units)
   SC_CORR = 7,         // backward through a binarised iteration: sum(g) / n_pos (the centre's adjoint)
+  SC_VMAX = 8,         // 8, 9: max |v| of the forward temporal pass of iteration k in slot 8 + (k & 1), as
+                       //   float bits in the slot's first word (atomicMax; the fp16 spatial pass's scale)
 };
 
 enum ErrBits : unsigned { ERR_DEGENERATE = 1u, ERR_NONFINITE = 2u };
@@ -84,6 +86,27 @@ __device__ __forceinline__ void split_planes(float a, float b, uint32_t (&o)[PL]
     if (i + 1 < PL) {
       a -= __uint_as_float(h << 16);
       b -= __uint_as_float(h & 0xffff0000u);
+    }
+  }
+}
+
+// fp16 version of split_planes (the fp16 spatial pass, spass_tc.cuh): a = sum_i plane_i
+// to 2^-(11 PL) relative while every plane stays in fp16's normal range (the callers
+// scale the data so that max |a| < 2^15).
+template <int PL>
+__device__ __forceinline__ void split_planes_f16(float a, float b, uint32_t (&o)[PL]) {
+#pragma unroll
+  for (int i = 0; i < PL; ++i) {
+    uint32_t h;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+    o[i] = h;
+    if (i + 1 < PL) {
+      float lo, hi;
+      asm("{.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;}"
+          : "=f"(lo), "=f"(hi)
+          : "r"(h));
+      a -= lo;
+      b -= hi;
     }
   }
 }

@@ -239,6 +239,7 @@ struct Plan {
   int64_t U;          // spass block units
   int G;              // spass grid
   bool tc;            // forward spatial pass on the tensor cores (spass_tc_kernel)
+  bool f16;           // ... in the two-plane fp16 format (fmt 1; temporal pass records max |v|)
   int Gtc;            // its grid
   bool tc5;           // ... on tcgen05 / TMEM (spass_tc5_kernel): 80-column strips
   int S5;             // its strips
@@ -266,7 +267,8 @@ struct Plan {
 
 bool valid_algo(int32_t algo) {
   return algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_FP32 ||
-         algo == SFSEG_ALGO_TWO_PASS_MMA_SYNC || algo == SFSEG_ALGO_TWO_PASS_TCGEN05;
+         algo == SFSEG_ALGO_TWO_PASS_MMA_SYNC || algo == SFSEG_ALGO_TWO_PASS_TCGEN05 ||
+         algo == SFSEG_ALGO_TWO_PASS_MMA_F16;
 }
 
 sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan* P,
@@ -313,11 +315,15 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->gx = ew_gx(P->H, P->BT);
   P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
   P->tc5 = P->tc && algo == SFSEG_ALGO_TWO_PASS_TCGEN05 && spass_tc5_supported(P->RS);
+  // the forward's default tensor-core format is two fp16 planes (A25); SFSEG_ALGO_TWO_PASS_MMA_SYNC
+  // selects the three-plane bf16 one (A23)
+  P->f16 = P->tc && (algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_MMA_F16);
   P->S5 = (int)((sh.W + k5OW - 1) / k5OW);
   P->NB5 = (int)((sh.H + k5NR - 1) / k5NR);
   P->U5 = P->BT * P->S5 * P->NB5;
   P->G5 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(), P->U5));
-  P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * spass_tc_occupancy(P->RS), P->U / 4));
+  P->Gtc = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)num_sms() * spass_tc_occupancy(P->RS, P->f16 ? 1 : 0), P->U / 4));
   P->f3d = algo == SFSEG_ALGO_AUTO && !P->bin && f3d_supported(P->RT, P->RS);
   P->TX = (int)((sh.W + kF3dTW - 1) / kF3dTW);
   P->TY = (int)((sh.H + f3d_th(std::min(P->RS, kF3dMaxR)) - 1) / f3d_th(std::min(P->RS, kF3dMaxR)));
@@ -443,10 +449,16 @@ cudaError_t launch_spass_forward(const Plan& P, SpassParams& sp, cudaStream_t st
   }
   if (P.tc) {
     sp.G = P.Gtc;
-    return launch_spass_tc(P.RS, sp, P.Gtc, st);
+    return launch_spass_tc(P.RS, sp, P.Gtc, P.f16 ? 1 : 0, st);
   }
   sp.G = P.G;
   return launch_spass_fwd(P.RS, sp, P.G, st);
+}
+
+// The forward temporal pass of iteration k records max |v| per volume for the fp16
+// spatial pass (slot SC_VMAX + (k & 1); the spatial pass of k zeroes the other slot).
+void set_tpass_vmax(TpassParams& tp, const Plan& P, void* ws, int k) {
+  tp.vmax = P.f16 ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + (k & 1)) : nullptr;
 }
 
 void fill_tpass_common(TpassParams& tp, const Plan& P, void* ws) {
@@ -575,7 +587,8 @@ sfseg_status ph_finalize(Rank& r, int k, cudaStream_t st) {
   return SFSEG_OK;
 }
 
-sfseg_status ph_T(Rank& r, cudaStream_t st) {
+sfseg_status ph_T(Rank& r, int k, cudaStream_t st) {
+  set_tpass_vmax(r.tp, r.P, r.ws, k);
   ProfScope ps(r.P.prof, st, PC_TPASS);
   SF_CUDA(launch_tpass_fwd(r.P.RT, r.tp, (int)r.P.B, st));
   SF_CUDA(after_launch("tpass(slab)", st));
@@ -967,7 +980,7 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
   if ((s = ph_finalize(r, 0, st)) != SFSEG_OK) return s;
   if ((s = nccl_exchange(r, c, st)) != SFSEG_OK) return s;
   for (int k = 1; k <= P.K; ++k) {
-    if ((s = ph_T(r, st)) != SFSEG_OK) return s;
+    if ((s = ph_T(r, k, st)) != SFSEG_OK) return s;
     if ((s = ph_S(r, k, st)) != SFSEG_OK) return s;
     if (k < P.K) {
       if ((s = nccl_exchange(r, c, st, /*with_allreduce=*/true)) != SFSEG_OK) return s;
@@ -1069,8 +1082,11 @@ sfseg_status sfseg_forward_path(sfseg_shape sh, sfseg_gauss g, int32_t algo, int
   const sfseg_options opt{algo, nullptr};
   sfseg_status s = make_plan(sh, 1, g, 1, &P, &opt);
   if (s != SFSEG_OK) return s;
-  info[0] = P.f3d ? SFSEG_PATH_FUSED_3D : P.tc5 ? SFSEG_PATH_TWO_PASS_TCGEN05 : P.tc ? SFSEG_PATH_TWO_PASS_TC
-                                                                               : SFSEG_PATH_TWO_PASS_FP32;
+  info[0] = P.f3d ? SFSEG_PATH_FUSED_3D
+            : P.tc5 ? SFSEG_PATH_TWO_PASS_TCGEN05
+            : P.f16 ? SFSEG_PATH_TWO_PASS_TC_F16
+            : P.tc  ? SFSEG_PATH_TWO_PASS_TC
+                    : SFSEG_PATH_TWO_PASS_FP32;
   info[1] = P.RT;
   info[2] = P.RS;
   return SFSEG_OK;
@@ -1231,6 +1247,7 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
   for (int k = 1; k <= K; ++k) {
     // (a2)+(a3) v = s_{k-1} * G_t * p_{k-1}
     {
+      set_tpass_vmax(tp, P, ws, k);
       ProfScope ps(P.prof, st, PC_TPASS);
       SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
       SF_CUDA(after_launch("tpass_fwd", st));
@@ -2084,7 +2101,7 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
   if ((s = local_exchange(R, st)) != SFSEG_OK) return s;
   for (int k = 1; k <= K; ++k) {
     for (auto& r : R)
-      if ((s = ph_T(r, st)) != SFSEG_OK) return s;
+      if ((s = ph_T(r, k, st)) != SFSEG_OK) return s;
     for (auto& r : R)
       if ((s = ph_S(r, k, st)) != SFSEG_OK) return s;
     if ((s = local_allreduce(R, st)) != SFSEG_OK) return s;

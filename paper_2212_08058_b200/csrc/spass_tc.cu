@@ -4,19 +4,23 @@
 
 namespace sfseg {
 namespace {
-template <int R, int EPI>
+template <int R, int EPI, int FMT>
 cudaError_t launch_tc_epi(const SpassParams& P, int grid, cudaStream_t st) {
-  const size_t smem = sptc_smem_bytes(R);
-  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(spass_tc_kernel<R, EPI>), smem);
+  const size_t smem = sptc_smem_bytes(R, FMT);
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(spass_tc_kernel<R, EPI, FMT>), smem);
   if (e != cudaSuccess) return e;
-  spass_tc_kernel<R, EPI><<<grid, kSpassThreads, smem, st>>>(P);
+  spass_tc_kernel<R, EPI, FMT><<<grid, kSpassThreads, smem, st>>>(P);
   return cudaGetLastError();
 }
 template <int R>
-cudaError_t launch_tc_one(const SpassParams& P, int grid, cudaStream_t st) {
-  if (P.plain) return launch_tc_epi<R, EPI_PLAIN>(P, grid, st);
-  if (P.tape_u || P.pprev) return launch_tc_epi<R, EPI_FWD_OPT>(P, grid, st);
-  return launch_tc_epi<R, EPI_FWD>(P, grid, st);
+cudaError_t launch_tc_one(const SpassParams& P, int grid, int fmt, cudaStream_t st) {
+  if (P.plain) return launch_tc_epi<R, EPI_PLAIN, 0>(P, grid, st);
+  if (fmt) {
+    if (P.tape_u || P.pprev) return launch_tc_epi<R, EPI_FWD_OPT, 1>(P, grid, st);
+    return launch_tc_epi<R, EPI_FWD, 1>(P, grid, st);
+  }
+  if (P.tape_u || P.pprev) return launch_tc_epi<R, EPI_FWD_OPT, 0>(P, grid, st);
+  return launch_tc_epi<R, EPI_FWD, 0>(P, grid, st);
 }
 }  // namespace
 
@@ -32,11 +36,11 @@ bool spass_tc_supported(int R) {
       return false;
   }
 }
-int spass_tc_occupancy(int R) {
+int spass_tc_occupancy(int R, int fmt) {
   switch (R) {
 #define TC_OCC(r) \
   case r:         \
-    return sptc_ctas_per_sm(r);
+    return sptc_ctas_per_sm(r, fmt);
     SPTC_RADII(TC_OCC)
 #undef TC_OCC
     default:
@@ -54,11 +58,11 @@ int spass_tc_boxw(int R) {
       return 0;
   }
 }
-cudaError_t launch_spass_tc(int R, const SpassParams& P, int grid, cudaStream_t st) {
+cudaError_t launch_spass_tc(int R, const SpassParams& P, int grid, int fmt, cudaStream_t st) {
   switch (R) {
 #define TC_CASE(r) \
   case r:          \
-    return launch_tc_one<r>(P, grid, st);
+    return launch_tc_one<r>(P, grid, fmt, st);
     SPTC_RADII(TC_CASE)
 #undef TC_CASE
     default:

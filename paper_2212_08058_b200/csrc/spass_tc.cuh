@@ -18,6 +18,16 @@
 // (per product below the 2^-24 rounding unit of an fp32 FMA).  PL = 2 (three terms,
 // ~2^-17) is the round-1 variant, kept compilable for A/B only.
 //
+// FMT = 1 (forward only, reading A25): two fp16 planes and three products
+// (a1g1, a2g1, a1g2).  fp16 keeps 11 significant bits, so two planes carry 22 bits
+// (|a - a1 - a2| <= 2^-22 |a|) -- half the tensor work of FMT = 0 -- but only while
+// both planes stay in fp16's normal range: the data are scaled per volume by 2^e with
+// max |v| < 2^(14 - e) from the temporal pass's max (tpass vmax, SC_VMAX), the taps by
+// 2^12 (smallest tap at 3 sigma ~ 2^-11 of the largest stays normal), the x-pass output
+// by 2^-12 before it is re-split, and the y-pass output by 2^-(12 + e) (all exact
+// powers of two).  Entries below 2^-24 of the volume's max |v| lose relative precision
+// (absolute error <= 2^-39 max |v|).
+//
 // Tiling.  Same work list, segments, TMA producer, ring streaming and finalize as
 // spass_kernel (spass.cuh header), with:
 //   x-pass: D[16 rows x 8 cols] += A[16 rows x 16 box cols] * Tx[16 x 8]; the
@@ -54,32 +64,49 @@ __host__ __device__ constexpr int sptc_nky(int R) { return (16 + 2 * R + 15) / 1
 __host__ __device__ constexpr int sptc_boxw(int R) { return 16 * (3 + sptc_nkx(R)) + 8; }  // == 8 or 24 mod 32
 __host__ __device__ constexpr int sptc_pro(int R) { return (31 + 2 * R) / 32; }
 __host__ __device__ constexpr int sptc_nslot(int R) { return sptc_pro(R) + 1; }
-__host__ __device__ constexpr size_t sptc_smem_for(int R, int stages) {
-  return sizeof(float) * (size_t)stages * kM * sptc_boxw(R)                       // TMA stages
-         + kTcPlanes * sizeof(uint16_t) * (size_t)sptc_nslot(R) * kM * kTcRingStride  // ring planes
-         + (size_t)sptc_nky(R) * kTcPlanes * 32 * 16                                   // Ty fragments
+__host__ __device__ constexpr int sptc_planes(int fmt) { return fmt ? 2 : kTcPlanes; }
+__host__ __device__ constexpr size_t sptc_smem_for(int R, int stages, int fmt = 0) {
+  return sizeof(float) * (size_t)stages * kM * sptc_boxw(R)                                // TMA stages
+         + sptc_planes(fmt) * sizeof(uint16_t) * (size_t)sptc_nslot(R) * kM * kTcRingStride  // ring planes
+         + (size_t)sptc_nky(R) * sptc_planes(fmt) * 32 * 16                                   // Ty fragments
          + 2 * 8 + 8 * 8 + 16;
 }
 #ifndef SPTC_MIN_CTAS
 #define SPTC_MIN_CTAS 3
 #endif
 // two TMA stages when SPTC_MIN_CTAS CTAs still share an SM, else one
-__host__ __device__ constexpr int sptc_stages(int R) {
-  return spass_fit_n(sptc_smem_for(R, 2)) >= SPTC_MIN_CTAS ? 2 : 1;
+__host__ __device__ constexpr int sptc_stages(int R, int fmt = 0) {
+  return spass_fit_n(sptc_smem_for(R, 2, fmt)) >= SPTC_MIN_CTAS ? 2 : 1;
 }
-__host__ __device__ constexpr size_t sptc_smem_bytes(int R) { return sptc_smem_for(R, sptc_stages(R)); }
-__host__ __device__ constexpr int sptc_ctas_per_sm(int R) {
-  return spass_fit_n(sptc_smem_bytes(R)) < 3 ? spass_fit_n(sptc_smem_bytes(R)) : 3;
+__host__ __device__ constexpr size_t sptc_smem_bytes(int R, int fmt = 0) {
+  return sptc_smem_for(R, sptc_stages(R, fmt), fmt);
+}
+__host__ __device__ constexpr int sptc_ctas_per_sm(int R, int fmt = 0) {
+  return spass_fit_n(sptc_smem_bytes(R, fmt)) < 3 ? spass_fit_n(sptc_smem_bytes(R, fmt)) : 3;
 }
 
+template <int FMT = 0>
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
-  asm(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  if (FMT)
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  else
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+template <int FMT, int PL>
+__device__ __forceinline__ void tc_split(float a, float b, uint32_t (&o)[PL]) {
+  if (FMT) split_planes_f16<PL>(a, b, o);
+  else split_planes<PL>(a, b, o);
+}
+// 2^e as a float for |e| <= 126 (exact)
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+constexpr int kF16TapExp = 12;  // FMT = 1: taps scaled by 2^12
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -103,15 +130,16 @@ __device__ __forceinline__ float sptc_w(const float* gsm, int d, int R) {
 // measured 5 % of the instructions were the p_{k-1} loads of the Rayleigh option)
 enum SptcEpi : int { EPI_PLAIN = 0, EPI_FWD = 1, EPI_FWD_OPT = 2 };  // OPT: tape and/or Rayleigh
 
-template <int R, int EPI>
+template <int R, int EPI, int FMT>
 __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid_constant__ SpassParams P) {
+  static_assert(FMT == 0 || EPI != EPI_PLAIN, "the fp16 format needs the forward's per-volume range (SC_VMAX)");
   constexpr int BOXW = sptc_boxw(R);
   constexpr int RA = spass_ra(R);
   constexpr int NKX = sptc_nkx(R);
   constexpr int NKY = sptc_nky(R);
   constexpr int PRO = sptc_pro(R);
   constexpr int NSLOT = sptc_nslot(R);
-  constexpr int NST = sptc_stages(R);
+  constexpr int NST = sptc_stages(R, FMT);
   constexpr int RSW = kTcRingStride / 2;  // ring row stride in u32 words
   constexpr int PLANE = NSLOT * kM * RSW;  // words per ring plane
   constexpr unsigned STAGE_BYTES = kM * BOXW * sizeof(float);
@@ -120,8 +148,9 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
 
   extern __shared__ __align__(128) unsigned char smem[];
   float* stage = reinterpret_cast<float*>(smem);                          // [NST][32][BOXW]
-  constexpr int PL = kTcPlanes;
-  constexpr int NPR = sptc_nprod();
+  constexpr int PL = sptc_planes(FMT);
+  constexpr int NPR = FMT ? 3 : sptc_nprod();
+  constexpr float TSC = FMT ? (float)(1 << kF16TapExp) : 1.f;  // tap scale
   uint32_t* ring = reinterpret_cast<uint32_t*>(stage + NST * kM * BOXW);  // [PL planes][NSLOT*32][RSW]
   uint4* tyf = reinterpret_cast<uint4*>(ring + PL * PLANE);                // [NKY][PL][32]
   uint64_t* bars = reinterpret_cast<uint64_t*>(tyf + NKY * PL * 32);
@@ -155,7 +184,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
       const int i = gi + 8 * (j & 1);
       const int kk = 16 * s + 2 * ti + 8 * (j >> 1);
       uint32_t pp[PL];
-      split_planes<PL>(sptc_w(gsm, kk - i - R, R), sptc_w(gsm, kk + 1 - i - R, R), pp);
+      tc_split<FMT, PL>(TSC * sptc_w(gsm, kk - i - R, R), TSC * sptc_w(gsm, kk + 1 - i - R, R), pp);
       v[j] = pp[pl];
     }
     tyf[idx] = make_uint4(v[0], v[1], v[2], v[3]);
@@ -170,10 +199,15 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
       for (int j = 0; j < 2; ++j) {
         const int d = 16 * s + 2 * t + 8 * j - g - 8 * par - RA;
         uint32_t pp[PL];
-        split_planes<PL>(sptc_w(gsm, d, R), sptc_w(gsm, d + 1, R), pp);
+        tc_split<FMT, PL>(TSC * sptc_w(gsm, d, R), TSC * sptc_w(gsm, d + 1, R), pp);
 #pragma unroll
         for (int q = 0; q < PL; ++q) bx[q][par][s][j] = pp[q];
       }
+  if (FMT && blockIdx.x == 0 && tid == 0) {
+    // the slot the NEXT iteration's temporal pass will max into (this iteration's
+    // slot was filled by the temporal pass that produced v)
+    for (int b = 0; b < P.B; ++b) *reinterpret_cast<unsigned*>(P.sc + b * kScal + SC_VMAX + ((P.k + 1) & 1)) = 0u;
+  }
   __syncthreads();
 
   // ---- producer (thread 0): the x-block sequence of the CTA's unit range
@@ -213,6 +247,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
   const int last = P.last;
   double acc0 = 0.0, acc1 = 0.0;
   int cur_vol = -1;
+  float dsc = 1.f, usc = 1.f;  // FMT = 1: data scale 2^e and output scale 2^-(12 + e) of the volume
   auto flush = [&](int vol) {
     const double s0 = block_sum<kSpassThreads>(acc0, red);
     const double s1 = block_sum<kSpassThreads>(acc1, red);
@@ -239,6 +274,14 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
     if (vol != cur_vol) {
       if (cur_vol >= 0) flush(cur_vol);
       cur_vol = vol;
+      if (FMT) {
+        const float vmax = __uint_as_float(*reinterpret_cast<const unsigned*>(P.sc + vol * kScal + SC_VMAX + (P.k & 1)));
+        int ex = 0;
+        if (vmax > 0.f && vmax <= 3.4e38f) frexpf(vmax, &ex);  // max |v| < 2^ex
+        const int e = min(max(14 - ex, -100), 100);
+        dsc = pow2f(e);
+        usc = pow2f(-e - kF16TapExp);
+      }
     }
     const int c0 = sg.s * kTW;
     const bool wlive = c0 + 32 * hh < W;  // this warp's 32 columns exist (ragged strip)
@@ -318,14 +361,14 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
 #pragma unroll
           for (int nl = 0; nl < 4; ++nl) {
             const uint4& a = ay[sptc_pb(p)];
-            mma16816(p == 0 ? acc[nl] : acs[nl], a.x, a.y, a.z, a.w, bq[sptc_pa(p)][2 * nl],
-                     bq[sptc_pa(p)][2 * nl + 1]);
+            mma16816<FMT>(p == 0 ? acc[nl] : acs[nl], a.x, a.y, a.z, a.w, bq[sptc_pa(p)][2 * nl],
+                          bq[sptc_pa(p)][2 * nl + 1]);
           }
       }
 #pragma unroll
       for (int nl = 0; nl < 4; ++nl)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[nl][i] += acs[nl][i];
+        for (int i = 0; i < 4; ++i) acc[nl][i] = FMT ? (acc[nl][i] + acs[nl][i]) * usc : acc[nl][i] + acs[nl][i];
       // epilogue
       float s0 = 0.f, s1 = 0.f;
       const int yb = (sg.yb0 + m) * kM + 16 * mt + g;
@@ -380,15 +423,21 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
 #pragma unroll
           for (int j = 0; j <= NKX; ++j) {
             const float* p0 = sb + 16 * (2 * hh + j);
-            const float2 v00 = *reinterpret_cast<const float2*>(p0);
-            const float2 v10 = *reinterpret_cast<const float2*>(p0 + 8 * BOXW);
-            const float2 v01 = *reinterpret_cast<const float2*>(p0 + 8);
-            const float2 v11 = *reinterpret_cast<const float2*>(p0 + 8 * BOXW + 8);
+            float2 v00 = *reinterpret_cast<const float2*>(p0);
+            float2 v10 = *reinterpret_cast<const float2*>(p0 + 8 * BOXW);
+            float2 v01 = *reinterpret_cast<const float2*>(p0 + 8);
+            float2 v11 = *reinterpret_cast<const float2*>(p0 + 8 * BOXW + 8);
+            if (FMT) {
+              v00 = make_float2(v00.x * dsc, v00.y * dsc);
+              v10 = make_float2(v10.x * dsc, v10.y * dsc);
+              v01 = make_float2(v01.x * dsc, v01.y * dsc);
+              v11 = make_float2(v11.x * dsc, v11.y * dsc);
+            }
             uint32_t a0[PL], a1[PL], a2[PL], a3[PL];
-            split_planes<PL>(v00.x, v00.y, a0);
-            split_planes<PL>(v10.x, v10.y, a1);
-            split_planes<PL>(v01.x, v01.y, a2);
-            split_planes<PL>(v11.x, v11.y, a3);
+            tc_split<FMT, PL>(v00.x, v00.y, a0);
+            tc_split<FMT, PL>(v10.x, v10.y, a1);
+            tc_split<FMT, PL>(v01.x, v01.y, a2);
+            tc_split<FMT, PL>(v11.x, v11.y, a3);
             // product-major order: consecutive HMMAs write different accumulators
 #pragma unroll
             for (int p = 0; p < NPR; ++p)
@@ -401,7 +450,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
                   float(&d)[4] = p == 0 ? acc[2 * qq + par] : acs[2 * qq + par];
                   const int qa = sptc_pa(p);
                   const uint32_t* bb = bx[sptc_pb(p)][par][s];
-                  mma16816(d, a0[qa], a1[qa], a2[qa], a3[qa], bb[0], bb[1]);
+                  mma16816<FMT>(d, a0[qa], a1[qa], a2[qa], a3[qa], bb[0], bb[1]);
                 }
               }
           }
@@ -410,11 +459,12 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
 #pragma unroll
         for (int nl = 0; nl < 4; ++nl) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[nl][i] += acs[nl][i];
+          for (int i = 0; i < 4; ++i)
+            acc[nl][i] = FMT ? (acc[nl][i] + acs[nl][i]) * (1.f / (float)(1 << kF16TapExp)) : acc[nl][i] + acs[nl][i];
           const int w0 = slot_row * RSW + 4 * (4 * hh + nl) + t;
           uint32_t q0[PL], q1[PL];
-          split_planes<PL>(acc[nl][0], acc[nl][1], q0);
-          split_planes<PL>(acc[nl][2], acc[nl][3], q1);
+          tc_split<FMT, PL>(acc[nl][0], acc[nl][1], q0);
+          tc_split<FMT, PL>(acc[nl][2], acc[nl][3], q1);
 #pragma unroll
           for (int q = 0; q < PL; ++q) {
             ring[q * PLANE + w0] = q0[q];

@@ -29,6 +29,7 @@ struct TpassParams {
   const float* halo_hi;  // [B][RT][H][Wp] frames t = T..T+RT-1 or null
   float* out;            // pitched [B*T][H][Wp]
   const double* sc;      // per-volume scalars [B][kScal]
+  unsigned* vmax;        // FWD: atomicMax of max |out| per volume (float bits, stride 2 kScal words) or null
   long frame4;           // H*Wp/4 float4 per frame
   int T;
   int fexp;              // FWDF: exponent of F multiplying the source (1 or 2)
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   float4 acc[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float vm = 0.f;  // max |out| of this thread (FWD with vmax)
 #pragma unroll
   for (int d = 0; d < NS; ++d) issue(d);
   for (int j0 = 0; j0 < jend; j0 += NR) {
@@ -170,13 +172,30 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
       const int slot0 = (((d - 2 * RT) % NR) + NR) % NR;
       const int t = jp - 2 * RT;
       if (active && t >= 0 && t < T) {
-        if (MODE == TP_FWD) st_f4_hint(out + (long)t * P.frame4, f4_scale(acc[slot0], scale), pol);
-        else __stcg(out + (long)t * P.frame4, f4_scale(acc[slot0], scale));
+        const float4 o = f4_scale(acc[slot0], scale);
+        if (MODE == TP_FWD) {
+          st_f4_hint(out + (long)t * P.frame4, o, pol);
+          vm = fmaxf(vm, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
+        } else {
+          __stcg(out + (long)t * P.frame4, o);
+        }
       }
       acc[slot0] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   cp_async_wait<0>();
+  if (MODE == TP_FWD && P.vmax) {  // max |v| of the volume: the fp16 spatial pass's range (max is order-free)
+    __shared__ unsigned wm[kTpThreads / 32];
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(vm));
+    if ((tid & 31) == 0) wm[tid >> 5] = m;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned mm = wm[0];
+#pragma unroll
+      for (int i = 1; i < kTpThreads / 32; ++i) mm = max(mm, wm[i]);
+      atomicMax(P.vmax + (long)b * 2 * kScal, mm);
+    }
+  }
 }
 
 }  // namespace sfseg

@@ -34,7 +34,8 @@ def main():
     F, _ = O.combine(wl.ch, wl.w)
     xo, sto = OP.power_iterate(F, O.gaussian_taps(c.sigma_t, c.radius_t), O.gaussian_taps(c.sigma_s, c.radius_s), c.K)
     out["oracle_s"] = time.time() - t0
-    for tag, algo in (("tc", sf.ALGO_TWO_PASS_MMA_SYNC), ("tcgen05", sf.ALGO_TWO_PASS_TCGEN05), ("fp32", sf.ALGO_TWO_PASS_FP32)):
+    for tag, algo in (("tc", sf.ALGO_TWO_PASS_MMA_SYNC), ("tcgen05", sf.ALGO_TWO_PASS_TCGEN05),
+                      ("f16", sf.ALGO_TWO_PASS_MMA_F16), ("fp32", sf.ALGO_TWO_PASS_FP32)):
         s = sf.Solver((c.B, c.T, c.H, c.W), c.C, g, c.K, algo=algo)
         x = s.forward(ch, wl.w).cpu().numpy()
         st = s.stats.cpu().numpy()
@@ -42,6 +43,7 @@ def main():
                     "gain_rel": float(np.abs(st[..., 1] / sto["gain"] - 1).max())}
     out["tc_over_fp32_l2"] = out["tc"]["rel_l2"] / out["fp32"]["rel_l2"]
     out["tcgen05_over_fp32_l2"] = out["tcgen05"]["rel_l2"] / out["fp32"]["rel_l2"]
+    out["f16_over_fp32_l2"] = out["f16"]["rel_l2"] / out["fp32"]["rel_l2"]
     print(json.dumps(out))
 
 
