@@ -133,7 +133,7 @@ def _dist():
 def _default_config(args, world: int) -> str:
     if args.config:
         return args.config
-    if world > 1:
+    if world > 1 or getattr(args, "slab_at_1", False):
         return "c4" if args.shard == "volume" else "c5"
     return "c2"
 
@@ -265,7 +265,7 @@ def run_ours(args):
             "fp32": sf.ALGO_TWO_PASS_FP32,
             "f16": sf.ALGO_TWO_PASS_MMA_F16}[args.algo]
     cfg = WL.get_config(cfg_name)
-    slab = world > 1 and args.shard == "slab" and cfg_name != "c4"
+    slab = (world > 1 or args.slab_at_1) and args.shard == "slab" and cfg_name != "c4"
     vshard = world > 1 and not slab      # independent volumes split across ranks (c4: 64/N each)
     K = cfg.K
     gauss = sf.Gauss(cfg.sigma_t, cfg.sigma_s, cfg.radius_t, cfg.radius_s)
@@ -287,7 +287,8 @@ def run_ours(args):
     ch_host = torch.from_numpy(wl.ch).pin_memory()
     ch = ch_host.to(dev)
     if slab:
-        solver = SlabSolver(comm, (B, T, H, W), cfg.T, t0, Cn, gauss, K, device=dev)
+        solver = SlabSolver(comm, (B, T, H, W), cfg.T, t0, Cn, gauss, K, device=dev, algo=algo,
+                            serial=args.slab_serial)
     else:
         solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev, want_tape=(args.config == "c3"), algo=algo)
     full = args.config == "c2f" and not slab
@@ -631,6 +632,11 @@ def main():
                     help="1 (default): replay the step as one captured CUDA graph (measured 2-3 %% faster than "
                          "stream launches at c2/probe/c2f, profiles/tc/ab_graph.txt); 0: stream launches. "
                          "Multi-rank time slabs and the training step (c3) always use stream launches")
+    ap.add_argument("--slab-at-1", action="store_true",
+                    help="run the time-slab path (NCCL communicator, overlapped schedule) with one rank: the N=1 "
+                         "dry run of the multi-GPU launcher")
+    ap.add_argument("--slab-serial", action="store_true",
+                    help="time slabs: the serial schedule instead of the overlapped one (A/B)")
     ap.add_argument("--shard", default="slab", choices=["volume", "slab"],
                     help="N>1: time slabs of one volume with NCCL halos (default, c5) or the c4 batch split by "
                          "volume (64/N per rank, no collective)")

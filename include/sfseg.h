@@ -137,10 +137,21 @@ typedef struct {
   float kappa0;     /* steepness of the first binarised iteration (> 0) */
   float growth;     /* geometric growth of the steepness per iteration (> 0) */
 } sfseg_binarize;
+/* slab_schedule (time slabs, a sfseg_dist or sfseg_power_iterate_slabs):
+ *   SFSEG_SLAB_OVERLAP (0): per iteration the spatial pass computes the r_t boundary frames
+ *     first; the halo exchange runs on a second stream (the communicator's, or one the
+ *     emulation creates for the call) while the interior frames are computed, and the norm
+ *     allreduce + finalize run there while the next temporal pass runs (the normalisation
+ *     s_k is applied by the next spatial pass instead of the temporal pass).
+ *   SFSEG_SLAB_SERIAL (1): the same kernels in the same order on the caller's stream only
+ *     (bitwise the same results; for checking the overlapped schedule). */
+#define SFSEG_SLAB_OVERLAP 0
+#define SFSEG_SLAB_SERIAL 1
 typedef struct {
   int32_t algo;
   sfseg_profiler* profiler;
   const sfseg_binarize* binarize;
+  int32_t slab_schedule;
 } sfseg_options;
 
 /* Per-kernel timing object (owned by the caller).  sfseg_profiler_read syncs the

@@ -61,7 +61,8 @@ class BinarizeC(C.Structure):
 
 
 class OptionsC(C.Structure):
-    _fields_ = [("algo", C.c_int32), ("profiler", C.c_void_p), ("binarize", C.c_void_p)]
+    _fields_ = [("algo", C.c_int32), ("profiler", C.c_void_p), ("binarize", C.c_void_p),
+                ("slab_schedule", C.c_int32)]
 
 
 class AdamwC(C.Structure):
@@ -236,10 +237,14 @@ PATH_TWO_PASS_TCGEN05 = 4
 PATH_TWO_PASS_TC_F16 = 5
 
 
-def _options(algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None, binarize=None) -> OptionsC:
+SLAB_OVERLAP, SLAB_SERIAL = 0, 1
+
+
+def _options(algo: int = ALGO_AUTO, profiler: Optional[Profiler] = None, binarize=None,
+             slab_schedule: int = SLAB_OVERLAP) -> OptionsC:
     """sfseg_options; binarize = (n_cont, kappa0, growth) or None (the BinarizeC is kept alive
     on the returned object for the duration of the call)."""
-    o = OptionsC(int(algo), profiler.handle if profiler is not None else None, None)
+    o = OptionsC(int(algo), profiler.handle if profiler is not None else None, None, int(slab_schedule))
     if binarize is not None:
         o._bz = BinarizeC(int(binarize[0]), float(binarize[1]), float(binarize[2]))
         o.binarize = C.cast(C.pointer(o._bz), C.c_void_p)
@@ -390,9 +395,11 @@ def power_iterate_backward(ch, w, gauss: Gauss, K: int, dL_dx, b: float = 0.0, a
 
 def power_iterate_slabs(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, b: float = 0.0,
                         act: int = ACT_IDENTITY, x0=None, want_rayleigh: bool = False, stream=None,
-                        algo: int = ALGO_AUTO, want_tape: bool = False):
+                        algo: int = ALGO_AUTO, want_tape: bool = False, slab_schedule: int = SLAB_OVERLAP):
     """Time-slab decomposition of the solve emulated on ONE GPU (sfseg_power_iterate_slabs):
-    the per-rank phases of the multi-GPU path with in-process halo copies and reduction.
+    the per-rank phases of the multi-GPU path with in-process halo copies and reduction, in
+    the overlapped schedule (halo copies and the norm reduction on a second stream) or the
+    serial one (SLAB_SERIAL: same kernels, one stream).
     Returns (x, stats) or, with want_tape, (x, stats, tape) for power_iterate_slabs_backward."""
     _require(ch, "ch", 5)
     B, Cn, T, H, W = ch.shape
@@ -413,7 +420,8 @@ def power_iterate_slabs(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, 
         _require(x0, "x0", 4, shape=(B, T, H, W), device=ch.device)
     _check(lib().sfseg_power_iterate_slabs(_ptr(ch), Cn, _weights(w, Cn), float(b), int(act), shp, g, int(K),
                                            nsl, _ptr(x0), _ptr(x), _ptr(stats), int(want_rayleigh), _ptr(tape),
-                                           _ptr(ws), n.value, C.byref(_options(algo)), _stream(stream)),
+                                           _ptr(ws), n.value, C.byref(_options(algo, slab_schedule=slab_schedule)),
+                                           _stream(stream)),
            "sfseg_power_iterate_slabs")
     _check(lib().sfseg_slabs_sync_status(shp, Cn, g, int(K), nsl, _ptr(ws), _stream(stream)),
            "sfseg_power_iterate_slabs (device)")

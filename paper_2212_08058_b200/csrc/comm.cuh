@@ -62,6 +62,8 @@ struct sfseg_comm {
   int rank = 0;
   int device = 0;
   int32_t* flag = nullptr;  // device word of the pre-solve validation agreement (dist_agree)
+  cudaStream_t cs = nullptr;  // comm stream of the overlapped time-slab schedule (SlabSched)
+  cudaEvent_t ev[4] = {};     // its hand-off events
 };
 
 namespace sfseg {

@@ -241,6 +241,7 @@ struct Plan {
   bool tc;            // forward spatial pass on the tensor cores (spass_tc_kernel)
   bool f16;           // ... in the two-plane fp16 format (fmt 1; temporal pass records max |v|)
   int Gtc;            // its grid
+  int Gcap, Gcap_tc;  // resident-CTA caps of the FP32 / tensor-core passes (grids of frame-range launches)
   bool tc5;           // ... on tcgen05 / TMEM (spass_tc5_kernel): 80-column strips
   int S5;             // its strips
   int NB5;            // its 64-row blocks per column
@@ -312,6 +313,7 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->U = P->BT * P->S * P->NB;
   const int64_t cap = (int64_t)num_sms() * spass_occupancy(P->RS);
   P->G = (int)std::max<int64_t>(1, std::min<int64_t>(cap, P->U / 4));
+  P->Gcap = (int)cap;
   P->gx = ew_gx(P->H, P->BT);
   P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
   P->tc5 = P->tc && algo == SFSEG_ALGO_TWO_PASS_TCGEN05 && spass_tc5_supported(P->RS);
@@ -322,8 +324,8 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->NB5 = (int)((sh.H + k5NR - 1) / k5NR);
   P->U5 = P->BT * P->S5 * P->NB5;
   P->G5 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(), P->U5));
-  P->Gtc = (int)std::max<int64_t>(
-      1, std::min<int64_t>((int64_t)num_sms() * spass_tc_occupancy(P->RS, P->f16 ? 1 : 0), P->U / 4));
+  P->Gcap_tc = num_sms() * spass_tc_occupancy(P->RS, P->f16 ? 1 : 0);
+  P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)P->Gcap_tc, P->U / 4));
   P->f3d = algo == SFSEG_ALGO_AUTO && !P->bin && f3d_supported(P->RT, P->RS);
   P->TX = (int)((sh.W + kF3dTW - 1) / kF3dTW);
   P->TY = (int)((sh.H + f3d_th(std::min(P->RS, kF3dMaxR)) - 1) / f3d_th(std::min(P->RS, kF3dMaxR)));
@@ -447,12 +449,15 @@ cudaError_t launch_spass_forward(const Plan& P, SpassParams& sp, cudaStream_t st
     sp.G = P.G5;
     return launch_spass_tc5(P.RS, sp, P.G5, st);
   }
-  if (P.tc) {
-    sp.G = P.Gtc;
-    return launch_spass_tc(P.RS, sp, P.Gtc, P.f16 ? 1 : 0, st);
+  if (sp.t_cnt > 0) {  // frame-range launch (time-slab schedule): its own unit count and grid
+    sp.U = (int64_t)P.B * sp.t_cnt * P.S * P.NB;
+    sp.G = (int)std::max<int64_t>(1, std::min<int64_t>(P.tc ? P.Gcap_tc : P.Gcap, sp.U / 4));
+  } else {
+    sp.U = P.U;
+    sp.G = P.tc ? P.Gtc : P.G;
   }
-  sp.G = P.G;
-  return launch_spass_fwd(P.RS, sp, P.G, st);
+  if (P.tc) return launch_spass_tc(P.RS, sp, sp.G, P.f16 ? 1 : 0, st);
+  return launch_spass_fwd(P.RS, sp, sp.G, st);
 }
 
 // The forward temporal pass of iteration k records max |v| per volume for the fp16
@@ -554,6 +559,8 @@ sfseg_status rank_setup(Rank& r, cudaStream_t st) {
   r.tp.out = r.v;
   r.tp.halo_lo = r.has_lo ? r.hlo : nullptr;
   r.tp.halo_hi = r.has_hi ? r.hhi : nullptr;
+  r.tp.lag = 1;   // lagged normalisation (slab_iterations)
+  r.sp.lag = 1;
   return SFSEG_OK;
 }
 
@@ -595,7 +602,9 @@ sfseg_status ph_T(Rank& r, int k, cudaStream_t st) {
   return SFSEG_OK;
 }
 
-sfseg_status ph_S(Rank& r, int k, cudaStream_t st) {
+// Spatial pass of iteration k over frames [t_lo, t_lo + t_cnt) of every volume; acc: add the
+// launch's norm sums to loc (the later launches of one iteration, in a fixed order).
+sfseg_status ph_S_range(Rank& r, int k, int t_lo, int t_cnt, int acc, cudaStream_t st) {
   r.sp.out = r.p;
   r.sp.pprev = r.rayleigh ? r.p : nullptr;
   r.sp.tape_u = r.tape ? reinterpret_cast<float*>(static_cast<char*>(r.tape) + r.P.tape_hdr_bytes +
@@ -603,9 +612,97 @@ sfseg_status ph_S(Rank& r, int k, cudaStream_t st) {
                        : nullptr;
   r.sp.k = k;
   r.sp.last = (k == r.P.K) ? 1 : 0;
+  r.sp.t_lo = t_lo;
+  r.sp.t_cnt = t_cnt;
+  r.sp.loc_acc = acc;
   ProfScope ps(r.P.prof, st, PC_SPASS);
   SF_CUDA(launch_spass_forward(r.P, r.sp, st));
   SF_CUDA(after_launch("spass(slab)", st));
+  return SFSEG_OK;
+}
+
+// The frames a rank's neighbours need (its r_t boundary frames) are computed first, so the
+// halo transfer can run while the interior frames are computed.  With no neighbour, or a
+// slab too thin for disjoint boundary ranges, one launch covers the slab.
+sfseg_status ph_S_boundary(Rank& r, int k, cudaStream_t st) {
+  const int T = (int)r.P.T, RT = r.P.RT;
+  const int lo = r.has_lo ? RT : 0, hi = r.has_hi ? RT : 0;
+  if (lo + hi == 0 || lo + hi >= T) return ph_S_range(r, k, 0, T, 0, st);
+  sfseg_status s = SFSEG_OK;
+  if (lo > 0 && (s = ph_S_range(r, k, 0, lo, 0, st)) != SFSEG_OK) return s;
+  if (hi > 0) return ph_S_range(r, k, T - hi, hi, lo > 0 ? 1 : 0, st);
+  return SFSEG_OK;
+}
+sfseg_status ph_S_interior(Rank& r, int k, cudaStream_t st) {
+  const int T = (int)r.P.T, RT = r.P.RT;
+  const int lo = r.has_lo ? RT : 0, hi = r.has_hi ? RT : 0;
+  if (lo + hi == 0 || lo + hi >= T) return SFSEG_OK;
+  return ph_S_range(r, k, lo, T - lo - hi, 1, st);
+}
+
+// Streams and events of the overlapped time-slab schedule.  Compute (st): temporal pass,
+// boundary spatial pass, interior spatial pass.  Comm (cs): the halo exchange (after the
+// boundary pass, overlapping the interior pass) and the norm allreduce + finalize (after
+// the interior pass, overlapping the next temporal pass, which does not need s_k: the
+// normalisation is lagged into the next spatial pass, TpassParams::lag / SpassParams::lag).
+// serial: cs == st and no events (the same kernels in the same per-stream order: bitwise
+// the same results).
+struct SlabSched {
+  cudaStream_t st = nullptr, cs = nullptr;
+  cudaEvent_t ev[4] = {};
+  bool ovl = false;
+  bool own = false;  // stream / events created for this call (single-GPU emulation)
+  enum { EV_B = 0, EV_H = 1, EV_I = 2, EV_F = 3 };
+  cudaError_t rec(int e, cudaStream_t s) { return ovl ? cudaEventRecord(ev[e], s) : cudaSuccess; }
+  cudaError_t wait(cudaStream_t s, int e) { return ovl ? cudaStreamWaitEvent(s, ev[e], 0) : cudaSuccess; }
+  cudaError_t init_own(cudaStream_t compute, bool overlap) {
+    st = cs = compute;
+    ovl = overlap;
+    if (!overlap) return cudaSuccess;
+    own = true;
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    return e;
+  }
+  ~SlabSched() {
+    if (!own) return;
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (cs) cudaStreamDestroy(cs);
+  }
+};
+
+// The K iterations of the time-slab forward for the ranks in R (one per process with NCCL,
+// all of them in the single-GPU emulation); exch / reduce enqueue the halo exchange and the
+// norm allreduce on a stream.  Entered after the combine, its reduction and the first halo
+// exchange (all on st); returns with st after the last finalize.
+template <class Exch, class Reduce>
+sfseg_status slab_iterations(std::vector<Rank*>& R, SlabSched& S, Exch&& exch, Reduce&& reduce) {
+  const int K = R[0]->P.K;
+  sfseg_status s = SFSEG_OK;
+  for (int k = 1; k <= K; ++k) {
+    if (k > 1) SF_CUDA(S.wait(S.st, SlabSched::EV_H));  // halos of p_{k-1}
+    for (Rank* r : R)
+      if ((s = ph_T(*r, k, S.st)) != SFSEG_OK) return s;
+    if (k > 1) SF_CUDA(S.wait(S.st, SlabSched::EV_F));  // s_{k-1} for the spatial pass
+    for (Rank* r : R)
+      if ((s = ph_S_boundary(*r, k, S.st)) != SFSEG_OK) return s;
+    if (k < K) {
+      SF_CUDA(S.rec(SlabSched::EV_B, S.st));
+      SF_CUDA(S.wait(S.cs, SlabSched::EV_B));
+      if ((s = exch(S.cs)) != SFSEG_OK) return s;
+      SF_CUDA(S.rec(SlabSched::EV_H, S.cs));
+    }
+    for (Rank* r : R)
+      if ((s = ph_S_interior(*r, k, S.st)) != SFSEG_OK) return s;
+    SF_CUDA(S.rec(SlabSched::EV_I, S.st));
+    SF_CUDA(S.wait(S.cs, SlabSched::EV_I));
+    if ((s = reduce(S.cs)) != SFSEG_OK) return s;
+    for (Rank* r : R)
+      if ((s = ph_finalize(*r, k, S.cs)) != SFSEG_OK) return s;
+    SF_CUDA(S.rec(SlabSched::EV_F, S.cs));
+  }
+  SF_CUDA(S.wait(S.st, SlabSched::EV_F));
   return SFSEG_OK;
 }
 
@@ -963,6 +1060,7 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
   if (agreed != SFSEG_OK) return agreed;  // a peer failed its validation: nobody starts the solve
   Rank r;
   r.P = P;
+  r.P.tc5 = false;  // time slabs: frame-range launches and the lagged scale are in the mma.sync / FP32 passes
   r.ch = ch;
   r.x0 = x0;
   r.in_T = (int)P.T;
@@ -979,16 +1077,18 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
   if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) return s;
   if ((s = ph_finalize(r, 0, st)) != SFSEG_OK) return s;
   if ((s = nccl_exchange(r, c, st)) != SFSEG_OK) return s;
-  for (int k = 1; k <= P.K; ++k) {
-    if ((s = ph_T(r, k, st)) != SFSEG_OK) return s;
-    if ((s = ph_S(r, k, st)) != SFSEG_OK) return s;
-    if (k < P.K) {
-      if ((s = nccl_exchange(r, c, st, /*with_allreduce=*/true)) != SFSEG_OK) return s;
-    } else if ((s = nccl_allreduce(r, c, st)) != SFSEG_OK) {
-      return s;
-    }
-    if ((s = ph_finalize(r, k, st)) != SFSEG_OK) return s;
+  SlabSched S;
+  S.st = S.cs = st;
+  if (!(opt && opt->slab_schedule == SFSEG_SLAB_SERIAL) && c->cs) {  // overlapped on the comm's stream
+    S.cs = c->cs;
+    S.ovl = true;
+    for (int i = 0; i < 4; ++i) S.ev[i] = c->ev[i];
   }
+  std::vector<Rank*> R{&r};
+  if ((s = slab_iterations(
+           R, S, [&](cudaStream_t q) { return nccl_exchange(r, c, q); },
+           [&](cudaStream_t q) { return nccl_allreduce(r, c, q); })) != SFSEG_OK)
+    return s;
   return ph_final(r, st);
 }
 
@@ -1957,10 +2057,16 @@ sfseg_status sfseg_comm_create(const uint8_t id_host[128], int32_t nranks, int32
     delete c;
     return SFSEG_ERR_CUDA;
   }
-  if (api.CommInitRank(&c->comm, nranks, id, rank) != ncclSuccess) {
+  // the overlapped time-slab schedule's comm stream and hand-off events (setup call, not a solve)
+  bool ok = cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking) == cudaSuccess;
+  for (int i = 0; i < 4 && ok; ++i) ok = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok || api.CommInitRank(&c->comm, nranks, id, rank) != ncclSuccess) {
     cudaFree(c->flag);
+    for (cudaEvent_t e : c->ev)
+      if (e) cudaEventDestroy(e);
+    if (c->cs) cudaStreamDestroy(c->cs);
     delete c;
-    return SFSEG_ERR_NCCL;
+    return ok ? SFSEG_ERR_NCCL : SFSEG_ERR_CUDA;
   }
   *out = c;
   return SFSEG_OK;
@@ -1972,6 +2078,9 @@ sfseg_status sfseg_comm_destroy(sfseg_comm* c) {
   sfseg_status s = SFSEG_OK;
   if (c->comm && api.ok && api.CommDestroy(c->comm) != ncclSuccess) s = SFSEG_ERR_NCCL;
   if (c->flag) cudaFree(c->flag);
+  for (cudaEvent_t e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->cs) cudaStreamDestroy(c->cs);
   delete c;
   return s;
 }
@@ -2072,6 +2181,7 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
     sfseg_shape ls = sh;
     ls.T = t1 - t0;
     if ((s = make_plan(ls, C, gauss, K, &R[i].P, opt)) != SFSEG_OK) return s;
+    R[i].P.tc5 = false;  // as in dist_power_iterate
     if (tape) {
       R[i].tape = static_cast<char*>(tape) + toff;
       toff += align_up(R[i].P.tape_bytes);
@@ -2099,16 +2209,14 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
   for (auto& r : R)
     if ((s = ph_finalize(r, 0, st)) != SFSEG_OK) return s;
   if ((s = local_exchange(R, st)) != SFSEG_OK) return s;
-  for (int k = 1; k <= K; ++k) {
-    for (auto& r : R)
-      if ((s = ph_T(r, k, st)) != SFSEG_OK) return s;
-    for (auto& r : R)
-      if ((s = ph_S(r, k, st)) != SFSEG_OK) return s;
-    if ((s = local_allreduce(R, st)) != SFSEG_OK) return s;
-    for (auto& r : R)
-      if ((s = ph_finalize(r, k, st)) != SFSEG_OK) return s;
-    if (k < K && (s = local_exchange(R, st)) != SFSEG_OK) return s;
-  }
+  SlabSched S;
+  SF_CUDA(S.init_own(st, nslabs > 1 && !(opt && opt->slab_schedule == SFSEG_SLAB_SERIAL)));
+  std::vector<Rank*> RP;
+  for (auto& r : R) RP.push_back(&r);
+  if ((s = slab_iterations(
+           RP, S, [&](cudaStream_t q) { return local_exchange(R, q); },
+           [&](cudaStream_t q) { return local_allreduce(R, q); })) != SFSEG_OK)
+    return s;
   for (auto& r : R)
     if ((s = ph_final(r, st)) != SFSEG_OK) return s;
   return SFSEG_OK;

@@ -94,6 +94,10 @@ struct SpassParams {
   int K, k;                // iteration (FWD) or backward step (BWD), 1-based
   int last;                // FWD: write y instead of p
   int plain;               // FWD: write u = G_s v only (no F multiplies, no norm; full-operator path)
+  int t_lo, t_cnt;         // t_cnt > 0: units cover frames [t_lo, t_lo + t_cnt) of every volume only
+                           //   (time-slab schedule: boundary frames first, interior after); U = B t_cnt S NB
+  int lag;                 // FWD: v came unscaled (lagged normalisation): u *= s_{k-1} = sc[SC_S] here
+  int loc_acc;             // time-slab mode: add this launch's sums to loc (later launches of one iteration)
   float g[kMaxRS + 1];     // g[d] = weight of spatial offset +-d (same taps for y and x)
 };
 
@@ -153,8 +157,13 @@ __device__ __forceinline__ void spass_finalize(const SpassParams& P, double* red
     }
     if ((wide && tid == 0) || (!wide && lane == 0)) {
       if (P.loc) {
-        P.loc[2 * b] = s0;
-        P.loc[2 * b + 1] = s1;
+        if (P.loc_acc) {  // fixed launch order: deterministic
+          P.loc[2 * b] += s0;
+          P.loc[2 * b + 1] += s1;
+        } else {
+          P.loc[2 * b] = s0;
+          P.loc[2 * b + 1] = s1;
+        }
       } else if (MODE == SP_FWD) {
         fwd_finalize(P.sc + b * kScal, P.stats, P.tape_nu, P.err, P.K, P.k, P.pprev != nullptr, b, s0, s1);
       } else {
@@ -190,6 +199,15 @@ __device__ __forceinline__ Seg seg_decode(long u, long u_end, int NB, int S) {
   g.yb1 = (int)min((long)NB, (long)g.yb0 + (u_end - u));
   return g;
 }
+// the same with a frame range (P.t_cnt > 0): unit frame index -> volume frame b T + t_lo + t
+__device__ __forceinline__ Seg seg_decode(const SpassParams& P, long u, long u_end) {
+  Seg g = seg_decode(u, u_end, P.NB, P.S);
+  if (P.t_cnt > 0) {
+    const int b = g.bt / P.t_cnt;
+    g.bt = b * P.T + P.t_lo + (g.bt - b * P.t_cnt);
+  }
+  return g;
+}
 
 // One CTA's walk over the block units [u_begin, u_end) (see the header comment).
 // TMA stage parity continues across calls through pseq_io / cseq_io (persistent
@@ -221,7 +239,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
   auto producer_next = [&]() {
     while (pu < u_end) {
       if (pn == 0) {
-        pseg = seg_decode(pu, u_end, NB, S);
+        pseg = seg_decode(P, pu, u_end);
         pnx = (pseg.yb1 - pseg.yb0) + PRO;
         pgs = pseg.yb0 * kM - R - OFF;
       }
@@ -252,11 +270,12 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
 
   // per-volume scalars for the backward epilogue (refreshed per volume)
   float cn = 0.f, inv_nu = 0.f, inv_nu_prev = 0.f;
+  float lag_s = 1.f;  // forward with lagged normalisation: s_{k-1} of the volume
 
   unsigned cseq = cseq_io;  // consumed TMA loads (stage / parity)
   long u = u_begin;
   while (u < u_end) {
-    const Seg sg = seg_decode(u, u_end, NB, S);
+    const Seg sg = seg_decode(P, u, u_end);
     const int nyb = sg.yb1 - sg.yb0;
     const int nxb = nyb + PRO;
     const int gs = sg.yb0 * kM - R - OFF;
@@ -265,6 +284,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
     if (vol != cur_vol) {
       if (cur_vol >= 0) flush(cur_vol);
       cur_vol = vol;
+      if (MODE == SP_FWD && P.lag) lag_s = (float)P.sc[vol * kScal + SC_S];
       if (MODE == SP_BWD) {
         cn = (float)P.sc[vol * kScal + SC_CN];
         inv_nu = (float)P.sc[vol * kScal + SC_INV_NU];
@@ -336,7 +356,7 @@ __device__ __forceinline__ void spass_run(const SpassParams& P, long u_begin, lo
         if (y >= yend) break;
         const long off = ((long)sg.bt * H + y) * Wp + x;
         float4 f = pr.f[i];
-        float4 uu = a[i];
+        float4 uu = (MODE == SP_FWD) ? f4_scale(a[i], lag_s) : a[i];
         if (!xfull) {
           f = f4_mul(f, msk);
           uu = f4_mul(uu, msk);

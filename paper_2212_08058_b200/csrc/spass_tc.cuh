@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
   auto producer_next = [&]() {
     while (pu < u_end) {
       if (pn == 0) {
-        pseg = seg_decode(pu, u_end, NB, S);
+        pseg = seg_decode(P, pu, u_end);
         pnx = (pseg.yb1 - pseg.yb0) + PRO;
         pgs = pseg.yb0 * kM - R;
       }
@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
   const int last = P.last;
   double acc0 = 0.0, acc1 = 0.0;
   int cur_vol = -1;
-  float dsc = 1.f, usc = 1.f;  // FMT = 1: data scale 2^e and output scale 2^-(12 + e) of the volume
+  float dsc = 1.f, usc = 1.f;  // FMT = 1: data scale 2^e and output scale 2^-(12 + e) (x s_{k-1} when lagged)
+  float lag_s = 1.f;           // FMT = 0: s_{k-1} of the volume when the normalisation is lagged (else 1)
   auto flush = [&](int vol) {
     const double s0 = block_sum<kSpassThreads>(acc0, red);
     const double s1 = block_sum<kSpassThreads>(acc1, red);
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
   unsigned cseq = 0;
   long u = u_begin;
   while (u < u_end) {
-    const Seg sg = seg_decode(u, u_end, NB, S);
+    const Seg sg = seg_decode(P, u, u_end);
     const int nyb = sg.yb1 - sg.yb0;
     const int nxb = nyb + PRO;
     const int gs = sg.yb0 * kM - R;
@@ -274,13 +275,14 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
     if (vol != cur_vol) {
       if (cur_vol >= 0) flush(cur_vol);
       cur_vol = vol;
+      if (!plain && P.lag) lag_s = (float)P.sc[vol * kScal + SC_S];
       if (FMT) {
         const float vmax = __uint_as_float(*reinterpret_cast<const unsigned*>(P.sc + vol * kScal + SC_VMAX + (P.k & 1)));
         int ex = 0;
         if (vmax > 0.f && vmax <= 3.4e38f) frexpf(vmax, &ex);  // max |v| < 2^ex
         const int e = min(max(14 - ex, -100), 100);
         dsc = pow2f(e);
-        usc = pow2f(-e - kF16TapExp);
+        usc = pow2f(-e - kF16TapExp) * lag_s;
       }
     }
     const int c0 = sg.s * kTW;
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
 #pragma unroll
       for (int nl = 0; nl < 4; ++nl)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[nl][i] = FMT ? (acc[nl][i] + acs[nl][i]) * usc : acc[nl][i] + acs[nl][i];
+        for (int i = 0; i < 4; ++i) acc[nl][i] = (acc[nl][i] + acs[nl][i]) * (FMT ? usc : lag_s);
       // epilogue
       float s0 = 0.f, s1 = 0.f;
       const int yb = (sg.yb0 + m) * kM + 16 * mt + g;

@@ -30,6 +30,7 @@ struct TpassParams {
   float* out;            // pitched [B*T][H][Wp]
   const double* sc;      // per-volume scalars [B][kScal]
   unsigned* vmax;        // FWD: atomicMax of max |out| per volume (float bits, stride 2 kScal words) or null
+  int lag;               // FWD: no scale (the spatial pass applies s_{k-1}: lagged normalisation, time slabs)
   long frame4;           // H*Wp/4 float4 per frame
   int T;
   int fexp;              // FWDF: exponent of F multiplying the source (1 or 2)
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   const float4* U1 = nullptr;
   float cn = 0.f, inv_nu = 0.f, corr = 0.f, scale = 1.f;
   if (MODE == TP_FWD) {
-    scale = (float)P.sc[b * kScal + SC_S];
+    scale = P.lag ? 1.f : (float)P.sc[b * kScal + SC_S];
   } else if (MODE == TP_FWDF) {
     scale = (float)P.sc[b * kScal + SC_S];
     Fp = reinterpret_cast<const float4*>(P.F) + b * vol4 + ec;

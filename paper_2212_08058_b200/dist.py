@@ -13,8 +13,8 @@ from typing import Optional, Tuple
 
 import torch
 
-from . import (DistC, Gauss, Shape, _alloc_bytes, _alloc_ws, _check, _ptr, _require, _stream, _weights, lib,
-               ACT_IDENTITY)
+from . import (DistC, Gauss, Shape, _alloc_bytes, _alloc_ws, _check, _options, _ptr, _require, _stream, _weights,
+               lib, ACT_IDENTITY)
 
 
 def slab_range(T: int, n: int, r: int) -> Tuple[int, int]:
@@ -32,6 +32,8 @@ def broadcast_unique_id(rank: int, group=None) -> bytes:
         raw = (C.c_uint8 * 128)()
         _check(lib().sfseg_get_unique_id(raw), "sfseg_get_unique_id")
         buf = torch.tensor(list(bytes(raw)), dtype=torch.uint8)
+    if not dist.is_initialized():   # one process: nothing to broadcast
+        return bytes(buf.tolist())
     backend = dist.get_backend(group)
     dev_buf = buf.cuda() if backend == "nccl" else buf
     dist.broadcast(dev_buf, src=0, group=group)
@@ -61,8 +63,10 @@ class SlabSolver:
     """One rank of a time-slab sharded solve (ch / x are this rank's local slab)."""
 
     def __init__(self, comm: Comm, local_shape, T_global: int, t_offset: int, C_: int, gauss: Gauss, K: int,
-                 device="cuda", want_tape: bool = False):
+                 device="cuda", want_tape: bool = False, serial: bool = False, algo: int = 0):
         self.comm, self.shape = comm, tuple(int(v) for v in local_shape)
+        # overlapped schedule (halo exchange under the interior frames, lagged allreduce) unless serial
+        self.opt = _options(int(algo), slab_schedule=1 if serial else 0)
         self.C, self.gauss, self.K = int(C_), gauss, int(K)
         self.dist = DistC(comm.handle, int(T_global), int(t_offset))
         n = C.c_size_t(0)
@@ -82,10 +86,10 @@ class SlabSolver:
         if x_out is None:
             x_out = torch.empty(self.shape, dtype=torch.float32, device=self.device)
         _require(x_out, "x_out", 4, shape=self.shape, device=self.device)
-        _check(lib().sfseg_power_iterate(
+        _check(lib().sfseg_power_iterate_ex(
             _ptr(ch), self.C, _weights(w, self.C), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
             None, _ptr(x_out), None, _ptr(self.stats), 0, _ptr(self.tape), _ptr(self.ws), self.ws_bytes,
-            C.byref(self.dist), _stream(stream)), "sfseg_power_iterate(dist)")
+            C.byref(self.dist), C.byref(self.opt), _stream(stream)), "sfseg_power_iterate(dist)")
         if check:
             self.sync(stream)
         return x_out

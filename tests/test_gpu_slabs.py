@@ -124,3 +124,35 @@ def test_slab_backward_matches_single_gpu_and_oracle(sf, name, shape, nslabs, ac
     assert _rel(dws, np.array(dw1)) <= 1e-5     # same arithmetic, different reduction order
     assert abs(dbs - dbo) <= 1e-3 * max(abs(dbo), np.abs(dwo).max())
     assert _rel(xs.cpu().numpy(), x1.cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("name,shape,nslabs,algo", [
+    ("c2", dict(T=40, H=70, W=150), 3, "auto"),    # 13/14-frame slabs, r_t = 6: boundary + 1-2 interior frames
+    ("c2", dict(T=26, H=70, W=150), 4, "auto"),    # middle slabs too thin to split: one launch
+    ("c5", dict(T=40, H=64, W=140), 2, "fp32"),    # r_t = 9, FP32-FMA spatial pass
+    ("c4", dict(B=2, T=30, H=48, W=70), 2, "mma"),  # B > 1, bf16 three-plane pass
+])
+def test_slab_overlapped_schedule_bitwise_equals_serial(sf, name, shape, nslabs, algo):
+    """The overlapped time-slab schedule (boundary frames first, halo copies under the interior
+    frames and the norm reduction under the next temporal pass, on a second stream) gives
+    bitwise the serial schedule's x, stats and tape; both match the single-GPU solve."""
+    cfg = WL.get_config(name, **shape)
+    wl = WL.generate(name, cfg=cfg)
+    g = sf.Gauss(cfg.sigma_t, cfg.sigma_s, cfg.radius_t, cfg.radius_s)
+    A = {"auto": sf.ALGO_AUTO, "fp32": sf.ALGO_TWO_PASS_FP32, "mma": sf.ALGO_TWO_PASS_MMA_SYNC}[algo]
+    ch = torch.from_numpy(wl.ch).cuda()
+    K = 6
+    res = {}
+    for sched in (sf.SLAB_OVERLAP, sf.SLAB_SERIAL):
+        x, st, tape = sf.power_iterate_slabs(ch, wl.w, g, K, nslabs, want_rayleigh=True, algo=A, want_tape=True,
+                                             slab_schedule=sched)
+        torch.cuda.synchronize()
+        res[sched] = (x.cpu().numpy(), st.cpu().numpy(), tape.cpu().numpy())
+    for a, b in zip(res[sf.SLAB_OVERLAP], res[sf.SLAB_SERIAL]):
+        assert np.array_equal(a, b)
+    B, C, T, H, W = wl.ch.shape
+    s1 = sf.Solver((B, T, H, W), C, g, K, algo=A)
+    x1 = s1.forward(ch, wl.w, want_rayleigh=True).cpu().numpy()
+    for b in range(B):
+        assert _rel(res[sf.SLAB_OVERLAP][0][b], x1[b].astype(np.float64)) < 1e-6
+    np.testing.assert_allclose(res[sf.SLAB_OVERLAP][1], s1.stats.cpu().numpy(), rtol=1e-6)
