@@ -16,8 +16,8 @@ cudaError_t launch_tpass_fwdf(int RT, const TpassParams& P, int B, cudaStream_t 
 bool spass_tc_supported(int R);
 int spass_tc_occupancy(int R, int fmt = 0);
 int spass_tc_boxw(int R);
-// fmt 0: three bf16 planes / six products; 1: two fp16 planes / three products (forward
-// only; needs the temporal pass's per-volume max |v| in SC_VMAX, TpassParams::vmax)
+// fmt 0: three bf16 planes / six products; 1: two fp16 planes / three products (needs the
+// preceding temporal pass's per-volume max |v|: TpassParams::vmax -> SpassParams::vslot)
 cudaError_t launch_spass_tc(int R, const SpassParams& P, int grid, int fmt, cudaStream_t st);
 // tcgen05 / TMEM spatial pass (spass_tc5.cuh): strips of 80 output columns, 128-column TMA boxes
 bool spass_tc5_supported(int R);

@@ -460,10 +460,12 @@ cudaError_t launch_spass_forward(const Plan& P, SpassParams& sp, cudaStream_t st
   return launch_spass_fwd(P.RS, sp, sp.G, st);
 }
 
-// The forward temporal pass of iteration k records max |v| per volume for the fp16
-// spatial pass (slot SC_VMAX + (k & 1); the spatial pass of k zeroes the other slot).
-void set_tpass_vmax(TpassParams& tp, const Plan& P, void* ws, int k) {
-  tp.vmax = P.f16 ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + (k & 1)) : nullptr;
+// Temporal pass j of a sequence of (temporal, spatial) pass pairs records max |v| per volume
+// for the fp16 spatial pass (slot SC_VMAX + (j & 1); that spatial pass zeroes the other slot).
+// Every pair whose spatial pass runs in the fp16 format must go through this.
+void set_vslot(TpassParams& tp, SpassParams* sp, const Plan& P, void* ws, int j) {
+  tp.vmax = P.f16 ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + (j & 1)) : nullptr;
+  if (sp) sp->vslot = j & 1;
 }
 
 void fill_tpass_common(TpassParams& tp, const Plan& P, void* ws) {
@@ -595,7 +597,7 @@ sfseg_status ph_finalize(Rank& r, int k, cudaStream_t st) {
 }
 
 sfseg_status ph_T(Rank& r, int k, cudaStream_t st) {
-  set_tpass_vmax(r.tp, r.P, r.ws, k);
+  set_vslot(r.tp, &r.sp, r.P, r.ws, k);
   ProfScope ps(r.P.prof, st, PC_TPASS);
   SF_CUDA(launch_tpass_fwd(r.P.RT, r.tp, (int)r.P.B, st));
   SF_CUDA(after_launch("tpass(slab)", st));
@@ -918,6 +920,7 @@ sfseg_status bw_step(BwdRank& q, int k, cudaStream_t st) {
   Rank& r = *q.r;
   const Plan& P = r.P;
   q.tp.u1 = slab_tape_u(r, k - 1);
+  set_vslot(q.tp, &q.sp, P, r.ws, k);
   {
     ProfScope ps(P.prof, st, PC_BWD);
     SF_CUDA(launch_tpass_bwd(P.RT, q.tp, (int)P.B, st));
@@ -1347,7 +1350,7 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
   for (int k = 1; k <= K; ++k) {
     // (a2)+(a3) v = s_{k-1} * G_t * p_{k-1}
     {
-      set_tpass_vmax(tp, P, ws, k);
+      set_vslot(tp, &sp, P, ws, k);
       ProfScope ps(P.prof, st, PC_TPASS);
       SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
       SF_CUDA(after_launch("tpass_fwd", st));
@@ -1516,6 +1519,7 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   tp.out = v;
   for (int k = K; k >= 1; --k) {
     tp.u1 = tape_u(k - 1);
+    set_vslot(tp, &sp, P, ws, k);
     {
       ProfScope ps(P.prof, st, PC_BWD);
       SF_CUDA(launch_tpass_bwd(P.RT, tp, (int)P.B, st));
@@ -1722,6 +1726,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   const int fexp[3] = {0, 2, 1};  // G*(S^p X), G*(F^2 S^p X), G*(F S^p X)
   for (int k = 1; k <= K; ++k) {
     for (int c = 0; c < 3; ++c) {
+      set_vslot(tp, &sp, P, ws, 3 * (k - 1) + c);
       {
         ProfScope ps(P.prof, st, PC_TPASS);
         if (fexp[c] == 0) {

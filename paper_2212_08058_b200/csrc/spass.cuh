@@ -98,6 +98,8 @@ struct SpassParams {
                            //   (time-slab schedule: boundary frames first, interior after); U = B t_cnt S NB
   int lag;                 // FWD: v came unscaled (lagged normalisation): u *= s_{k-1} = sc[SC_S] here
   int loc_acc;             // time-slab mode: add this launch's sums to loc (later launches of one iteration)
+  int vslot;               // fp16 tensor-core pass: max |v| in sc[SC_VMAX + vslot] (written by the temporal
+                           //   pass that produced v); the pass zeroes slot vslot ^ 1 for the next pair
   float g[kMaxRS + 1];     // g[d] = weight of spatial offset +-d (same taps for y and x)
 };
 

@@ -132,7 +132,6 @@ enum SptcEpi : int { EPI_PLAIN = 0, EPI_FWD = 1, EPI_FWD_OPT = 2 };  // OPT: tap
 
 template <int R, int EPI, int FMT>
 __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid_constant__ SpassParams P) {
-  static_assert(FMT == 0 || EPI != EPI_PLAIN, "the fp16 format needs the forward's per-volume range (SC_VMAX)");
   constexpr int BOXW = sptc_boxw(R);
   constexpr int RA = spass_ra(R);
   constexpr int NKX = sptc_nkx(R);
@@ -204,9 +203,9 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
         for (int q = 0; q < PL; ++q) bx[q][par][s][j] = pp[q];
       }
   if (FMT && blockIdx.x == 0 && tid == 0) {
-    // the slot the NEXT iteration's temporal pass will max into (this iteration's
-    // slot was filled by the temporal pass that produced v)
-    for (int b = 0; b < P.B; ++b) *reinterpret_cast<unsigned*>(P.sc + b * kScal + SC_VMAX + ((P.k + 1) & 1)) = 0u;
+    // the slot the NEXT temporal pass will max into (this pass's slot, vslot, was filled
+    // by the temporal pass that produced v)
+    for (int b = 0; b < P.B; ++b) *reinterpret_cast<unsigned*>(P.sc + b * kScal + SC_VMAX + (P.vslot ^ 1)) = 0u;
   }
   __syncthreads();
 
@@ -277,7 +276,7 @@ __global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid
       cur_vol = vol;
       if (!plain && P.lag) lag_s = (float)P.sc[vol * kScal + SC_S];
       if (FMT) {
-        const float vmax = __uint_as_float(*reinterpret_cast<const unsigned*>(P.sc + vol * kScal + SC_VMAX + (P.k & 1)));
+        const float vmax = __uint_as_float(*reinterpret_cast<const unsigned*>(P.sc + vol * kScal + SC_VMAX + P.vslot));
         int ex = 0;
         if (vmax > 0.f && vmax <= 3.4e38f) frexpf(vmax, &ex);  // max |v| < 2^ex
         const int e = min(max(14 - ex, -100), 100);

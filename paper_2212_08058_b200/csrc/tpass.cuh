@@ -29,7 +29,7 @@ struct TpassParams {
   const float* halo_hi;  // [B][RT][H][Wp] frames t = T..T+RT-1 or null
   float* out;            // pitched [B*T][H][Wp]
   const double* sc;      // per-volume scalars [B][kScal]
-  unsigned* vmax;        // FWD: atomicMax of max |out| per volume (float bits, stride 2 kScal words) or null
+  unsigned* vmax;        // atomicMax of max |out| per volume (float bits, stride 2 kScal words) or null
   int lag;               // FWD: no scale (the spatial pass applies s_{k-1}: lagged normalisation, time slabs)
   long frame4;           // H*Wp/4 float4 per frame
   int T;
@@ -174,18 +174,15 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
       const int t = jp - 2 * RT;
       if (active && t >= 0 && t < T) {
         const float4 o = f4_scale(acc[slot0], scale);
-        if (MODE == TP_FWD) {
-          st_f4_hint(out + (long)t * P.frame4, o, pol);
-          vm = fmaxf(vm, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
-        } else {
-          __stcg(out + (long)t * P.frame4, o);
-        }
+        if (MODE == TP_FWD) st_f4_hint(out + (long)t * P.frame4, o, pol);
+        else __stcg(out + (long)t * P.frame4, o);
+        vm = fmaxf(vm, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
       }
       acc[slot0] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   cp_async_wait<0>();
-  if (MODE == TP_FWD && P.vmax) {  // max |v| of the volume: the fp16 spatial pass's range (max is order-free)
+  if (P.vmax) {  // max |out| of the volume: the fp16 spatial pass's range (max is order-free)
     __shared__ unsigned wm[kTpThreads / 32];
     const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(vm));
     if ((tid & 31) == 0) wm[tid >> 5] = m;

@@ -66,7 +66,8 @@ class SlabSolver:
                  device="cuda", want_tape: bool = False, serial: bool = False, algo: int = 0):
         self.comm, self.shape = comm, tuple(int(v) for v in local_shape)
         # overlapped schedule (halo exchange under the interior frames, lagged allreduce) unless serial
-        self.opt = _options(int(algo), slab_schedule=1 if serial else 0)
+        self.algo, self.serial = int(algo), bool(serial)
+        self.profiler = None   # optional sf.Profiler (per-pass event timing, benchmark instrumentation)
         self.C, self.gauss, self.K = int(C_), gauss, int(K)
         self.dist = DistC(comm.handle, int(T_global), int(t_offset))
         n = C.c_size_t(0)
@@ -86,10 +87,11 @@ class SlabSolver:
         if x_out is None:
             x_out = torch.empty(self.shape, dtype=torch.float32, device=self.device)
         _require(x_out, "x_out", 4, shape=self.shape, device=self.device)
+        opt = _options(self.algo, self.profiler, slab_schedule=1 if self.serial else 0)
         _check(lib().sfseg_power_iterate_ex(
             _ptr(ch), self.C, _weights(w, self.C), float(b), int(act), Shape(*self.shape), self.gauss.c(), self.K,
             None, _ptr(x_out), None, _ptr(self.stats), 0, _ptr(self.tape), _ptr(self.ws), self.ws_bytes,
-            C.byref(self.dist), C.byref(self.opt), _stream(stream)), "sfseg_power_iterate(dist)")
+            C.byref(self.dist), C.byref(opt), _stream(stream)), "sfseg_power_iterate(dist)")
         if check:
             self.sync(stream)
         return x_out

@@ -87,7 +87,9 @@ def test_nccl_single_rank_dist_path(sf):
         gr = torch.from_numpy(np.random.default_rng(2).normal(size=(1, 12, 60, 100)).astype(np.float32)).cuda()
         dwd, dbd = sb.backward(ch, [1.3], gr, 0.1, 1)
         _, dw1, db1 = sf.power_iterate_backward(ch, [1.3], g, 6, gr, 0.1, 1)
-        assert abs(dwd[0] - dw1[0]) <= 1e-5 * abs(dw1[0]) and abs(dbd - db1) <= 1e-5 * abs(db1)
+        # the slab forward's lagged normalisation rounds u differently from the single-GPU forward
+        scale = max(abs(dw1[0]), abs(db1))
+        assert abs(dwd[0] - dw1[0]) <= 1e-4 * scale and abs(dbd - db1) <= 1e-4 * scale
         # a bad argument on a rank is agreed on before any data-path collective (returns, no hang)
         with pytest.raises(sf.SfsegError):
             sb.backward(ch, [float("nan")], gr, 0.1, 1)
@@ -121,7 +123,7 @@ def test_slab_backward_matches_single_gpu_and_oracle(sf, name, shape, nslabs, ac
     dwo, dbo = O.power_iterate_backward(wl.ch, w, b, act, O.gaussian_taps(cfg.sigma_t, cfg.radius_t),
                                         O.gaussian_taps(cfg.sigma_s, cfg.radius_s), K, gr.astype(np.float64))
     assert _rel(dws, np.array(dwo)) <= 1e-3
-    assert _rel(dws, np.array(dw1)) <= 1e-5     # same arithmetic, different reduction order
+    assert _rel(dws, np.array(dw1)) <= 1e-4     # lagged normalisation + reduction order
     assert abs(dbs - dbo) <= 1e-3 * max(abs(dbo), np.abs(dwo).max())
     assert _rel(xs.cpu().numpy(), x1.cpu().numpy()) <= 1e-6
 
