@@ -413,7 +413,7 @@ def power_iterate_slabs(ch: torch.Tensor, w, gauss: Gauss, K: int, nslabs: int, 
     if want_tape:
         tb = C.c_size_t(0)
         _check(lib().sfseg_slabs_tape_bytes(shp, Cn, g, int(K), nsl, C.byref(tb)), "sfseg_slabs_tape_bytes")
-        tape = _alloc_bytes(tb.value, ch.device)
+        tape = torch.zeros(max(tb.value, 256), dtype=torch.uint8, device=ch.device)  # padding bytes defined
     x = torch.empty((B, T, H, W), dtype=torch.float32, device=ch.device)
     stats = torch.zeros((B, int(K), 3), dtype=torch.float64, device=ch.device)
     if x0 is not None:

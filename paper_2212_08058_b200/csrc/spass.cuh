@@ -201,9 +201,32 @@ __device__ __forceinline__ Seg seg_decode(long u, long u_end, int NB, int S) {
   g.yb1 = (int)min((long)NB, (long)g.yb0 + (u_end - u));
   return g;
 }
+#ifndef SPASS_CHUNK
+#define SPASS_CHUNK 0  // A/B: > 0 walks each frame in bands of SPASS_CHUNK blocks across all strips
+#endif
 // the same with a frame range (P.t_cnt > 0): unit frame index -> volume frame b T + t_lo + t
 __device__ __forceinline__ Seg seg_decode(const SpassParams& P, long u, long u_end) {
+#if SPASS_CHUNK > 0
+  // frame-major; inside a frame, band c (blocks [c CH, c CH + len)) of strip 0, 1, ..., S - 1:
+  // horizontally adjacent strips of the same rows run back to back (their x-halo re-reads of
+  // v hit L2) at the cost of PRO extra x-blocks per band
+  Seg g;
+  {
+    constexpr int CH = SPASS_CHUNK;
+    const int NB = P.NB, S = P.S;
+    const long per = (long)S * NB;
+    g.bt = (int)(u / per);
+    const long r = u - (long)g.bt * per;
+    const int c = (int)min(r / ((long)CH * S), (long)((NB - 1) / CH));
+    const int len = min(CH, NB - c * CH);
+    const long r2 = r - (long)c * CH * S;
+    g.s = (int)(r2 / len);
+    g.yb0 = c * CH + (int)(r2 - (long)g.s * len);
+    g.yb1 = (int)min((long)(c * CH + len), (long)g.yb0 + (u_end - u));
+  }
+#else
   Seg g = seg_decode(u, u_end, P.NB, P.S);
+#endif
   if (P.t_cnt > 0) {
     const int b = g.bt / P.t_cnt;
     g.bt = b * P.T + P.t_lo + (g.bt - b * P.t_cnt);

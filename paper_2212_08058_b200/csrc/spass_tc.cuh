@@ -81,8 +81,11 @@ __host__ __device__ constexpr int sptc_stages(int R, int fmt = 0) {
 __host__ __device__ constexpr size_t sptc_smem_bytes(int R, int fmt = 0) {
   return sptc_smem_for(R, sptc_stages(R, fmt), fmt);
 }
+#ifndef SPTC_LB
+#define SPTC_LB 3  // resident CTAs per SM the register budget is sized for (launch bounds)
+#endif
 __host__ __device__ constexpr int sptc_ctas_per_sm(int R, int fmt = 0) {
-  return spass_fit_n(sptc_smem_bytes(R, fmt)) < 3 ? spass_fit_n(sptc_smem_bytes(R, fmt)) : 3;
+  return spass_fit_n(sptc_smem_bytes(R, fmt)) < SPTC_LB ? spass_fit_n(sptc_smem_bytes(R, fmt)) : SPTC_LB;
 }
 
 template <int FMT = 0>
@@ -131,7 +134,7 @@ __device__ __forceinline__ float sptc_w(const float* gsm, int d, int R) {
 enum SptcEpi : int { EPI_PLAIN = 0, EPI_FWD = 1, EPI_FWD_OPT = 2 };  // OPT: tape and/or Rayleigh
 
 template <int R, int EPI, int FMT>
-__global__ void __launch_bounds__(kSpassThreads, 3) spass_tc_kernel(const __grid_constant__ SpassParams P) {
+__global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const __grid_constant__ SpassParams P) {
   constexpr int BOXW = sptc_boxw(R);
   constexpr int RA = spass_ra(R);
   constexpr int NKX = sptc_nkx(R);

@@ -16,6 +16,12 @@ r = d["roofline"]
 print(f"{sys.argv[1] or 'default':40s} ms/step {d['ms_per_step']:.3f}  spass {r['launch_ms']*1e3:.1f} us  "
       f"tpass {r.get('tpass', {}).get('launch_ms', 0)*1e3:.1f} us  value {d['value']:.3e}")
 PY
+  if [ -n "$NCU" ]; then   # DRAM bytes of one spatial-pass launch (after the plain run exited 0)
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+      -k regex:spass_tc -s 16 -c 1 python bench.py --no-cpu-baseline --no-e2e --steps 2 --warmup 1 \
+      > $OUT/ncu_$i.log 2>&1
+    grep -E "dram__bytes|gpu__time" $OUT/ncu_$i.log | sed "s/^/  [$i] /" >> $OUT/summary.txt
+  fi
   i=$((i+1))
 done
 unset SFSEG_NVCC_DEFS
