@@ -110,6 +110,9 @@ __device__ __forceinline__ void tc_split(float a, float b, uint32_t (&o)[PL]) {
 // 2^e as a float for |e| <= 126 (exact)
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 constexpr int kF16TapExp = 12;  // FMT = 1: taps scaled by 2^12
+#ifndef SPTC_F16_ACC3
+#define SPTC_F16_ACC3 0  // A/B: FMT = 1 with the two correction products in separate accumulators
+#endif
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -327,11 +330,15 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
       // The tensor core truncates each accumulation to the accumulator's magnitude, so the
       // corrections (<= 2^-8 of the result) are summed in their own accumulator and added
       // with one round-to-nearest FADD: 4 instead of 24 full-magnitude truncations per pass.
-      float acc[4][4], acs[4][4];
+      constexpr bool A3 = FMT && SPTC_F16_ACC3;
+      float acc[4][4], acs[4][4], ac2[A3 ? 4 : 1][4];
 #pragma unroll
       for (int nl = 0; nl < 4; ++nl)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[nl][i] = acs[nl][i] = 0.f;
+        for (int i = 0; i < 4; ++i) {
+          acc[nl][i] = acs[nl][i] = 0.f;
+          if (A3) ac2[A3 ? nl : 0][i] = 0.f;
+        }
       // ring slot of each x-block of this y window (x-blocks m .. m + PRO)
       uint32_t slot_addr[PRO + 1];
       {
@@ -365,14 +372,15 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
 #pragma unroll
           for (int nl = 0; nl < 4; ++nl) {
             const uint4& a = ay[sptc_pb(p)];
-            mma16816<FMT>(p == 0 ? acc[nl] : acs[nl], a.x, a.y, a.z, a.w, bq[sptc_pa(p)][2 * nl],
-                          bq[sptc_pa(p)][2 * nl + 1]);
+            mma16816<FMT>(p == 0 ? acc[nl] : (A3 && p == 2) ? ac2[A3 ? nl : 0] : acs[nl], a.x, a.y, a.z, a.w,
+                          bq[sptc_pa(p)][2 * nl], bq[sptc_pa(p)][2 * nl + 1]);
           }
       }
 #pragma unroll
       for (int nl = 0; nl < 4; ++nl)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[nl][i] = (acc[nl][i] + acs[nl][i]) * (FMT ? usc : lag_s);
+        for (int i = 0; i < 4; ++i)
+          acc[nl][i] = (acc[nl][i] + (A3 ? acs[nl][i] + ac2[A3 ? nl : 0][i] : acs[nl][i])) * (FMT ? usc : lag_s);
       // epilogue
       float s0 = 0.f, s1 = 0.f;
       const int yb = (sg.yb0 + m) * kM + 16 * mt + g;
@@ -412,11 +420,15 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
       const bool live = (row0 + kM > 0) && (row0 < H);
       const int slot_row = (n % NSLOT) * kM + 16 * mt + g;
       if (wlive) {
-        float acc[4][4], acs[4][4];  // leading product / corrections (see the y-pass)
+        constexpr bool A3 = FMT && SPTC_F16_ACC3;
+        float acc[4][4], acs[4][4], ac2[A3 ? 4 : 1][4];  // leading product / corrections (see the y-pass)
 #pragma unroll
         for (int nl = 0; nl < 4; ++nl)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[nl][i] = acs[nl][i] = 0.f;
+          for (int i = 0; i < 4; ++i) {
+            acc[nl][i] = acs[nl][i] = 0.f;
+            if (A3) ac2[A3 ? nl : 0][i] = 0.f;
+          }
         if (live) {
           const int st = (NST == 2) ? (cseq & 1) : 0;
           mbar_wait(&bars[st], (NST == 2) ? ((cseq >> 1) & 1) : (cseq & 1));
@@ -451,7 +463,8 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
                 if (s < 0 || s >= NKX) continue;
 #pragma unroll
                 for (int par = 0; par < 2; ++par) {
-                  float(&d)[4] = p == 0 ? acc[2 * qq + par] : acs[2 * qq + par];
+                  float(&d)[4] = p == 0 ? acc[2 * qq + par]
+                                 : (A3 && p == 2) ? ac2[A3 ? 2 * qq + par : 0] : acs[2 * qq + par];
                   const int qa = sptc_pa(p);
                   const uint32_t* bb = bx[sptc_pb(p)][par][s];
                   mma16816<FMT>(d, a0[qa], a1[qa], a2[qa], a3[qa], bb[0], bb[1]);
@@ -464,7 +477,9 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
         for (int nl = 0; nl < 4; ++nl) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            acc[nl][i] = FMT ? (acc[nl][i] + acs[nl][i]) * (1.f / (float)(1 << kF16TapExp)) : acc[nl][i] + acs[nl][i];
+            acc[nl][i] = FMT ? (acc[nl][i] + (A3 ? acs[nl][i] + ac2[A3 ? nl : 0][i] : acs[nl][i])) *
+                                   (1.f / (float)(1 << kF16TapExp))
+                             : acc[nl][i] + acs[nl][i];
           const int w0 = slot_row * RSW + 4 * (4 * hh + nl) + t;
           uint32_t q0[PL], q1[PL];
           tc_split<FMT, PL>(acc[nl][0], acc[nl][1], q0);

@@ -38,6 +38,9 @@ struct TpassParams {
 };
 
 constexpr int kTpThreads = 128;
+#ifndef TPASS_REV
+#define TPASS_REV 0  // A/B: walk the frames last to first (the symmetric taps make it the same filter)
+#endif
 // Resident CTAs per SM the register budget is sized for: the ring of 2RT+1
 // float4 accumulators dominates (RT=6: 52 registers).  At c2 (frame4 = 102,720
 // float4 columns) 6 x 128 threads per SM hold every column in ONE wave.
@@ -95,15 +98,22 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
 
   // jp = j + RT enumerates input frames j = -RT .. T+RT-1; output t = jp - 2RT
   // completes when input j = t + RT arrives.
+  // walk index j -> frame (TPASS_REV: T - 1 - j; the taps are symmetric, so the same ring
+  // computes the same filter on the mirrored sequence)
   auto frame_src = [&](int jp, int w) -> const float4* {
     const int j = jp - RT;
     if (j >= 0 && j < T) {
-      const long o = (long)j * P.frame4;
+      const long o = (long)(TPASS_REV ? T - 1 - j : j) * P.frame4;
       return (w == 0) ? src + o : (w == 1 ? Fp + o : U1 + o);
     }
     if (HALO && w == 0) {  // neighbour slab frames (time-slab sharding)
-      if (j < 0 && j >= -RT && hlo) return hlo + (long)(j + RT) * P.frame4;
-      if (j >= T && j < T + RT && hhi) return hhi + (long)(j - T) * P.frame4;
+      if (TPASS_REV) {
+        if (j < 0 && j >= -RT && hhi) return hhi + (long)(-1 - j) * P.frame4;
+        if (j >= T && j < T + RT && hlo) return hlo + (long)(T - 1 - j + RT) * P.frame4;
+      } else {
+        if (j < 0 && j >= -RT && hlo) return hlo + (long)(j + RT) * P.frame4;
+        if (j >= T && j < T + RT && hhi) return hhi + (long)(j - T) * P.frame4;
+      }
     }
     return nullptr;  // zero padding
   };
@@ -174,8 +184,9 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
       const int t = jp - 2 * RT;
       if (active && t >= 0 && t < T) {
         const float4 o = f4_scale(acc[slot0], scale);
-        if (MODE == TP_FWD) st_f4_hint(out + (long)t * P.frame4, o, pol);
-        else __stcg(out + (long)t * P.frame4, o);
+        float4* dst = out + (long)(TPASS_REV ? T - 1 - t : t) * P.frame4;
+        if (MODE == TP_FWD) st_f4_hint(dst, o, pol);
+        else __stcg(dst, o);
         vm = fmaxf(vm, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
       }
       acc[slot0] = make_float4(0.f, 0.f, 0.f, 0.f);
