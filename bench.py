@@ -367,11 +367,14 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]   # per-step ends (median / min)
     e0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         timed_step()
+        ev[i].record(stream)
     e1.record(stream)
     torch.cuda.synchronize(dev)
+    step_ms = [e0.elapsed_time(ev[0])] + [ev[i - 1].elapsed_time(ev[i]) for i in range(1, args.steps)]
     (fsolver if full else solver).sync()   # device errors of the timed steps (sticky error word)
     if world > 1:
         dist.barrier()
@@ -593,6 +596,10 @@ def run_ours(args):
                        "arithmetic": arith,
                        "l2": "inputs > L2 (ch 115 MB + F/p/v 344 MB vs 126 MB L2); no flush",
                        "launch": "one CUDA graph per step" if graph is not None else "stream launches"},
+            "step_ms": {"median": float(statistics.median(step_ms)), "min": float(min(step_ms)),
+                        "max": float(max(step_ms)), "rank": rank},
+            "once_per_solve_ms_per_step": prof["once"][0] / args.steps,   # combine + final scale (events)
+            "path_hbm_frac_12B_nameplate_8TBs": 12.0 * value / world / 1e9 / 8000.0,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": n_launch + (int(prof["backward"][1]) + 2 * args.steps if train else 0),
             "clocks": {k: ck[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},

@@ -1284,8 +1284,11 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
   cp.F = F;
   cp.p0 = p;
   cp.F_out = F_out;
-  combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
-  SF_CUDA(after_launch("combine", st));
+  {
+    ProfScope ps(P.prof, st, PC_ONCE);
+    combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
+    SF_CUDA(after_launch("combine", st));
+  }
 
   if (P.f3d) {
     // single-pass fused 3D iteration: p_{k-1} -> p_k ping-pong between the p and v buffers
@@ -1400,6 +1403,7 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
   if (P.kappa(K) > 0.f) return SFSEG_OK;   // x_out = the last binarised iterate (values in (0,1))
   // (a8) x_K = y_K / nu_K (dense output)
   {
+    ProfScope ps(P.prof, st, PC_ONCE);
     dim3 grid((unsigned)P.gx, (unsigned)P.BT);
     final_scale_kernel<<<grid, kEwThreads, 0, st>>>(p, x_out, at<double>(ws, P.off_sc), (int)P.T, (int)P.H, (int)P.W,
                                                     (int)P.Wp, (int)P.T, 0);
