@@ -4,9 +4,9 @@
 //
 //   X_crt = S^p [ (alpha^-1 - F^2) G*(S^p X) - G*(F^2 S^p X) + 2 F G*(F S^p X) ]
 //
-// per iteration: three temporal passes (tpass TP_FWDF: inputs a, F a, F^2 a with
-// a = S^p X carried as the stored iterate and the normaliser folded in), three
-// spatial passes (spass, plain mode: u = G_s v), then this file's epilogue
+// per iteration: one stacked temporal pass (tpass3_kernel: inputs a, F^2 a, F a with
+// a = S^p X carried as the stored iterate and the normaliser folded in; a and F read
+// once), three spatial passes (spass, plain mode: u = G_s v), then this file's epilogue
 // combining the three filtered volumes per voxel (+ norm partials).  Eq.9 gives
 // S and F (combine_full_kernel); x_0 = S (Alg.1 line 3) or a user x0.
 #pragma once
@@ -96,6 +96,7 @@ struct FullEpiParams {
   unsigned* err;
   double* stats;
   int B, T, H, Wp, W, K, k, last, gx;
+  int zero_vmax;        // zero the stacked temporal pass's three max |v| slots (fp16 spatial passes)
   float inv_alpha;
 };
 
@@ -108,6 +109,9 @@ __global__ void __launch_bounds__(kEwThreads) full_epilogue_kernel(const __grid_
   const int b = bt / P.T, t = bt - b * P.T;
   const long HWp = (long)P.H * P.Wp;
   const long W4 = P.Wp / 4;
+  if (P.zero_vmax && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)  // the three spatial passes are done
+    for (int v = 0; v < P.B; ++v)
+      for (int c = 0; c < 3; ++c) *reinterpret_cast<unsigned*>(P.sc + v * kScal + SC_VMAX + c) = 0u;
   double acc = 0.0;
   for (int y = blockIdx.x; y < P.H; y += P.gx) {
     for (long x4 = threadIdx.x; x4 < W4; x4 += kEwThreads) {

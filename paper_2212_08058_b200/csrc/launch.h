@@ -13,6 +13,7 @@ cudaError_t launch_spass_bwd(int R, const SpassParams& P, int grid, cudaStream_t
 cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_fwdf(int RT, const TpassParams& P, int B, cudaStream_t st);
+cudaError_t launch_tpass3(int RT, const Tpass3Params& P, int B, cudaStream_t st);
 bool spass_tc_supported(int R);
 int spass_tc_occupancy(int R, int fmt = 0);
 int spass_tc_boxw(int R);

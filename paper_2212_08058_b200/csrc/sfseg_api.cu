@@ -465,7 +465,10 @@ cudaError_t launch_spass_forward(const Plan& P, SpassParams& sp, cudaStream_t st
 // Every pair whose spatial pass runs in the fp16 format must go through this.
 void set_vslot(TpassParams& tp, SpassParams* sp, const Plan& P, void* ws, int j) {
   tp.vmax = P.f16 ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + (j & 1)) : nullptr;
-  if (sp) sp->vslot = j & 1;
+  if (sp) {
+    sp->vslot = j & 1;
+    sp->vzero = ((j & 1) ^ 1) + 1;
+  }
 }
 
 void fill_tpass_common(TpassParams& tp, const Plan& P, void* ws) {
@@ -1661,8 +1664,12 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   float* U = at<float>(ws, L.off_U);
   float* F = at<float>(ws, L.off_F);
   float* a = at<float>(ws, L.off_a);
-  float* v = at<float>(ws, L.off_v);
-  float* uo[3] = {at<float>(ws, L.off_ua), at<float>(ws, L.off_ub), at<float>(ws, L.off_uc)};
+  // four volumes for the three temporal outputs v_c and spatial outputs u_c: each spatial
+  // pass writes over a v already consumed (buffers 0..3 = off_v, off_ua, off_ub, off_uc)
+  float* buf[4] = {at<float>(ws, L.off_v), at<float>(ws, L.off_ua), at<float>(ws, L.off_ub),
+                   at<float>(ws, L.off_uc)};
+  float* vin[3] = {buf[0], buf[2], buf[3]};   // G_t*(a), G_t*(F^2 a), G_t*(F a)
+  float* uo[3] = {buf[1], buf[0], buf[2]};    // u_a over a free buffer, u_b over v_a, u_c over v_b
 
   // Eq.9 for S and F, U = S^p, a_0 = U x_0, ||x_0||
   CombineFullParams cp;
@@ -1697,15 +1704,23 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
 
   SpassParams sp;
   std::memset(&sp, 0, sizeof(sp));
-  if (!make_spass_fwd_tmap(&sp.tmap, P, v)) return SFSEG_ERR_CUDA;
+  CUtensorMap vmap[3];
+  for (int c = 0; c < 3; ++c)
+    if (!make_spass_fwd_tmap(&vmap[c], P, vin[c])) return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.plain = 1;
-  TpassParams tp;
+  Tpass3Params tp;
   std::memset(&tp, 0, sizeof(tp));
-  fill_tpass_common(tp, P, ws);
-  tp.src = a;
+  tp.a = a;
   tp.F = F;
-  tp.out = v;
+  for (int c = 0; c < 3; ++c) {
+    tp.out[c] = vin[c];
+    tp.vmax[c] = P.f16 ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + c) : nullptr;
+  }
+  tp.sc = at<double>(ws, P.off_sc);
+  tp.frame2 = P.H * P.Wp / 2;
+  tp.T = (int)P.T;
+  for (int i = 0; i < 2 * P.RT + 1; ++i) tp.g[i] = P.gt[i];
   FullEpiParams ep;
   std::memset(&ep, 0, sizeof(ep));
   ep.ua = uo[0];
@@ -1726,21 +1741,18 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   ep.W = (int)P.W;
   ep.K = K;
   ep.gx = P.gx;
+  ep.zero_vmax = P.f16 ? 1 : 0;
   ep.inv_alpha = (float)(1.0 / alpha);
-  const int fexp[3] = {0, 2, 1};  // G*(S^p X), G*(F^2 S^p X), G*(F S^p X)
   for (int k = 1; k <= K; ++k) {
+    {  // G_t*(S^p X), G_t*(F^2 S^p X), G_t*(F S^p X) in one pass over a and F
+      ProfScope ps(P.prof, st, PC_TPASS);
+      SF_CUDA(launch_tpass3(P.RT, tp, (int)P.B, st));
+      SF_CUDA(after_launch("tpass3_full", st));
+    }
     for (int c = 0; c < 3; ++c) {
-      set_vslot(tp, &sp, P, ws, 3 * (k - 1) + c);
-      {
-        ProfScope ps(P.prof, st, PC_TPASS);
-        if (fexp[c] == 0) {
-          SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
-        } else {
-          tp.fexp = fexp[c];
-          SF_CUDA(launch_tpass_fwdf(P.RT, tp, (int)P.B, st));
-        }
-        SF_CUDA(after_launch("tpass_full", st));
-      }
+      sp.tmap = vmap[c];
+      sp.vslot = c;
+      sp.vzero = 0;   // the epilogue zeroes the three slots
       sp.out = uo[c];
       sp.k = k;
       {

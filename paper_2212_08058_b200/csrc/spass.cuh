@@ -99,7 +99,9 @@ struct SpassParams {
   int lag;                 // FWD: v came unscaled (lagged normalisation): u *= s_{k-1} = sc[SC_S] here
   int loc_acc;             // time-slab mode: add this launch's sums to loc (later launches of one iteration)
   int vslot;               // fp16 tensor-core pass: max |v| in sc[SC_VMAX + vslot] (written by the temporal
-                           //   pass that produced v); the pass zeroes slot vslot ^ 1 for the next pair
+                           //   pass that produced v)
+  int vzero;               // > 0: the pass zeroes slot vzero - 1 for the next temporal pass (hot path:
+                           //   the other parity); 0: none (the full operator's epilogue zeroes its slots)
   float g[kMaxRS + 1];     // g[d] = weight of spatial offset +-d (same taps for y and x)
 };
 

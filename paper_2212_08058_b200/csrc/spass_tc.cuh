@@ -208,10 +208,10 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
 #pragma unroll
         for (int q = 0; q < PL; ++q) bx[q][par][s][j] = pp[q];
       }
-  if (FMT && blockIdx.x == 0 && tid == 0) {
+  if (FMT && P.vzero > 0 && blockIdx.x == 0 && tid == 0) {
     // the slot the NEXT temporal pass will max into (this pass's slot, vslot, was filled
     // by the temporal pass that produced v)
-    for (int b = 0; b < P.B; ++b) *reinterpret_cast<unsigned*>(P.sc + b * kScal + SC_VMAX + (P.vslot ^ 1)) = 0u;
+    for (int b = 0; b < P.B; ++b) *reinterpret_cast<unsigned*>(P.sc + b * kScal + SC_VMAX + P.vzero - 1) = 0u;
   }
   __syncthreads();
 

@@ -207,4 +207,114 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   }
 }
 
+// ------------------------------------------------------------------ full operator, three inputs
+// Row f1's three temporal passes in one ("three linearly independent inputs
+// share one G"): reads the stored iterate a and F once per frame and writes
+//   out_a = s G_t*(a),  out_b = s G_t*(F^2 a),  out_c = s G_t*(F a)   (s = SC_S),
+// 20 B/voxel instead of the 32 B of three single-input passes.  One float2 column per thread
+// (three register rings of 2RT+1 float2), 8-byte cp.async prefetch of a and F.
+struct Tpass3Params {
+  const float* a;          // pitched [B*T][H][Wp]
+  const float* F;
+  float* out[3];
+  unsigned* vmax[3];       // per-output max |out| slots (fp16 spatial pass) or null
+  const double* sc;
+  long frame2;             // H*Wp/2 float2 per frame
+  int T;
+  float g[2 * kMaxRT + 1];
+};
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constant__ Tpass3Params P) {
+  constexpr int NR = 2 * RT + 1;
+  constexpr int NS = 8;
+  __shared__ float2 sq[NS][2][kTpThreads];
+  const int b = blockIdx.y;
+  const int tid = threadIdx.x;
+  const long e = (long)blockIdx.x * kTpThreads + tid;
+  const bool active = e < P.frame2;
+  const int T = P.T;
+  const long vol2 = (long)T * P.frame2;
+  const long ec = active ? e : 0;
+  const float2* A = reinterpret_cast<const float2*>(P.a) + b * vol2 + ec;
+  const float2* Fp = reinterpret_cast<const float2*>(P.F) + b * vol2 + ec;
+  const float scale = (float)P.sc[b * kScal + SC_S];
+  const int jend = T + 2 * RT;
+  auto issue = [&](int jp) {
+    const int j = jp - RT;
+    if (jp < jend && j >= 0 && j < T) {
+      cp_async8(&sq[jp % NS][0][tid], A + (long)j * P.frame2);
+      cp_async8(&sq[jp % NS][1][tid], Fp + (long)j * P.frame2);
+    }
+    cp_async_commit();
+  };
+  float2 acc[3][NR];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < NR; ++i) acc[c][i] = make_float2(0.f, 0.f);
+  float vm[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int d = 0; d < NS; ++d) issue(d);
+  for (int j0 = 0; j0 < jend; j0 += NR) {
+#pragma unroll
+    for (int d = 0; d < NR; ++d) {
+      const int jp = j0 + d;
+      if (jp >= jend) break;
+      cp_async_wait<NS - 1>();
+      const int j = jp - RT;
+      float2 in[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      if (j >= 0 && j < T) {
+        const float2 a = sq[jp % NS][0][tid], f = sq[jp % NS][1][tid];
+        in[0] = a;
+        in[2] = make_float2(f.x * a.x, f.y * a.y);
+        in[1] = make_float2(f.x * in[2].x, f.y * in[2].y);  // F^2 a = F (F a)
+      }
+      issue(jp + NS);
+#pragma unroll
+      for (int ee = 0; ee < NR; ++ee) {
+        const int slot = (((d - 2 * RT + ee) % NR) + NR) % NR;
+        const float w = P.g[2 * RT - ee];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          acc[c][slot].x = fmaf(w, in[c].x, acc[c][slot].x);
+          acc[c][slot].y = fmaf(w, in[c].y, acc[c][slot].y);
+        }
+      }
+      const int slot0 = (((d - 2 * RT) % NR) + NR) % NR;
+      const int t = jp - 2 * RT;
+      if (active && t >= 0 && t < T) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float2 o = make_float2(acc[c][slot0].x * scale, acc[c][slot0].y * scale);
+          __stcg(reinterpret_cast<float2*>(P.out[c]) + b * vol2 + ec + (long)t * P.frame2, o);
+          vm[c] = fmaxf(vm[c], fmaxf(fabsf(o.x), fabsf(o.y)));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c][slot0] = make_float2(0.f, 0.f);
+    }
+  }
+  cp_async_wait<0>();
+  if (P.vmax[0]) {
+    __shared__ unsigned wm[3][kTpThreads / 32];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(vm[c]));
+      if ((tid & 31) == 0) wm[c][tid >> 5] = m;
+    }
+    __syncthreads();
+    if (tid < 3) {
+      unsigned mm = wm[tid][0];
+#pragma unroll
+      for (int i = 1; i < kTpThreads / 32; ++i) mm = max(mm, wm[tid][i]);
+      atomicMax(P.vmax[tid] + (long)b * 2 * kScal, mm);
+    }
+  }
+}
+
 }  // namespace sfseg
