@@ -432,7 +432,9 @@ def run_ours(args):
         except Exception:
             traffic = None
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    tp_bytes = 8.0 * B * T * H * W
+    # temporal pass: read p, write v (8 B/voxel); the full operator's stacked pass reads a and F
+    # and writes three outputs (20 B/voxel)
+    tp_bytes = (20.0 if full else 8.0) * B * T * H * W
     f3_ms, f3_n = prof["f3d"]
     if f3_n:
         # small radii: the fused single-pass 3D kernel is the whole iteration (HBM-bound):
