@@ -14,12 +14,13 @@ timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_r
 for c in probe c4 c3 c2f c5; do
   timeout 900 python bench.py --config $c --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err
 done
-for a in fp32 tcgen05; do
+timeout 900 python bench.py --config c5 --slab-at-1 --steps 5 --no-cpu-baseline > $OUT/bench_c5_slab1.json 2> $OUT/bench_c5_slab1.err
+for a in fp32 mma tcgen05; do
   timeout 900 python bench.py --algo $a --no-cpu-baseline --no-e2e > $OUT/bench_c2_$a.json 2> $OUT/bench_c2_$a.err
 done
 timeout 300 python tools/precision_c2.py c2 > $OUT/precision_c2.json 2> $OUT/precision_c2.err
 [ -x tools/tc05_rate ] && timeout 120 tools/tc05_rate > $OUT/tc05_rate.log 2>&1
-for c in c2 probe; do
+for c in c2 probe c3; do
   BC="python bench.py --config $c --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
   $BC > $OUT/plain_$c.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$c.csv $BC > $OUT/ncu_launches_$c.log 2>&1
