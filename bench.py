@@ -524,6 +524,8 @@ def run_ours(args):
                       "bound": "hbm"},
             "path_hbm_frac_algorithmic_12B": 12.0 * value / world / 1e9 / hbm_peak,
         }
+    if roofline.get("traffic"):   # ncu DRAM bytes per voxel of one launch (vs the algorithmic bytes)
+        roofline["traffic_bytes_per_voxel"] = roofline["traffic"] / vox
     # our kernels launched in the timed region: the passes (counted by the library's
     # event instrumentation) + combine, final scale, frame max and threshold per step
     n_launch = int(sp_n + tp_n + f3_n + 4 * args.steps)
