@@ -645,6 +645,16 @@ sfseg_status ph_S_interior(Rank& r, int k, cudaStream_t st) {
   return ph_S_range(r, k, lo, T - lo - hi, 1, st);
 }
 
+// The comm stream gets the highest priority: the spatial pass fills every SM with one wave
+// of CTAs, so the transfer kernels must be placed first when CTA slots free up (between the
+// boundary and interior launches) rather than queue behind the interior wave.
+cudaError_t create_comm_stream(cudaStream_t* s) {
+  int lo = 0, hi = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (e != cudaSuccess) return e;
+  return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, hi);
+}
+
 // Streams and events of the overlapped time-slab schedule.  Compute (st): temporal pass,
 // boundary spatial pass, interior spatial pass.  Comm (cs): the halo exchange (after the
 // boundary pass, overlapping the interior pass) and the norm allreduce + finalize (after
@@ -665,7 +675,7 @@ struct SlabSched {
     ovl = overlap;
     if (!overlap) return cudaSuccess;
     own = true;
-    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    cudaError_t e = create_comm_stream(&cs);
     for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
     return e;
   }
@@ -2079,7 +2089,7 @@ sfseg_status sfseg_comm_create(const uint8_t id_host[128], int32_t nranks, int32
     return SFSEG_ERR_CUDA;
   }
   // the overlapped time-slab schedule's comm stream and hand-off events (setup call, not a solve)
-  bool ok = cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking) == cudaSuccess;
+  bool ok = create_comm_stream(&c->cs) == cudaSuccess;
   for (int i = 0; i < 4 && ok; ++i) ok = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) == cudaSuccess;
   if (!ok || api.CommInitRank(&c->comm, nranks, id, rank) != ncclSuccess) {
     cudaFree(c->flag);
