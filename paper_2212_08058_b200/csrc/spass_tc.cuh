@@ -63,7 +63,10 @@ __host__ __device__ constexpr int sptc_nkx(int R) { return (16 + spass_ra(R) + R
 __host__ __device__ constexpr int sptc_nky(int R) { return (16 + 2 * R + 15) / 16; }
 __host__ __device__ constexpr int sptc_boxw(int R) { return 16 * (3 + sptc_nkx(R)) + 8; }  // == 8 or 24 mod 32
 __host__ __device__ constexpr int sptc_pro(int R) { return (31 + 2 * R) / 32; }
-__host__ __device__ constexpr int sptc_nslot(int R) { return sptc_pro(R) + 1; }
+#ifndef SPTC_ONEBAR
+#define SPTC_ONEBAR 0  // A/B: one more ring slot and one block barrier per 32-row block instead of two
+#endif
+__host__ __device__ constexpr int sptc_nslot(int R) { return sptc_pro(R) + 1 + SPTC_ONEBAR; }
 __host__ __device__ constexpr int sptc_planes(int fmt) { return fmt ? 2 : kTcPlanes; }
 __host__ __device__ constexpr size_t sptc_smem_for(int R, int stages, int fmt = 0) {
   return sizeof(float) * (size_t)stages * kM * sptc_boxw(R)                                // TMA stages
@@ -499,7 +502,10 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
         if (tid == 0) producer_next();
       }
       if (do_y && wlive) ypass(n - PRO, pre);
-      __syncthreads();  // ring slot (n + 1) % NSLOT may be overwritten next
+      // ring slot (n + 1) % NSLOT may be overwritten next.  SPTC_ONEBAR: that slot held x-block
+      // n - PRO - 1, whose last reader (the y-pass of the previous iteration) every warp finished
+      // before the barrier above, so no second barrier is needed
+      if (!SPTC_ONEBAR) __syncthreads();
     }
     u += nyb;
   }
