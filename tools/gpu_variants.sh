@@ -8,7 +8,7 @@ i=0
 for DEFS in "$@"; do
   export SFSEG_NVCC_DEFS="$DEFS"
   python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$i.log 2>&1
-  timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 10 --warmup 3 > $OUT/bench_$i.json 2> $OUT/bench_$i.err
+  timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 10 --warmup 3 $BENCH_ARGS > $OUT/bench_$i.json 2> $OUT/bench_$i.err
   python - "$DEFS" $OUT/bench_$i.json <<'PY' >> $OUT/summary.txt
 import json, sys
 d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
