@@ -356,6 +356,15 @@ sfseg_status sfseg_comm_destroy(sfseg_comm* comm);
  * multi-GPU solve for all slabs on `stream`: halo frames are
  * copied device-to-device and the norm partials summed in rank order.  Same
  * arguments/outputs as sfseg_power_iterate on the full dense volume (no tape). */
+/* Host only (no device work): the spatial-pass launches of one time-slab iteration of the
+ * overlapped schedule (SFSEG_SLAB_OVERLAP) for a slab of T frames with compiled
+ * temporal radius radius_t and the given neighbours, as (first frame, frame count) pairs in
+ * launch order in ranges_host[0 .. 2 n_ranges): the boundary ranges the neighbours need
+ * first (*n_boundary_host of them; the halo exchange is enqueued after these), then the
+ * interior.  The ranges tile [0, T) exactly.  Errors: SFSEG_ERR_INVALID_ARGUMENT. */
+sfseg_status sfseg_slab_launch_ranges(int32_t T, int32_t radius_t, int32_t has_lo, int32_t has_hi,
+                                      int32_t* ranges_host /*[6]*/, int32_t* n_ranges_host,
+                                      int32_t* n_boundary_host);
 sfseg_status sfseg_slabs_workspace_bytes(sfseg_shape shape, int32_t C, sfseg_gauss gauss, int32_t K,
                                          int32_t nslabs, size_t* ws_bytes_host);
 sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* w_host, float b,

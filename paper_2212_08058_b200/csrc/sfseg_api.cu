@@ -607,6 +607,37 @@ sfseg_status ph_T(Rank& r, int k, cudaStream_t st) {
   return SFSEG_OK;
 }
 
+// The spatial-pass launches of one slab iteration as (first frame, count) pairs in launch
+// order: the boundary ranges the neighbours need (the first r_t frames when there is a lower
+// neighbour, the last r_t when there is an upper one), then the interior.  With no neighbour,
+// or a slab too thin for disjoint boundary ranges, one launch covers the slab (counted as
+// boundary: the exchange waits for it).  Returns the number of ranges; *n_boundary of them
+// precede the halo exchange.
+int slab_ranges(int T, int RT, bool has_lo, bool has_hi, int32_t out[6], int32_t* n_boundary) {
+  const int lo = has_lo ? RT : 0, hi = has_hi ? RT : 0;
+  int n = 0;
+  if (lo + hi == 0 || lo + hi >= T) {
+    out[0] = 0;
+    out[1] = T;
+    *n_boundary = 1;
+    return 1;
+  }
+  if (lo > 0) {
+    out[2 * n] = 0;
+    out[2 * n + 1] = lo;
+    ++n;
+  }
+  if (hi > 0) {
+    out[2 * n] = T - hi;
+    out[2 * n + 1] = hi;
+    ++n;
+  }
+  *n_boundary = n;
+  out[2 * n] = lo;
+  out[2 * n + 1] = T - lo - hi;
+  return n + 1;
+}
+
 // Spatial pass of iteration k over frames [t_lo, t_lo + t_cnt) of every volume; acc: add the
 // launch's norm sums to loc (the later launches of one iteration, in a fixed order).
 sfseg_status ph_S_range(Rank& r, int k, int t_lo, int t_cnt, int acc, cudaStream_t st) {
@@ -627,22 +658,19 @@ sfseg_status ph_S_range(Rank& r, int k, int t_lo, int t_cnt, int acc, cudaStream
 }
 
 // The frames a rank's neighbours need (its r_t boundary frames) are computed first, so the
-// halo transfer can run while the interior frames are computed.  With no neighbour, or a
-// slab too thin for disjoint boundary ranges, one launch covers the slab.
+// halo transfer can run while the interior frames are computed (slab_ranges, exported as
+// sfseg_slab_launch_ranges for the host-logic tests).
 sfseg_status ph_S_boundary(Rank& r, int k, cudaStream_t st) {
-  const int T = (int)r.P.T, RT = r.P.RT;
-  const int lo = r.has_lo ? RT : 0, hi = r.has_hi ? RT : 0;
-  if (lo + hi == 0 || lo + hi >= T) return ph_S_range(r, k, 0, T, 0, st);
+  int32_t rg[6], nb = 0;
+  slab_ranges((int)r.P.T, r.P.RT, r.has_lo, r.has_hi, rg, &nb);
   sfseg_status s = SFSEG_OK;
-  if (lo > 0 && (s = ph_S_range(r, k, 0, lo, 0, st)) != SFSEG_OK) return s;
-  if (hi > 0) return ph_S_range(r, k, T - hi, hi, lo > 0 ? 1 : 0, st);
-  return SFSEG_OK;
+  for (int i = 0; i < nb && s == SFSEG_OK; ++i) s = ph_S_range(r, k, rg[2 * i], rg[2 * i + 1], i > 0 ? 1 : 0, st);
+  return s;
 }
 sfseg_status ph_S_interior(Rank& r, int k, cudaStream_t st) {
-  const int T = (int)r.P.T, RT = r.P.RT;
-  const int lo = r.has_lo ? RT : 0, hi = r.has_hi ? RT : 0;
-  if (lo + hi == 0 || lo + hi >= T) return SFSEG_OK;
-  return ph_S_range(r, k, lo, T - lo - hi, 1, st);
+  int32_t rg[6], nb = 0;
+  const int n = slab_ranges((int)r.P.T, r.P.RT, r.has_lo, r.has_hi, rg, &nb);
+  return n > nb ? ph_S_range(r, k, rg[2 * nb], rg[2 * nb + 1], 1, st) : SFSEG_OK;
 }
 
 // The comm stream gets the highest priority: the spatial pass fills every SM with one wave
@@ -2100,6 +2128,13 @@ sfseg_status sfseg_comm_create(const uint8_t id_host[128], int32_t nranks, int32
     return ok ? SFSEG_ERR_NCCL : SFSEG_ERR_CUDA;
   }
   *out = c;
+  return SFSEG_OK;
+}
+
+sfseg_status sfseg_slab_launch_ranges(int32_t T, int32_t radius_t, int32_t has_lo, int32_t has_hi,
+                                      int32_t* ranges_host, int32_t* n_ranges_host, int32_t* n_boundary_host) {
+  if (!ranges_host || !n_ranges_host || !n_boundary_host || T < 1 || radius_t < 0) return SFSEG_ERR_INVALID_ARGUMENT;
+  *n_ranges_host = slab_ranges(T, radius_t, has_lo != 0, has_hi != 0, ranges_host, n_boundary_host);
   return SFSEG_OK;
 }
 

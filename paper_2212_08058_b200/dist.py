@@ -40,6 +40,17 @@ def broadcast_unique_id(rank: int, group=None) -> bytes:
     return bytes(dev_buf.cpu().tolist())
 
 
+def slab_launch_ranges(T: int, radius_t: int, has_lo: bool, has_hi: bool):
+    """The spatial-pass launches of one iteration of the overlapped time-slab schedule
+    (sfseg_slab_launch_ranges, host only): ([(first frame, count), ...] in launch order,
+    number of boundary ranges launched before the halo exchange)."""
+    buf = (C.c_int32 * 6)()
+    n, nb = C.c_int32(0), C.c_int32(0)
+    _check(lib().sfseg_slab_launch_ranges(int(T), int(radius_t), int(bool(has_lo)), int(bool(has_hi)), buf,
+                                          C.byref(n), C.byref(nb)), "sfseg_slab_launch_ranges")
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(n.value)], nb.value
+
+
 class Comm:
     """sfseg_comm (NCCL communicator created from a broadcast unique id)."""
 

@@ -158,3 +158,61 @@ def test_slab_decomposition_equals_oracle(world, T):
     np.testing.assert_allclose(x, xo, rtol=0, atol=1e-13)
     for r in res:
         np.testing.assert_allclose(r[1][2], st["nu"], rtol=1e-13)
+
+
+def _frames(ranges):
+    out = []
+    for t0, n in ranges:
+        out.extend(range(t0, t0 + n))
+    return out
+
+
+def test_overlapped_schedule_launch_ranges():
+    """The overlapped schedule's spatial-pass launches (the library's own host logic,
+    sfseg_slab_launch_ranges) tile the slab exactly once, and every frame a neighbour needs
+    as halo is computed before the exchange; thin slabs collapse to one launch."""
+    from paper_2212_08058_b200.dist import slab_launch_ranges
+    for T in (1, 5, 6, 7, 12, 13, 19, 64, 70):
+        for RT in (0, 1, 3, 6, 9):
+            for lo in (False, True):
+                for hi in (False, True):
+                    rg, nb = slab_launch_ranges(T, RT, lo, hi)
+                    fr = _frames(rg)
+                    assert sorted(fr) == list(range(T)) and len(fr) == T, (T, RT, lo, hi, rg)
+                    assert 1 <= nb <= len(rg) and all(n > 0 for _, n in rg)
+                    before = set(_frames(rg[:nb]))
+                    need = set()
+                    if lo:
+                        need |= set(range(min(RT, T)))
+                    if hi:
+                        need |= set(range(max(0, T - RT), T))
+                    assert need <= before, (T, RT, lo, hi, rg, nb)
+                    if 0 < (RT if lo else 0) + (RT if hi else 0) < T:
+                        assert len(rg) == nb + 1     # an interior launch overlaps the exchange
+                    else:
+                        assert rg == [(0, T)] and nb == 1
+
+
+def _ranges_rank(rank, world, T_global, RT):
+    from paper_2212_08058_b200.dist import slab_launch_ranges
+    t0, t1 = slab_range(T_global, world, rank)
+    rg, nb = slab_launch_ranges(t1 - t0, RT, rank > 0, rank < world - 1)
+    # global frames this rank computes before its exchange, and the halo frames it receives
+    sent = sorted(t0 + f for f in _frames(rg[:nb]))
+    recv = []
+    if rank > 0:
+        recv += list(range(t0 - RT, t0))
+    if rank < world - 1:
+        recv += list(range(t1, t1 + RT))
+    g = [None] * world
+    dist.all_gather_object(g, (sent, recv))
+    # every halo frame a rank receives was computed by its owner before the owner's exchange
+    for r in range(world):
+        owner_sent = set().union(*[set(g[o][0]) for o in range(world) if o != r])
+        assert set(g[r][1]) <= owner_sent, (r, g)
+    return True
+
+
+@pytest.mark.parametrize("world,T,RT", [(2, 70, 6), (3, 64, 9), (4, 40, 6)])
+def test_overlapped_schedule_halo_frames_ready_before_exchange(world, T, RT):
+    assert all(r[1] for r in _run(_ranges_rank, world, T, RT))
