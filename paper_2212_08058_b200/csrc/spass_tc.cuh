@@ -407,13 +407,7 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
           const float2 yv = make_float2(f.x * uu.x, f.y * uu.y);
           s0 = fmaf(yv.x, yv.x, fmaf(yv.y, yv.y, s0));
           if (EPI == EPI_FWD_OPT && pprev) s1 = fmaf(pr.a[nl][i].x, uu.x, fmaf(pr.a[nl][i].y, uu.y, s1));
-#ifndef SPTC_TAPE_CS
-#define SPTC_TAPE_CS 0  // A/B: the tape u stored with evict-first (streaming) hints
-#endif
-          if (EPI == EPI_FWD_OPT && tape) {
-            if (SPTC_TAPE_CS) __stcs(reinterpret_cast<float2*>(tape + off), uu);
-            else *reinterpret_cast<float2*>(tape + off) = uu;
-          }
+          if (EPI == EPI_FWD_OPT && tape) *reinterpret_cast<float2*>(tape + off) = uu;
           *reinterpret_cast<float2*>(out + off) = last ? yv : make_float2(f.x * yv.x, f.y * yv.y);
         }
       }
