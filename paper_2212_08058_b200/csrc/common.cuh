@@ -22,7 +22,7 @@ constexpr int kSpassWarps = kSpassThreads / 32;
 constexpr int kSpassPartSlots = 1;    // norm partial slots per CTA
 constexpr int kRingStride = kTW + 4;  // ring row stride in floats (== 4 mod 32: conflict-free)
 constexpr int kMaxC = 64;       // channels passed by value in kernel parameters
-constexpr int kScal = 11;       // doubles of per-volume scalars
+constexpr int kScal = 14;       // doubles of per-volume scalars
 
 // per-volume scalar slots (double sc[B][kScal])
 enum ScalSlot : int {
@@ -34,9 +34,9 @@ enum ScalSlot : int {
   SC_NU = 5,           // last nu
   SC_THETA = 6,        // soft-binarisation: mean of the positive entries of y_k (y units)
   SC_CORR = 7,         // backward through a binarised iteration: sum(g) / n_pos (the centre's adjoint)
-  SC_VMAX = 8,         // 8, 9, 10: max |v| of a temporal pass's output for the fp16 spatial pass that
+  SC_VMAX = 8,         // 8 .. 13: max |v| of a temporal pass's output for the fp16 spatial pass that
                        //   reads it (float bits in the slot's first word, atomicMax): slot (k & 1) on
-                       //   the hot path, one slot per input of the full operator's stacked pass
+                       //   the hot path, slots 3 (k & 1) + c for the full operator's three inputs
 };
 
 enum ErrBits : unsigned { ERR_DEGENERATE = 1u, ERR_NONFINITE = 2u };

@@ -96,7 +96,6 @@ struct FullEpiParams {
   unsigned* err;
   double* stats;
   int B, T, H, Wp, W, K, k, last, gx;
-  int zero_vmax;        // zero the stacked temporal pass's three max |v| slots (fp16 spatial passes)
   float inv_alpha;
 };
 
@@ -109,9 +108,6 @@ __global__ void __launch_bounds__(kEwThreads) full_epilogue_kernel(const __grid_
   const int b = bt / P.T, t = bt - b * P.T;
   const long HWp = (long)P.H * P.Wp;
   const long W4 = P.Wp / 4;
-  if (P.zero_vmax && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)  // the three spatial passes are done
-    for (int v = 0; v < P.B; ++v)
-      for (int c = 0; c < 3; ++c) *reinterpret_cast<unsigned*>(P.sc + v * kScal + SC_VMAX + c) = 0u;
   double acc = 0.0;
   for (int y = blockIdx.x; y < P.H; y += P.gx) {
     for (long x4 = threadIdx.x; x4 < W4; x4 += kEwThreads) {

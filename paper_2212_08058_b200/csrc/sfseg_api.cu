@@ -1747,14 +1747,16 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
     if (!make_spass_fwd_tmap(&vmap[c], P, vin[c])) return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.plain = 1;
+  sp.ua = uo[0];       // the fused combination's operands (third pass, EPI_FULL)
+  sp.ub = uo[1];
+  sp.Ufull = U;
+  sp.inv_alpha = (float)(1.0 / alpha);
+  sp.stats = stats;
   Tpass3Params tp;
   std::memset(&tp, 0, sizeof(tp));
   tp.a = a;
   tp.F = F;
-  for (int c = 0; c < 3; ++c) {
-    tp.out[c] = vin[c];
-    tp.vmax[c] = P.f16 ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + c) : nullptr;
-  }
+  for (int c = 0; c < 3; ++c) tp.out[c] = vin[c];
   tp.sc = at<double>(ws, P.off_sc);
   tp.frame2 = P.H * P.Wp / 2;
   tp.T = (int)P.T;
@@ -1779,31 +1781,45 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   ep.W = (int)P.W;
   ep.K = K;
   ep.gx = P.gx;
-  ep.zero_vmax = P.f16 ? 1 : 0;
   ep.inv_alpha = (float)(1.0 / alpha);
+  // the combination fused into the third spatial pass (tensor-core plans; the FP32 and tcgen05
+  // passes keep the separate epilogue kernel)
+  const bool fuse = P.tc && !P.tc5;
   for (int k = 1; k <= K; ++k) {
+    const bool bink = bin && k > bin->n_cont;  // Alg.1 STEP 3 after this iteration
+    const int last = (k == K || bink) ? 1 : 0; // store y_k itself when it is binarised next
+    // max |v| slots of this iteration's three inputs: 3 (k & 1) + c; each spatial pass zeroes
+    // its input's slot of the other parity (last read by the previous iteration)
+    const int base = 3 * (k & 1), other = 3 * ((k + 1) & 1);
+    for (int c = 0; c < 3; ++c)
+      tp.vmax[c] = P.f16 ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + base + c) : nullptr;
     {  // G_t*(S^p X), G_t*(F^2 S^p X), G_t*(F S^p X) in one pass over a and F
       ProfScope ps(P.prof, st, PC_TPASS);
       SF_CUDA(launch_tpass3(P.RT, tp, (int)P.B, st));
       SF_CUDA(after_launch("tpass3_full", st));
     }
     for (int c = 0; c < 3; ++c) {
+      const bool fc = fuse && c == 2;
       sp.tmap = vmap[c];
-      sp.vslot = c;
-      sp.vzero = 0;   // the epilogue zeroes the three slots
-      sp.out = uo[c];
+      sp.vslot = base + c;
+      sp.vzero = other + c + 1;
+      sp.out = fc ? a : uo[c];
       sp.k = k;
+      sp.plain = fc ? 0 : 1;
+      sp.full_epi = fc ? 1 : 0;
+      sp.last = last;
       {
         ProfScope ps(P.prof, st, PC_SPASS);
         SF_CUDA(launch_spass_forward(P, sp, st));
-        SF_CUDA(after_launch("spass_plain", st));
+        SF_CUDA(after_launch(fc ? "spass_full" : "spass_plain", st));
       }
     }
-    const bool bink = bin && k > bin->n_cont;  // Alg.1 STEP 3 after this iteration
-    ep.k = k;
-    ep.last = (k == K || bink) ? 1 : 0;       // store y_k itself when it is binarised next
-    full_epilogue_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ep);
-    SF_CUDA(after_launch("full_epilogue", st));
+    if (!fuse) {
+      ep.k = k;
+      ep.last = last;
+      full_epilogue_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ep);
+      SF_CUDA(after_launch("full_epilogue", st));
+    }
     if (bink) {
       BinParams bp;
       std::memset(&bp, 0, sizeof(bp));

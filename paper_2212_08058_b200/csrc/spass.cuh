@@ -100,8 +100,13 @@ struct SpassParams {
   int loc_acc;             // time-slab mode: add this launch's sums to loc (later launches of one iteration)
   int vslot;               // fp16 tensor-core pass: max |v| in sc[SC_VMAX + vslot] (written by the temporal
                            //   pass that produced v)
-  int vzero;               // > 0: the pass zeroes slot vzero - 1 for the next temporal pass (hot path:
-                           //   the other parity); 0: none (the full operator's epilogue zeroes its slots)
+  int vzero;               // > 0: the pass zeroes slot vzero - 1 for the next temporal pass (the slot of
+                           //   the other iteration parity); 0: none
+  const float* ua;         // full operator, fused combination (spass_tc EPI_FULL): G*(S^p X), G*(F^2 S^p X)
+  const float* ub;
+  const float* Ufull;      //   S^p
+  float inv_alpha;         //   1 / alpha
+  int full_epi;            //   the launch selects EPI_FULL
   float g[kMaxRS + 1];     // g[d] = weight of spatial offset +-d (same taps for y and x)
 };
 

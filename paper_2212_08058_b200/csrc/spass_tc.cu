@@ -14,6 +14,7 @@ cudaError_t launch_tc_epi(const SpassParams& P, int grid, cudaStream_t st) {
 }
 template <int R>
 cudaError_t launch_tc_one(const SpassParams& P, int grid, int fmt, cudaStream_t st) {
+  if (P.full_epi) return fmt ? launch_tc_epi<R, EPI_FULL, 1>(P, grid, st) : launch_tc_epi<R, EPI_FULL, 0>(P, grid, st);
   if (P.plain) return fmt ? launch_tc_epi<R, EPI_PLAIN, 1>(P, grid, st) : launch_tc_epi<R, EPI_PLAIN, 0>(P, grid, st);
   if (fmt) {
     if (P.tape_u || P.pprev) return launch_tc_epi<R, EPI_FWD_OPT, 1>(P, grid, st);

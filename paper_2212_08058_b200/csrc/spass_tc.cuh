@@ -137,7 +137,10 @@ __device__ __forceinline__ float sptc_w(const float* gsm, int d, int R) {
 
 // Epilogue variants (compile-time, so the hot forward carries no dead predicated loads:
 // measured 5 % of the instructions were the p_{k-1} loads of the Rayleigh option)
-enum SptcEpi : int { EPI_PLAIN = 0, EPI_FWD = 1, EPI_FWD_OPT = 2 };  // OPT: tape and/or Rayleigh
+// OPT: tape and/or Rayleigh.  FULL: the full operator's combination (row f1, Eq.7) fused into
+// the third spatial pass: y = U [(1/alpha - F^2) ua - ub + 2 F uc] with uc this pass's output,
+// a_k = U y (y when last), norm partials of y.
+enum SptcEpi : int { EPI_PLAIN = 0, EPI_FWD = 1, EPI_FWD_OPT = 2, EPI_FULL = 3 };
 
 template <int R, int EPI, int FMT>
 __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const __grid_constant__ SpassParams P) {
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
       const int yb = (sg.yb0 + m) * kM + 16 * mt + g;
       const long base = row_base(m);
       const float* fb = P.F + base;
-      const float* ab = pprev + base;
+      const float* ab = EPI == EPI_FULL ? P.Ufull + base : pprev + base;
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const bool rok = yb + 8 * i < yend;
@@ -323,7 +326,8 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
           pr.f[nl][i] = pr.a[nl][i] = make_float2(0.f, 0.f);
           if (!plain && rok && cst[nl]) {
             pr.f[nl][i] = *reinterpret_cast<const float2*>(fb + (long)8 * i * Wp + 8 * nl);
-            if (EPI == EPI_FWD_OPT && pprev) pr.a[nl][i] = __ldcg(reinterpret_cast<const float2*>(ab + (long)8 * i * Wp + 8 * nl));
+            if ((EPI == EPI_FWD_OPT && pprev) || EPI == EPI_FULL)
+              pr.a[nl][i] = __ldcg(reinterpret_cast<const float2*>(ab + (long)8 * i * Wp + 8 * nl));
           }
         }
       }
@@ -404,6 +408,17 @@ __global__ void __launch_bounds__(kSpassThreads, SPTC_LB) spass_tc_kernel(const 
             continue;
           }
           const float2 f = pr.f[nl][i];
+          if (EPI == EPI_FULL) {
+            const float2 U = pr.a[nl][i];
+            const float2 ua = __ldcs(reinterpret_cast<const float2*>(P.ua + off));
+            const float2 ub = __ldcs(reinterpret_cast<const float2*>(P.ub + off));
+            const float vx = (P.inv_alpha - f.x * f.x) * ua.x - ub.x + 2.f * f.x * uu.x;
+            const float vy = (P.inv_alpha - f.y * f.y) * ua.y - ub.y + 2.f * f.y * uu.y;
+            const float2 yv = make_float2(U.x * vx * cmask[nl].x, U.y * vy * cmask[nl].y);
+            s0 = fmaf(yv.x, yv.x, fmaf(yv.y, yv.y, s0));
+            *reinterpret_cast<float2*>(out + off) = last ? yv : make_float2(U.x * yv.x, U.y * yv.y);
+            continue;
+          }
           const float2 yv = make_float2(f.x * uu.x, f.y * uu.y);
           s0 = fmaf(yv.x, yv.x, fmaf(yv.y, yv.y, s0));
           if (EPI == EPI_FWD_OPT && pprev) s1 = fmaf(pr.a[nl][i].x, uu.x, fmaf(pr.a[nl][i].y, uu.y, s1));
