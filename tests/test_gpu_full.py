@@ -57,6 +57,7 @@ def _check(sf, s_ch, ws, f_ch, wf, p, alpha, sig_t, sig_s, r_t, r_s, K, bs=0.0, 
     ((1, 6, 40, 70), (2, 6), 0.2, 1.0),
     ((2, 5, 33, 150), (1, 3), 0.1, 0.8),     # B > 1, ragged strips / blocks, small radii
     ((1, 9, 70, 130), (6, 24), 1.0, 1.0),    # config-2 radii across several strips
+    ((2, 5, 40, 150), (3, 9), 0.5, 1.2),     # B > 1 on the tensor-core plan (fused combination)
 ])
 def test_full_random(sf, shape, radii, p, alpha):
     B, T, H, W = shape
