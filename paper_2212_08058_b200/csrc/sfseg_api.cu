@@ -1747,6 +1747,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
     if (!make_spass_fwd_tmap(&vmap[c], P, vin[c])) return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.plain = 1;
+  sp.F = F;            // the full layout's pairwise map (fill_spass_common points at the hot path's F slot)
   sp.ua = uo[0];       // the fused combination's operands (third pass, EPI_FULL)
   sp.ub = uo[1];
   sp.Ufull = U;
