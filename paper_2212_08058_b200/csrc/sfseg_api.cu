@@ -1783,9 +1783,12 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   ep.K = K;
   ep.gx = P.gx;
   ep.inv_alpha = (float)(1.0 / alpha);
-  // the combination fused into the third spatial pass (tensor-core plans; the FP32 and tcgen05
-  // passes keep the separate epilogue kernel)
-  const bool fuse = P.tc && !P.tc5;
+  // SFSEG_FULL_FUSE (A/B, measured slower): the combination fused into the third
+  // spatial pass (spass_tc EPI_FULL) instead of full_epilogue_kernel
+#ifndef SFSEG_FULL_FUSE
+#define SFSEG_FULL_FUSE 0
+#endif
+  const bool fuse = SFSEG_FULL_FUSE && P.tc && !P.tc5;
   for (int k = 1; k <= K; ++k) {
     const bool bink = bin && k > bin->n_cont;  // Alg.1 STEP 3 after this iteration
     const int last = (k == K || bink) ? 1 : 0; // store y_k itself when it is binarised next
