@@ -21,7 +21,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libsfseg.so")
 
-SOURCES = ["sfseg_api.cu", "spass_fwd.cu", "spass_bwd.cu", "tpass.cu", "f3d.cu", "spass_tc.cu", "spass_tc5.cu"]
+SOURCES = ["sfseg_api.cu", "spass_fwd.cu", "spass_bwd.cu", "tpass.cu", "f3d.cu", "spass_tc.cu", "spass_tc6.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]

@@ -36,7 +36,10 @@ enum ScalSlot : int {
   SC_CORR = 7,         // backward through a binarised iteration: sum(g) / n_pos (the centre's adjoint)
   SC_VMAX = 8,         // 8 .. 13: max |v| of a temporal pass's output for the fp16 spatial pass that
                        //   reads it (float bits in the slot's first word, atomicMax): slot (k & 1) on
-                       //   the hot path, slots 3 (k & 1) + c for the full operator's three inputs
+                       //   the hot path, slots 3 (k & 1) + c for the full operator's three inputs.
+                       //   With the tcgen05 spatial pass (spass_tc6) slot (k & 1) holds max |p_k| instead
+                       //   (written by combine for k = 0 and by the spatial pass of iteration k)
+  SC_VEXP = 10,        // tcgen05 pass: exponent e of the fp16 planes of v (v 2^e), written by TP_FWD16
 };
 
 enum ErrBits : unsigned { ERR_DEGENERATE = 1u, ERR_NONFINITE = 2u };

@@ -11,6 +11,8 @@ namespace sfseg {
 cudaError_t launch_spass_fwd(int R, const SpassParams& P, int grid, cudaStream_t st);
 cudaError_t launch_spass_bwd(int R, const SpassParams& P, int grid, cudaStream_t st);
 cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t st);
+// TP_FWD16: v written as two fp16 planes for the tcgen05 spatial pass (spass_tc6.cuh)
+cudaError_t launch_tpass_fwd16(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_fwdf(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass3(int RT, const Tpass3Params& P, int B, cudaStream_t st);
@@ -20,9 +22,11 @@ int spass_tc_boxw(int R);
 // fmt 0: three bf16 planes / six products; 1: two fp16 planes / three products (needs the
 // preceding temporal pass's per-volume max |v|: TpassParams::vmax -> SpassParams::vslot)
 cudaError_t launch_spass_tc(int R, const SpassParams& P, int grid, int fmt, cudaStream_t st);
-// tcgen05 / TMEM spatial pass (spass_tc5.cuh): strips of 80 output columns, 128-column TMA boxes
-bool spass_tc5_supported(int R);
-cudaError_t launch_spass_tc5(int R, const SpassParams& P, int grid, cudaStream_t st);
+// tcgen05 / TMEM spatial pass (spass_tc6.cuh): strips of 128 output columns, x-blocks of 128 rows,
+// y-blocks of 64 rows; input v as two fp16 planes (TP_FWD16), forward epilogues only
+bool spass_tc6_supported(int R);
+size_t spass_tc6_smem(int R);
+cudaError_t launch_spass_tc6(int R, const SpassParams& P, int grid, cudaStream_t st);
 bool f3d_supported(int RT, int R);
 int f3d_occupancy(int RT, int R);
 cudaError_t launch_f3d(int RT, int R, const F3dParams& P, int grid, cudaStream_t st);

@@ -24,6 +24,7 @@ struct CombineParams {
   unsigned* counter;
   unsigned* err;
   double* loc;          // time-slab mode: per-volume local sum of x_0^2 -> loc[2b]
+  unsigned* pmax;       // max |p_0| per volume (float bits, stride 2 kScal words; tcgen05 pass) or null
   int B, C, T, H, W, Wp, act, gx;
   int in_T, in_t0;      // ch / x0 buffers hold in_T frames; this call's frame t is buffer frame in_t0 + t
   float bias;
@@ -49,6 +50,7 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
   const float* chf = P.ch + (long)b * P.C * vol_dense + (long)(P.in_t0 + t) * HW;  // frame base, channel 0
   const long dbase = (long)b * vol_dense + (long)(P.in_t0 + t) * HW;              // dense x0 / F_out frame base
   double acc = 0.0;
+  float pm = 0.f;
   for (int y0 = blockIdx.x * kRows; y0 < P.H; y0 += P.gx * kRows) {
     for (int c0 = 0; c0 < P.Wp; c0 += kEwThreads * kCols) {
       float z[kRows][kCols];
@@ -91,6 +93,7 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
             f = (P.act == 1) ? 1.f / (1.f + expf(-z[r][i])) : z[r][i];
             xx = P.x0 ? xv[r][i] : f;
             pv = f * xx;
+            pm = fmaxf(pm, fabsf(pv));
             if (P.F_out) P.F_out[dbase + (long)y * P.W + x] = f;
             acc += (double)xx * (double)xx;
           }
@@ -99,6 +102,10 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
           if (P.x0p) P.x0p[po] = xx;
         }
     }
+  }
+  if (P.pmax) {   // order-free max: one atomic per warp
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(pm));
+    if ((threadIdx.x & 31) == 0) atomicMax(P.pmax + (long)b * 2 * kScal, m);
   }
   if (P.partials == nullptr) return;  // plain combine (sfseg_combine_channels): no reduction
   const double s = block_sum<kEwThreads>(acc, red);

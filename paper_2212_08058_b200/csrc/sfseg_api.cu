@@ -28,7 +28,7 @@
 #include "bwd.cuh"
 #include "learn.cuh"
 #include "launch.h"
-#include "spass_tc5.cuh"
+#include "spass_tc6.cuh"
 
 using namespace sfseg;
 
@@ -144,6 +144,22 @@ PFN_encodeTiled get_encode() {
   return fn;
 }
 
+// The two fp16 planes of v for the tcgen05 spatial pass: dims {W, H, 2 BT} (plane-frames
+// [bt][plane]), box {64, 128, 2} = both planes of a 128-row x 64-column tile, SWIZZLE_128B (the
+// MMA's K-major B operand layout); columns >= W and rows outside [0, H) read as zero.
+bool make_planes_tmap(CUtensorMap* map, const void* base, int64_t W, int64_t H, int64_t BT, int64_t Wp) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)(2 * BT)};
+  cuuint64_t strides[2] = {(cuuint64_t)(Wp * 2), (cuuint64_t)(H * Wp * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)k6BoxW, (cuuint32_t)k6XN, 2u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool make_volume_tmap(CUtensorMap* map, const float* base, int64_t W, int64_t H, int64_t BT, int64_t Wp, int boxw,
                       int boxh = kM) {
   PFN_encodeTiled enc = get_encode();
@@ -242,11 +258,12 @@ struct Plan {
   bool f16;           // ... in the two-plane fp16 format (fmt 1; temporal pass records max |v|)
   int Gtc;            // its grid
   int Gcap, Gcap_tc;  // resident-CTA caps of the FP32 / tensor-core passes (grids of frame-range launches)
-  bool tc5;           // ... on tcgen05 / TMEM (spass_tc5_kernel): 80-column strips
-  int S5;             // its strips
-  int NB5;            // its 64-row blocks per column
-  int64_t U5;         // its units = BT * S5 * NB5
-  int G5;             // its grid (one CTA per SM: all 512 TMEM columns)
+  bool tc6;           // ... on tcgen05 / TMEM (spass_tc6_kernel, hot forward only): 128-column strips,
+                      //   v written by the temporal pass as two fp16 planes (TP_FWD16)
+  int S6;             // its strips
+  int NB6;            // its 64-row y-blocks per column
+  int64_t U6;         // its units = BT * S6 * NB6
+  int G6;             // its grid (one CTA per SM: all 512 TMEM columns)
   int gx;             // elementwise grid.x per frame
   bool f3d;           // single-pass fused 3D kernel (small radii) for the single-GPU forward
   int TX, TY;         // f3d tiles per frame (64 columns x f3d_th(RS) rows)
@@ -316,14 +333,14 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->Gcap = (int)cap;
   P->gx = ew_gx(P->H, P->BT);
   P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
-  P->tc5 = P->tc && algo == SFSEG_ALGO_TWO_PASS_TCGEN05 && spass_tc5_supported(P->RS);
+  P->tc6 = P->tc && algo == SFSEG_ALGO_TWO_PASS_TCGEN05 && spass_tc6_supported(P->RS) && !P->bin;
   // the forward's default tensor-core format is two fp16 planes (A25); SFSEG_ALGO_TWO_PASS_MMA_SYNC
   // selects the three-plane bf16 one (A23)
   P->f16 = P->tc && (algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_MMA_F16);
-  P->S5 = (int)((sh.W + k5OW - 1) / k5OW);
-  P->NB5 = (int)((sh.H + k5NR - 1) / k5NR);
-  P->U5 = P->BT * P->S5 * P->NB5;
-  P->G5 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(), P->U5));
+  P->S6 = (int)((sh.W + k6M - 1) / k6M);
+  P->NB6 = (int)((sh.H + k6YN - 1) / k6YN);
+  P->U6 = P->BT * P->S6 * P->NB6;
+  P->G6 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(), P->U6));
   P->Gcap_tc = num_sms() * spass_tc_occupancy(P->RS, P->f16 ? 1 : 0);
   P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)P->Gcap_tc, P->U / 4));
   P->f3d = algo == SFSEG_ALGO_AUTO && !P->bin && f3d_supported(P->RT, P->RS);
@@ -332,7 +349,7 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->U3 = P->B * P->TY * P->TX * P->T;
   P->G3 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * f3d_occupancy(P->RT, P->RS), P->U3 / 4));
   // partials: spass [2][B][G], combine/init [B][T*gx], contraction [G2][C+1]
-  size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max({(size_t)P->G * kSpassPartSlots, (size_t)P->Gtc, (size_t)P->G3 * kF3dCW}),
+  size_t n_part = std::max<size_t>(2 * (size_t)P->B * std::max({(size_t)P->G * kSpassPartSlots, (size_t)P->Gtc, (size_t)P->G3 * kF3dCW, (size_t)P->G6}),
                                    2 * (size_t)P->BT * P->gx);
   {  // backward contraction: one (C_pad + 1)-vector per (frame, block)
     const int cpad = C <= 1 ? 1 : C <= 2 ? 2 : C <= 4 ? 4 : C <= 8 ? 8 : C <= 16 ? 16 : kMaxC;
@@ -438,17 +455,9 @@ void fill_spass_common(SpassParams& sp, const Plan& P, void* ws) {
 // Forward spatial pass: the tensor-core kernel when the plan selected it, else the FP32 one.
 // Input descriptor of the forward spatial pass over v (box width of the selected kernel).
 bool make_spass_fwd_tmap(CUtensorMap* map, const Plan& P, const float* v) {
-  if (P.tc5) return make_volume_tmap(map, v, P.W, P.H, P.BT, P.Wp, k5Lanes, k5IR);
   return make_volume_tmap(map, v, P.W, P.H, P.BT, P.Wp, P.tc ? spass_tc_boxw(P.RS) : spass_boxw(P.RS));
 }
 cudaError_t launch_spass_forward(const Plan& P, SpassParams& sp, cudaStream_t st) {
-  if (P.tc5) {
-    sp.S = P.S5;
-    sp.NB = P.NB5;
-    sp.U = P.U5;
-    sp.G = P.G5;
-    return launch_spass_tc5(P.RS, sp, P.G5, st);
-  }
   if (sp.t_cnt > 0) {  // frame-range launch (time-slab schedule): its own unit count and grid
     sp.U = (int64_t)P.B * sp.t_cnt * P.S * P.NB;
     sp.G = (int)std::max<int64_t>(1, std::min<int64_t>(P.tc ? P.Gcap_tc : P.Gcap, sp.U / 4));
@@ -1104,7 +1113,7 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
   if (agreed != SFSEG_OK) return agreed;  // a peer failed its validation: nobody starts the solve
   Rank r;
   r.P = P;
-  r.P.tc5 = false;  // time slabs: frame-range launches and the lagged scale are in the mma.sync / FP32 passes
+  r.P.tc6 = false;  // time slabs: frame-range launches and the lagged scale are in the mma.sync / FP32 passes
   r.ch = ch;
   r.x0 = x0;
   r.in_T = (int)P.T;
@@ -1227,7 +1236,7 @@ sfseg_status sfseg_forward_path(sfseg_shape sh, sfseg_gauss g, int32_t algo, int
   sfseg_status s = make_plan(sh, 1, g, 1, &P, &opt);
   if (s != SFSEG_OK) return s;
   info[0] = P.f3d ? SFSEG_PATH_FUSED_3D
-            : P.tc5 ? SFSEG_PATH_TWO_PASS_TCGEN05
+            : P.tc6 ? SFSEG_PATH_TWO_PASS_TCGEN05
             : P.f16 ? SFSEG_PATH_TWO_PASS_TC_F16
             : P.tc  ? SFSEG_PATH_TWO_PASS_TC
                     : SFSEG_PATH_TWO_PASS_FP32;
@@ -1325,6 +1334,7 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
   cp.F = F;
   cp.p0 = p;
   cp.F_out = F_out;
+  if (P.tc6) cp.pmax = reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX);   // max |p_0|
   {
     ProfScope ps(P.prof, st, PC_ONCE);
     combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
@@ -1381,7 +1391,9 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
 
   SpassParams sp;
   std::memset(&sp, 0, sizeof(sp));
-  if (!make_spass_fwd_tmap(&sp.tmap, P, v)) return SFSEG_ERR_CUDA;
+  if (!(P.tc6 ? make_planes_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp) : make_spass_fwd_tmap(&sp.tmap, P, v)))
+    return SFSEG_ERR_CUDA;
+  if (P.tc6 && !make_volume_tmap(&sp.fmap, F, P.W, P.H, P.BT, P.Wp, k6M, k6YN)) return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.stats = stats;
   sp.tape_nu = tape_nu;
@@ -1390,10 +1402,28 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
   fill_tpass_common(tp, P, ws);
   tp.src = p;
   tp.out = v;
+  double* const scv = at<double>(ws, P.off_sc);
+  auto pmax_slot = [&](int j) { return reinterpret_cast<unsigned*>(scv + SC_VMAX + (j & 1)); };
+  if (P.tc6) {
+    float gsum = 0.f;
+    for (int i = 0; i < 2 * P.RT + 1; ++i) gsum += std::fabs(P.gt[i]);
+    tp.gsum = gsum * (1.f + 1e-5f);   // |v| <= s gsum max |p| with margin for rounding
+    tp.vexp_out = scv + SC_VEXP;
+    sp.S = P.S6;
+    sp.NB = P.NB6;
+    sp.U = P.U6;
+    sp.G = P.G6;
+  }
 
   for (int k = 1; k <= K; ++k) {
     // (a2)+(a3) v = s_{k-1} * G_t * p_{k-1}
-    {
+    if (P.tc6) {   // as two fp16 planes of v 2^e (e from max |p_{k-1}|, slot (k-1) & 1)
+      tp.pmax_in = pmax_slot(k - 1);
+      tp.pmax_zero = pmax_slot(k);
+      ProfScope ps(P.prof, st, PC_TPASS);
+      SF_CUDA(launch_tpass_fwd16(P.RT, tp, (int)P.B, st));
+      SF_CUDA(after_launch("tpass_fwd16", st));
+    } else {
       set_vslot(tp, &sp, P, ws, k);
       ProfScope ps(P.prof, st, PC_TPASS);
       SF_CUDA(launch_tpass_fwd(P.RT, tp, (int)P.B, st));
@@ -1406,7 +1436,12 @@ sfseg_status sfseg_power_iterate_ex(const float* ch, int32_t C, const float* w_h
     sp.tape_u = tape ? tape_u(k - 1) : nullptr;
     sp.k = k;
     sp.last = (k == K || kap > 0.f) ? 1 : 0;   // a binarised iteration stores y_k itself
-    {
+    if (P.tc6) {
+      sp.pslot = sp.last ? 0 : (k & 1) + 1;   // max |p_k| for the next temporal pass
+      ProfScope ps(P.prof, st, PC_SPASS);
+      SF_CUDA(launch_spass_tc6(P.RS, sp, P.G6, st));
+      SF_CUDA(after_launch("spass_tc6", st));
+    } else {
       ProfScope ps(P.prof, st, PC_SPASS);
       SF_CUDA(launch_spass_forward(P, sp, st));
       SF_CUDA(after_launch("spass_fwd", st));
@@ -1788,7 +1823,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
 #ifndef SFSEG_FULL_FUSE
 #define SFSEG_FULL_FUSE 0
 #endif
-  const bool fuse = SFSEG_FULL_FUSE && P.tc && !P.tc5;
+  const bool fuse = SFSEG_FULL_FUSE && P.tc;
   for (int k = 1; k <= K; ++k) {
     const bool bink = bin && k > bin->n_cont;  // Alg.1 STEP 3 after this iteration
     const int last = (k == K || bink) ? 1 : 0; // store y_k itself when it is binarised next
@@ -2267,7 +2302,7 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
     sfseg_shape ls = sh;
     ls.T = t1 - t0;
     if ((s = make_plan(ls, C, gauss, K, &R[i].P, opt)) != SFSEG_OK) return s;
-    R[i].P.tc5 = false;  // as in dist_power_iterate
+    R[i].P.tc6 = false;  // as in dist_power_iterate
     if (tape) {
       R[i].tape = static_cast<char*>(tape) + toff;
       toff += align_up(R[i].P.tape_bytes);

@@ -74,6 +74,8 @@ enum SpassMode : int { SP_FWD = 0, SP_BWD = 1 };
 
 struct SpassParams {
   CUtensorMap tmap;        // input volume (v): dims {W, H, B*T}, box {BOXW, kM, 1}, fp32
+                           //   (tcgen05 pass: the fp16 planes of v, make_planes_tmap)
+  CUtensorMap fmap;        // tcgen05 pass: F, dims {W, H, B*T}, box {128, 64, 1}, fp32
   const float* F;          // pitched [B*T][H][Wp]
   float* out;              // FWD: p (or y when last) ; BWD: x_bar (in place)
   float* tape_u;           // FWD: record u (nullable)
@@ -102,6 +104,8 @@ struct SpassParams {
                            //   pass that produced v)
   int vzero;               // > 0: the pass zeroes slot vzero - 1 for the next temporal pass (the slot of
                            //   the other iteration parity); 0: none
+  int pslot;               // tcgen05 pass (spass_tc6): > 0 records max |p_k| per volume into
+                           //   sc[SC_VMAX + pslot - 1] (the next TP_FWD16 temporal pass's range); 0: none
   const float* ua;         // full operator, fused combination (spass_tc EPI_FULL): G*(S^p X), G*(F^2 S^p X)
   const float* ub;
   const float* Ufull;      //   S^p

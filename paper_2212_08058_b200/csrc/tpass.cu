@@ -23,6 +23,9 @@ static cudaError_t launch_tpass_t(int RT, const TpassParams& P, int B, cudaStrea
 cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t st) {
   return launch_tpass_t<TP_FWD>(RT, P, B, st);
 }
+cudaError_t launch_tpass_fwd16(int RT, const TpassParams& P, int B, cudaStream_t st) {
+  return launch_tpass_t<TP_FWD16>(RT, P, B, st);
+}
 cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st) {
   return launch_tpass_t<TP_BWD>(RT, P, B, st);
 }

@@ -19,6 +19,8 @@ enum TpassMode : int {
   TP_BWD = 1,   // src = F * y_bar_k, y_bar_k = (x_bar_k - [x_k > 0] corr - F u_{k-1} cn) * inv_nu (Appendix A;
                 //   corr != 0 only after a soft-binarised iteration, reading A21)
   TP_FWDF = 2,  // full SFSeg operator (f1): src = F^fexp * a, out = s_{k-1} * G_t * src  (Eq.7's three inputs)
+  TP_FWD16 = 3, // as TP_FWD, out = the two fp16 planes of v 2^e ([bt][plane][H][Wp] halves, 4 B/voxel) for the
+                //   tcgen05 spatial pass (spass_tc6.cuh); e from max |p_{k-1}| so that |v 2^e| < 2^14
 };
 
 struct TpassParams {
@@ -30,6 +32,10 @@ struct TpassParams {
   float* out;            // pitched [B*T][H][Wp]
   const double* sc;      // per-volume scalars [B][kScal]
   unsigned* vmax;        // atomicMax of max |out| per volume (float bits, stride 2 kScal words) or null
+  const unsigned* pmax_in;  // FWD16: max |src| per volume (float bits, stride 2 kScal words)
+  unsigned* pmax_zero;     // FWD16: slot zeroed for the next spatial pass's max |p_k| (or null)
+  double* vexp_out;        // FWD16: sc + SC_VEXP (stride kScal): the exponent e written per volume
+  float gsum;              // FWD16: sum of |g| (|v| <= s gsum max |src|)
   int lag;               // FWD: no scale (the spatial pass applies s_{k-1}: lagged normalisation, time slabs)
   long frame4;           // H*Wp/4 float4 per frame
   int T;
@@ -46,7 +52,14 @@ constexpr int kTpThreads = 128;
 // float4 columns) 6 x 128 threads per SM hold every column in ONE wave.
 __host__ __device__ constexpr int tpass_min_blocks(int RT) { return RT <= 6 ? 6 : (RT <= 9 ? 4 : 2); }
 // cp.async stages per input stream (frames prefetched ahead of the ring).
-__host__ __device__ constexpr int tpass_stages(int MODE) { return MODE == TP_FWD ? 12 : (MODE == TP_FWDF ? 6 : 4); }
+__host__ __device__ constexpr int tpass_stages(int MODE) {
+  return (MODE == TP_FWD || MODE == TP_FWD16) ? 12 : (MODE == TP_FWDF ? 6 : 4);
+}
+constexpr int kF16DataExp = 14;  // TP_FWD16: |v 2^e| < 2^14 (fp16 max 65504)
+__device__ __forceinline__ void st_u2_hint(uint2* ptr, uint2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol)
+               : "memory");
+}
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
@@ -67,7 +80,8 @@ template <int RT, int MODE, bool HALO>
 __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel(const __grid_constant__ TpassParams P) {
   constexpr int NR = 2 * RT + 1;
   constexpr int NS = tpass_stages(MODE);
-  constexpr int NIN = (MODE == TP_FWD) ? 1 : (MODE == TP_FWDF ? 2 : 3);
+  constexpr bool F16 = MODE == TP_FWD16;
+  constexpr int NIN = (MODE == TP_FWD || F16) ? 1 : (MODE == TP_FWDF ? 2 : 3);
   __shared__ float4 sq[NS][NIN][kTpThreads];
   const int b = blockIdx.y;
   const int tid = threadIdx.x;
@@ -80,8 +94,20 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   const float4* Fp = nullptr;
   const float4* U1 = nullptr;
   float cn = 0.f, inv_nu = 0.f, corr = 0.f, scale = 1.f;
-  if (MODE == TP_FWD) {
+  float m16 = 1.f;  // FWD16: s_{k-1} 2^e
+  if (MODE == TP_FWD || F16) {
     scale = P.lag ? 1.f : (float)P.sc[b * kScal + SC_S];
+    if (F16) {
+      const float bound = scale * __uint_as_float(P.pmax_in[(long)b * 2 * kScal]) * P.gsum;
+      int ex = 0;
+      if (bound > 0.f && bound <= 3.4e38f) frexpf(bound, &ex);  // bound < 2^ex
+      const int e = min(max(kF16DataExp - ex, -100), 100);
+      m16 = scale * __int_as_float((127 + e) << 23);
+      if (blockIdx.x == 0 && tid == 0) {
+        P.vexp_out[(long)b * kScal] = (double)e;
+        if (P.pmax_zero) P.pmax_zero[(long)b * 2 * kScal] = 0u;
+      }
+    }
   } else if (MODE == TP_FWDF) {
     scale = (float)P.sc[b * kScal + SC_S];
     Fp = reinterpret_cast<const float4*>(P.F) + b * vol4 + ec;
@@ -132,7 +158,7 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
     const int j = jp - RT;
     const int sl = jp % NS;
     float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (MODE == TP_FWD) {
+    if (MODE == TP_FWD || F16) {
       if (frame_src(jp, 0)) val = sq[sl][0][tid];
     } else if (MODE == TP_FWDF) {
       if (j >= 0 && j < T) {
@@ -155,7 +181,8 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   };
 
   // forward: keep v in L2 for the spatial pass that reads it next (and its halo re-reads)
-  const uint64_t pol = MODE == TP_FWD ? l2_policy_evict_last() : 0ull;
+  const uint64_t pol = (MODE == TP_FWD || F16) ? l2_policy_evict_last() : 0ull;
+  uint2* const o16 = F16 ? reinterpret_cast<uint2*>(P.out) + (long)b * T * 2 * P.frame4 + ec : nullptr;
   float4 acc[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -182,7 +209,15 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
       }
       const int slot0 = (((d - 2 * RT) % NR) + NR) % NR;
       const int t = jp - 2 * RT;
-      if (active && t >= 0 && t < T) {
+      if (F16 && active && t >= 0 && t < T) {
+        const float4 o = f4_scale(acc[slot0], m16);
+        uint32_t h0[2], h1[2];
+        split_planes_f16<2>(o.x, o.y, h0);
+        split_planes_f16<2>(o.z, o.w, h1);
+        uint2* dst = o16 + (long)(TPASS_REV ? T - 1 - t : t) * 2 * P.frame4;
+        st_u2_hint(dst, make_uint2(h0[0], h1[0]), pol);
+        st_u2_hint(dst + P.frame4, make_uint2(h0[1], h1[1]), pol);
+      } else if (active && t >= 0 && t < T) {
         const float4 o = f4_scale(acc[slot0], scale);
         float4* dst = out + (long)(TPASS_REV ? T - 1 - t : t) * P.frame4;
         if (MODE == TP_FWD) st_f4_hint(dst, o, pol);

@@ -1,7 +1,9 @@
-"""The tcgen05 / TMEM spatial pass (spass_tc5.cuh: UTCHMMA with operands in tensor memory,
-three bf16 planes and six products per tap) against the f64 oracle: every compiled radius,
-ragged strips (80-column strips: W not a multiple of 80) and blocks, B > 1, the Rayleigh /
-tape epilogue and the plain pass of the backward."""
+"""The tcgen05 / TMEM spatial pass (spass_tc6.cuh: UTCHMMA with dense-rate shapes, x-pass
+operands from the TMA box of the fp16 planes the temporal pass writes, y-pass A operand in
+tensor memory) against the f64 oracle: every compiled radius, ragged strips (128-column
+strips: W not a multiple of 128) and 64-row blocks, B > 1, H = 1, segments spanning many
+x-blocks (more units than CTAs), the Rayleigh / tape epilogue, and the backward of a
+tcgen05 forward (plain mma.sync pass)."""
 import numpy as np
 import pytest
 
@@ -42,14 +44,15 @@ def _solve(sf, ch, w, g, K, rayleigh=False):
 
 
 @pytest.mark.parametrize("r_s,shape", [
-    (24, (1, 6, 70, 200)),     # 3 strips (80 + 80 + 40), ragged 32-row blocks
-    (8, (2, 5, 33, 130)),
-    (9, (1, 4, 40, 81)),       # one live column in the last strip
+    (24, (1, 6, 70, 300)),     # 3 strips (128 + 128 + 44), ragged 64-row blocks
+    (8, (2, 5, 33, 130)),      # B = 2, two columns in the last strip
+    (9, (1, 4, 40, 129)),      # one live column in the last strip
     (12, (1, 3, 97, 71)),      # W < one strip
-    (16, (1, 3, 64, 160)),     # exact strips and blocks
-    (18, (2, 4, 50, 170)),
+    (16, (1, 3, 128, 256)),    # exact strips and blocks
+    (18, (2, 4, 200, 170)),
     (24, (1, 2, 1, 300)),      # H = 1
     (24, (1, 1, 5, 5)),        # tiny: pure padding around one partial block
+    (24, (1, 20, 480, 260)),   # 960 units > 148 CTAs: segments of several y-blocks, Q ring wraps
 ])
 def test_tcgen05_spatial_radii(sf, r_s, shape):
     B, T, H, W = shape
