@@ -303,7 +303,7 @@ def run_ours(args):
     path_info = sf.forward_path((B, T, H, W), gauss, algo)
     path_tc = path_info[0] in (sf.PATH_TWO_PASS_TC, sf.PATH_TWO_PASS_TCGEN05, sf.PATH_TWO_PASS_TC_F16)
     path_f16 = path_info[0] == sf.PATH_TWO_PASS_TC_F16
-    path_t5 = path_info[0] == sf.PATH_TWO_PASS_TCGEN05
+    path_t6 = path_info[0] == sf.PATH_TWO_PASS_TCGEN05
     thr_solver = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev) if slab else solver
 
     train = args.config == "c3" and not slab
@@ -461,13 +461,18 @@ def run_ours(args):
         # take 13.5 us at the measured dense bf16 peak); both reported
         RSc = path_info[2]
         NB_ = -(-H // 32)
-        if path_t5:
-            # per (frame, 80-column strip, 64-row block): 6 products x (NKY + 8) MMAs, M=128 N=64 K=16
-            nky5 = (64 + RSc + 15) // 16 + (RSc + 15) // 16
-            tc_flops = float(B * T * (-(-W // 80)) * (-(-H // 64))) * TC_PRODUCTS * (nky5 + 8) * 262144
-            kname = (f"spass_tc5_kernel<R={RSc}> (tcgen05.mma kind::f16, operands in TMEM / smem, accumulators in "
-                     f"TMEM; x/y Gaussian as banded Toeplitz products, three bf16 planes x six products per tap "
-                     f"(fp32-class) + F multiplies + norm)")
+        if path_t6:
+            # per (frame, 128-column strip): NB6 64-row y-blocks (3 x NKY MMAs) and NB6 + 1 64-row
+            # x-blocks (3 x NKX MMAs), M=128 N=64 K=16 (262144 flop); partial segments at CTA-range
+            # boundaries add a few x-blocks (not counted)
+            ra6 = 8 * ((RSc + 7) // 8)
+            nkx6 = (128 + 2 * ra6) // 16
+            nky6 = 4 + 2 * ((RSc + 15) // 16)
+            nb6, s6 = -(-H // 64), -(-W // 128)
+            tc_flops = float(B * T * s6) * 3 * (nb6 * nky6 + (nb6 + 1) * nkx6) * 262144
+            kname = (f"spass_tc6_kernel<R={RSc}> (tcgen05.mma kind::f16 M=128 N=64, accumulators in TMEM: x-pass "
+                     f"from SWIZZLE_128B TMA boxes of the fp16 planes of v, y-pass A operand in TMEM; two fp16 "
+                     f"planes x three products per tap (fp32-class) + F multiplies + norm + max |p|)")
             tc_ceiling = float(peaks.get("bf16_tflops", 2250.0))
         else:
             ra = (RSc + 3) // 4 * 4
@@ -571,7 +576,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(args.config)
 
-    if path_f16:
+    if path_t6 or path_f16:
         arith = ("fp32 FFMA everywhere except the forward spatial pass of r_s >= 8, which runs on the tensor "
                  "pipe with each operand and tap split into two fp16 planes (22 significant bits, per-volume "
                  "power-of-two range scaling) and three products per tap, fp32 accumulation (fp32-class: x_K "

@@ -333,14 +333,20 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->Gcap = (int)cap;
   P->gx = ew_gx(P->H, P->BT);
   P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
-  P->tc6 = P->tc && algo == SFSEG_ALGO_TWO_PASS_TCGEN05 && spass_tc6_supported(P->RS) && !P->bin;
+  // the hot forward's default spatial pass (r_s in 8..24, no soft-binarisation): tcgen05 / TMEM
+  P->tc6 = P->tc && spass_tc6_supported(P->RS) && !P->bin &&
+           (algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_TCGEN05);
   // the forward's default tensor-core format is two fp16 planes (A25); SFSEG_ALGO_TWO_PASS_MMA_SYNC
   // selects the three-plane bf16 one (A23)
   P->f16 = P->tc && (algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_MMA_F16);
   P->S6 = (int)((sh.W + k6M - 1) / k6M);
   P->NB6 = (int)((sh.H + k6YN - 1) / k6YN);
   P->U6 = P->BT * P->S6 * P->NB6;
-  P->G6 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(), P->U6));
+  {  // one CTA per SM; a multiple of B x S when that fits, so CTA ranges align with strips (spass_tc6.cuh)
+    const int64_t bs = P->B * P->S6, sms = num_sms();
+    const int64_t g = bs <= sms ? bs * (sms / bs) : sms;
+    P->G6 = (int)std::max<int64_t>(1, std::min<int64_t>(g, P->U6));
+  }
   P->Gcap_tc = num_sms() * spass_tc_occupancy(P->RS, P->f16 ? 1 : 0);
   P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)P->Gcap_tc, P->U / 4));
   P->f3d = algo == SFSEG_ALGO_AUTO && !P->bin && f3d_supported(P->RT, P->RS);

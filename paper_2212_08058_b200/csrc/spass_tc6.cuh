@@ -186,14 +186,23 @@ __device__ __forceinline__ float t6_w(const float* gsm, int d, int R) {
 // the data exponent e of volume b (written by the temporal pass, TP_FWD16)
 __device__ __forceinline__ int t6_vexp(const double* sc, int b) { return (int)sc[b * kScal + SC_VEXP]; }
 
-// Segment walker shared by the roles: the CTA's unit range [u_begin, u_end) of units
-// (bt, strip, 64-row y-block) as column segments of ny y-blocks and ny + 1 x-blocks.
+// Segment walker shared by the roles.  Units are (volume b, strip s, frame t, 64-row y-block),
+// in that order (volume-major: the finalize's per-volume CTA ranges; strip-major inside a
+// volume: with the grid a multiple of B x S every CTA owns a frame range of ONE strip, and the
+// CTAs of the S strips walk the same frames and rows at the same pace, so a strip's x-halo
+// columns are read from L2 right after its neighbour fetched them).  A CTA's unit range
+// [u_begin, u_end) decomposes into column segments of ny y-blocks and ny + 1 x-blocks.
 struct T6Seg {
   int bt, s, yb0, ny;
 };
-__device__ __forceinline__ T6Seg t6_seg(long u, long u_end, int NBY, int S) {
-  const Seg g = seg_decode(u, u_end, NBY, S);
-  return T6Seg{g.bt, g.s, g.yb0, g.yb1 - g.yb0};
+__device__ __forceinline__ T6Seg t6_seg(long u, long u_end, int NBY, int S, int T) {
+  const long col = u / NBY;                 // (b, s, t)
+  const int yb0 = (int)(u - col * NBY);
+  const int t = (int)(col % T);
+  const long bs = col / T;
+  const int s = (int)(bs % S);
+  const int b = (int)(bs / S);
+  return T6Seg{b * T + t, s, yb0, (int)min((long)NBY - yb0, u_end - u)};
 }
 
 template <int R, int EPI>
@@ -288,7 +297,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     if (lane == 0) {
       unsigned n = 0;
       for (long u = u_begin; u < u_end;) {
-        const T6Seg sg = t6_seg(u, u_end, NBY, S);
+        const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
         const int x0 = sg.s * k6M - RA;
         for (int i = 0; i <= sg.ny; ++i, ++n) {
           const unsigned st = n & 1;
@@ -321,7 +330,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
           yg0 += (unsigned)ys.ny + 1;
         }
         if (yu >= u_end) return false;
-        ys = t6_seg(yu, u_end, NBY, S);
+        ys = t6_seg(yu, u_end, NBY, S, T);
         yj = 0;
         yrel = 0;
         yhave = true;
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       };
       bool ymore = y_next();
       for (long u = u_begin; u < u_end;) {
-        const T6Seg sg = t6_seg(u, u_end, NBY, S);
+        const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
         for (int i = 0; i <= sg.ny; ++i) {
           issue_x();
           // y-blocks whose x-blocks were all issued before this one (their split ran under it)
@@ -400,7 +409,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     // ================================================================== splitters (warps 2-5)
     unsigned total = 0;
     for (long u = u_begin; u < u_end;) {
-      const T6Seg sg = t6_seg(u, u_end, NBY, S);
+      const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
       total += (unsigned)sg.ny + 1;
       u += sg.ny;
     }
@@ -488,7 +497,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       }
       if (!fhave) {
         if (fu >= u_end) return;
-        fs = t6_seg(fu, u_end, NBY, S);
+        fs = t6_seg(fu, u_end, NBY, S, T);
         fj = 0;
         fhave = true;
       }
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     }
     unsigned m = 0;
     for (long u = u_begin; u < u_end;) {
-      const T6Seg sg = t6_seg(u, u_end, NBY, S);
+      const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
       const int vol = sg.bt / T;
       if (vol != cur_vol) {
         if (cur_vol >= 0) flush(cur_vol);
@@ -535,22 +544,39 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
               : "memory");
           t6_wait_ld();
           if (!xin) continue;
+          // one element per row: F from the shared tile, p (and the options) stored through
+          // running pointers; full 16-row chunks take the branch-free path
+          const int r0 = 16 * c;
+          const float* fr = ft + r0 * k6M;
+          float* op = P.out + base + (long)r0 * Wp;
+          if (r0 + 16 <= nrow && !OPT) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int r = 16 * c + i;
-            if (r >= nrow) break;
-            const long off = base + (long)r * Wp;
-            const float f = ft[r * k6M];
-            const float uu = __uint_as_float(q[i]) * usc;
-            const float yv = f * uu;
-            s0 = fmaf(yv, yv, s0);
-            if (OPT) {
-              if (P.pprev) s1 = fmaf(__ldcg(P.pprev + off), uu * cmask, s1);
-              if (P.tape_u) P.tape_u[off] = uu * cmask;
+            for (int i = 0; i < 16; ++i) {
+              const float f = fr[i * k6M];
+              const float yv = f * (__uint_as_float(q[i]) * usc);
+              s0 = fmaf(yv, yv, s0);
+              const float pv = P.last ? yv : f * yv;
+              pmax = fmaxf(pmax, fabsf(pv));
+              *op = pv;
+              op += Wp;
             }
-            const float pv = P.last ? yv : f * yv;
-            pmax = fmaxf(pmax, fabsf(pv));
-            P.out[off] = pv;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (r0 + i >= nrow) break;
+              const long off = base + (long)(r0 + i) * Wp;
+              const float f = fr[i * k6M];
+              const float uu = __uint_as_float(q[i]) * usc;
+              const float yv = f * uu;
+              s0 = fmaf(yv, yv, s0);
+              if (OPT) {
+                if (P.pprev) s1 = fmaf(__ldcg(P.pprev + off), uu * cmask, s1);
+                if (P.tape_u) P.tape_u[off] = uu * cmask;
+              }
+              const float pv = P.last ? yv : f * yv;
+              pmax = fmaxf(pmax, fabsf(pv));
+              P.out[off] = pv;
+            }
           }
         }
         t6_fence_before();
@@ -566,6 +592,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     if (cur_vol >= 0) flush(cur_vol);
   }
 #ifdef T6_PROFILE
+  if (warp == 6 && lane == 0) printf("[t6cta] %d %lld\n", blockIdx.x, clock64() - prof_t0);
   if (blockIdx.x == 0 && lane == 0 && (warp <= 2 || warp == 6))
     printf("[t6prof] warp %d total %lld waits: prod sempty %lld fempty %lld | iss sfull %lld d1empty %lld qfull %lld "
            "d2empty %lld | split d1full %lld sfree %lld | epi ffull %lld d2full %lld\n",

@@ -139,14 +139,17 @@ def test_forward_path_selection(lib):
     """Host-side plan introspection: which forward kernels a problem runs on, per algo."""
     import paper_2212_08058_b200 as m
     shp = (1, 70, 480, 854)
-    assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24)) == (m.PATH_TWO_PASS_TC_F16, 6, 24)
+    assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24)) == (m.PATH_TWO_PASS_TCGEN05, 6, 24)
     assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3)) == (m.PATH_FUSED_3D, 1, 3)
     # spatial radii below the tensor-core kernel's smallest compiled radius: FP32 pass
     assert m.forward_path(shp, m.Gauss(2.0, 2.0, 6, 6))[0] == m.PATH_TWO_PASS_FP32
     # requested radii round up to compiled ones (extra taps are zero)
     assert m.forward_path(shp, m.Gauss(1.5, 6.0, 5, 17))[1:] == (5, 18)
     assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3), m.ALGO_TWO_PASS)[0] == m.PATH_TWO_PASS_FP32
-    assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS)[0] == m.PATH_TWO_PASS_TC_F16
+    assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS)[0] == m.PATH_TWO_PASS_TCGEN05
+    assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_TCGEN05)[0] == m.PATH_TWO_PASS_TCGEN05
+    # radii outside the tcgen05 kernel's set (c5's r_s = 36): the mma.sync fp16 pass
+    assert m.forward_path(shp, m.Gauss(3.0, 12.0, 9, 36))[0] == m.PATH_TWO_PASS_TC_F16
     assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_MMA_SYNC)[0] == m.PATH_TWO_PASS_TC
     assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_FP32)[0] == m.PATH_TWO_PASS_FP32
     assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_MMA_F16)[0] == m.PATH_TWO_PASS_TC_F16

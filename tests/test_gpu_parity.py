@@ -444,8 +444,8 @@ def test_backward_user_x0(sf):
 
 
 @pytest.mark.parametrize("algo,radii,expect", [
-    ("auto", (6, 24), "f16"), ("auto", (1, 3), "f3d"), ("fp32", (6, 24), "fp32"), ("two", (1, 3), "fp32"),
-    ("mma", (6, 24), "tc"),
+    ("auto", (6, 24), "t6"), ("auto", (1, 3), "f3d"), ("fp32", (6, 24), "fp32"), ("two", (1, 3), "fp32"),
+    ("mma", (6, 24), "tc"), ("f16", (6, 24), "f16"),
 ])
 def test_reported_path_is_the_launched_path(sf, algo, radii, expect):
     """sfseg_forward_path's answer matches the kernels that actually run (per-category
@@ -454,10 +454,10 @@ def test_reported_path_is_the_launched_path(sf, algo, radii, expect):
     g = sf.Gauss(r_t / 3.0 if r_t > 1 else 0.5, r_s / 3.0, r_t, r_s)
     shape = (1, 14, 64, 140)
     sel = {"auto": sf.ALGO_AUTO, "fp32": sf.ALGO_TWO_PASS_FP32, "two": sf.ALGO_TWO_PASS,
-           "mma": sf.ALGO_TWO_PASS_MMA_SYNC}[algo]
+           "mma": sf.ALGO_TWO_PASS_MMA_SYNC, "f16": sf.ALGO_TWO_PASS_MMA_F16}[algo]
     path = sf.forward_path(shape, g, sel)[0]
     want = {"tc": sf.PATH_TWO_PASS_TC, "f16": sf.PATH_TWO_PASS_TC_F16, "f3d": sf.PATH_FUSED_3D,
-            "fp32": sf.PATH_TWO_PASS_FP32}[expect]
+            "fp32": sf.PATH_TWO_PASS_FP32, "t6": sf.PATH_TWO_PASS_TCGEN05}[expect]
     assert path == want
     rng = np.random.default_rng(3)
     ch = torch.from_numpy((rng.random((1, 1) + shape[1:]) * 0.8 + 0.1).astype(np.float32)).cuda()
@@ -468,7 +468,7 @@ def test_reported_path_is_the_launched_path(sf, algo, radii, expect):
     s.forward(ch, [1.0])
     n = {k: v[1] for k, v in prof.read().items()}
     prof.close()
-    if expect in ("tc", "f16", "fp32"):
+    if expect in ("tc", "f16", "fp32", "t6"):
         assert n["tpass"] == 3 and n["spass"] == 3 and n["f3d"] == 0
     else:
         assert n["f3d"] == 3 and n["spass"] == 0 and n["tpass"] == 0

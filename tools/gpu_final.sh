@@ -15,11 +15,11 @@ for c in probe c4 c3 c2f c5; do
   timeout 900 python bench.py --config $c --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err
 done
 timeout 900 python bench.py --config c5 --slab-at-1 --steps 5 --no-cpu-baseline > $OUT/bench_c5_slab1.json 2> $OUT/bench_c5_slab1.err
-for a in fp32 mma tcgen05; do
+for a in fp32 mma f16; do
   timeout 900 python bench.py --algo $a --no-cpu-baseline --no-e2e > $OUT/bench_c2_$a.json 2> $OUT/bench_c2_$a.err
 done
 timeout 300 python tools/precision_c2.py c2 > $OUT/precision_c2.json 2> $OUT/precision_c2.err
-[ -x tools/tc05_rate ] && timeout 120 tools/tc05_rate > $OUT/tc05_rate.log 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/tc05_rate2 tools/tc05_rate2.cu && timeout 120 tools/tc05_rate2 > $OUT/tc05_rate2.log 2>&1
 for c in c2 probe c3; do
   BC="python bench.py --config $c --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
   $BC > $OUT/plain_$c.log 2>&1 && \
@@ -27,10 +27,10 @@ for c in c2 probe c3; do
 done
 BC="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 $BC > $OUT/plain_full.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:spass_tc -s 16 -c 1 -o $OUT/spass $BC > $OUT/ncu_spass.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:spass_tc6 -s 16 -c 1 -o $OUT/spass $BC > $OUT/ncu_spass.log 2>&1
 $BC > $OUT/plain_full2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:tpass -s 16 -c 1 -o $OUT/tpass $BC > $OUT/ncu_tpass.log 2>&1
-BT="python bench.py --algo tcgen05 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+BT="python bench.py --algo f16 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 $BT > $OUT/plain_full3.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:spass_tc5 -s 16 -c 1 -o $OUT/spass_tc5 $BT > $OUT/ncu_tc5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:spass_tc_kernel -s 16 -c 1 -o $OUT/spass_mma_f16 $BT > $OUT/ncu_mma_f16.log 2>&1
 echo done > $OUT/DONE
