@@ -27,6 +27,8 @@ struct CombineFullParams {
   double* partials;     // [B][T*gx]
   unsigned* counter;
   unsigned* err;
+  unsigned* amax;       // tcgen05 plain passes: max |a_0| (float bits, stride 2 kScal words) or null
+  unsigned* fmax;       // ... and max |F| per volume
   int B, Cs, Cf, T, H, W, Wp, act_s, act_f, gx;
   float bs, bf, p;
   float ws[kMaxC];
@@ -46,6 +48,7 @@ __global__ void __launch_bounds__(kEwThreads) combine_full_kernel(const __grid_c
   const float* ff = P.f_ch + (long)b * P.Cf * vol + (long)t * HW;
   const long dbase = (long)b * vol + (long)t * HW;
   double acc = 0.0;
+  float am = 0.f, fm = 0.f;
   for (int y = blockIdx.x; y < P.H; y += P.gx) {
     for (int x = threadIdx.x; x < P.Wp; x += kEwThreads) {
       const long po = (long)bt * HWp + (long)y * P.Wp + x;
@@ -65,6 +68,16 @@ __global__ void __launch_bounds__(kEwThreads) combine_full_kernel(const __grid_c
       P.U[po] = u;
       P.F[po] = f;
       P.a0[po] = a;
+      am = fmaxf(am, fabsf(a));
+      fm = fmaxf(fm, fabsf(f));
+    }
+  }
+  if (P.amax) {   // order-free maxima, one atomic per warp
+    const unsigned ma = __reduce_max_sync(0xffffffffu, __float_as_uint(am));
+    const unsigned mf = __reduce_max_sync(0xffffffffu, __float_as_uint(fm));
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(P.amax + (long)b * 2 * kScal, ma);
+      atomicMax(P.fmax + (long)b * 2 * kScal, mf);
     }
   }
   const double s = block_sum<kEwThreads>(acc, red);
@@ -95,6 +108,7 @@ struct FullEpiParams {
   unsigned* counter;
   unsigned* err;
   double* stats;
+  unsigned* amax;       // tcgen05 plain passes: max |a_k| per volume (the next stacked temporal pass's range)
   int B, T, H, Wp, W, K, k, last, gx;
   float inv_alpha;
 };
@@ -109,6 +123,7 @@ __global__ void __launch_bounds__(kEwThreads) full_epilogue_kernel(const __grid_
   const long HWp = (long)P.H * P.Wp;
   const long W4 = P.Wp / 4;
   double acc = 0.0;
+  float am = 0.f;
   for (int y = blockIdx.x; y < P.H; y += P.gx) {
     for (long x4 = threadIdx.x; x4 < W4; x4 += kEwThreads) {
       const long po = (long)bt * HWp + (long)y * P.Wp + 4 * x4;
@@ -131,8 +146,13 @@ __global__ void __launch_bounds__(kEwThreads) full_epilogue_kernel(const __grid_
         s2 = fmaf(yv[i], yv[i], s2);
       }
       *reinterpret_cast<float4*>(P.out + po) = make_float4(o[0], o[1], o[2], o[3]);
+      am = fmaxf(am, fmaxf(fmaxf(fabsf(o[0]), fabsf(o[1])), fmaxf(fabsf(o[2]), fabsf(o[3]))));
       acc += (double)s2;
     }
+  }
+  if (P.amax) {
+    const unsigned ma = __reduce_max_sync(0xffffffffu, __float_as_uint(am));
+    if ((threadIdx.x & 31) == 0) atomicMax(P.amax + (long)b * 2 * kScal, ma);
   }
   const double s = block_sum<kEwThreads>(acc, red);
   const long nper = (long)P.T * P.gx;

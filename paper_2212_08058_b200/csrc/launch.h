@@ -15,7 +15,8 @@ cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t s
 cudaError_t launch_tpass_fwd16(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_fwdf(int RT, const TpassParams& P, int B, cudaStream_t st);
-cudaError_t launch_tpass3(int RT, const Tpass3Params& P, int B, cudaStream_t st);
+// f16: the three outputs as two fp16 planes each (the tcgen05 plain passes; Tpass3Params F16 fields)
+cudaError_t launch_tpass3(int RT, const Tpass3Params& P, int B, cudaStream_t st, bool f16 = false);
 bool spass_tc_supported(int R);
 int spass_tc_occupancy(int R, int fmt = 0);
 int spass_tc_boxw(int R);

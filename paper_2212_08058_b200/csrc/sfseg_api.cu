@@ -1778,6 +1778,15 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   cp.p = (float)p;
   for (int c = 0; c < Cs; ++c) cp.ws[c] = ws_host[c];
   for (int c = 0; c < Cf; ++c) cp.wf[c] = wf_host[c];
+  // tcgen05 plain passes (no soft-binarisation): the stacked temporal pass writes fp16 planes with
+  // exponents from max |a| (slot SC_VMAX + (k & 1)) and max |F| (SC_VMAX + 5); e_c in SC_VMAX + 2 + c
+  const bool t6 = P.tc6 && !bin;
+  double* const scf = at<double>(ws, P.off_sc);
+  auto uslot = [&](int j) { return reinterpret_cast<unsigned*>(scf + SC_VMAX + j); };
+  if (t6) {
+    cp.amax = uslot(0);
+    cp.fmax = uslot(5);
+  }
   combine_full_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
   SF_CUDA(after_launch("combine_full", st));
 
@@ -1785,7 +1794,8 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   std::memset(&sp, 0, sizeof(sp));
   CUtensorMap vmap[3];
   for (int c = 0; c < 3; ++c)
-    if (!make_spass_fwd_tmap(&vmap[c], P, vin[c])) return SFSEG_ERR_CUDA;
+    if (!(t6 ? make_planes_tmap(&vmap[c], vin[c], P.W, P.H, P.BT, P.Wp) : make_spass_fwd_tmap(&vmap[c], P, vin[c])))
+      return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.plain = 1;
   sp.F = F;            // the full layout's pairwise map (fill_spass_common points at the hot path's F slot)
@@ -1803,6 +1813,17 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   tp.frame2 = P.H * P.Wp / 2;
   tp.T = (int)P.T;
   for (int i = 0; i < 2 * P.RT + 1; ++i) tp.g[i] = P.gt[i];
+  if (t6) {
+    float gsum = 0.f;
+    for (int i = 0; i < 2 * P.RT + 1; ++i) gsum += std::fabs(P.gt[i]);
+    tp.gsum = gsum * (1.f + 1e-5f);
+    tp.fmax_in = uslot(5);
+    tp.vexp_out = scf + SC_VMAX + 2;
+    sp.S = P.S6;
+    sp.NB = P.NB6;
+    sp.U = P.U6;
+    sp.G = P.G6;
+  }
   FullEpiParams ep;
   std::memset(&ep, 0, sizeof(ep));
   ep.ua = uo[0];
@@ -1829,7 +1850,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
 #ifndef SFSEG_FULL_FUSE
 #define SFSEG_FULL_FUSE 0
 #endif
-  const bool fuse = SFSEG_FULL_FUSE && P.tc;
+  const bool fuse = SFSEG_FULL_FUSE && P.tc && !t6;
   for (int k = 1; k <= K; ++k) {
     const bool bink = bin && k > bin->n_cont;  // Alg.1 STEP 3 after this iteration
     const int last = (k == K || bink) ? 1 : 0; // store y_k itself when it is binarised next
@@ -1837,13 +1858,29 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
     // its input's slot of the other parity (last read by the previous iteration)
     const int base = 3 * (k & 1), other = 3 * ((k + 1) & 1);
     for (int c = 0; c < 3; ++c)
-      tp.vmax[c] = P.f16 ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + base + c) : nullptr;
+      tp.vmax[c] = (P.f16 && !t6) ? reinterpret_cast<unsigned*>(at<double>(ws, P.off_sc) + SC_VMAX + base + c) : nullptr;
+    if (t6) {
+      tp.amax_in = uslot((k - 1) & 1);
+      tp.amax_zero = uslot(k & 1);
+    }
     {  // G_t*(S^p X), G_t*(F^2 S^p X), G_t*(F S^p X) in one pass over a and F
       ProfScope ps(P.prof, st, PC_TPASS);
-      SF_CUDA(launch_tpass3(P.RT, tp, (int)P.B, st));
+      SF_CUDA(launch_tpass3(P.RT, tp, (int)P.B, st, t6));
       SF_CUDA(after_launch("tpass3_full", st));
     }
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < 3 && t6; ++c) {   // u_c = G_xy v_c on the tcgen05 pass (plain epilogue)
+      sp.tmap = vmap[c];
+      sp.eslot = SC_VMAX + 2 + c;
+      sp.out = uo[c];
+      sp.k = k;
+      sp.plain = 1;
+      sp.full_epi = 0;
+      sp.last = last;
+      ProfScope ps(P.prof, st, PC_SPASS);
+      SF_CUDA(launch_spass_tc6(P.RS, sp, P.G6, st));
+      SF_CUDA(after_launch("spass_tc6_plain", st));
+    }
+    for (int c = 0; c < 3 && !t6; ++c) {
       const bool fc = fuse && c == 2;
       sp.tmap = vmap[c];
       sp.vslot = base + c;
@@ -1862,6 +1899,7 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
     if (!fuse) {
       ep.k = k;
       ep.last = last;
+      ep.amax = (t6 && !last) ? uslot(k & 1) : nullptr;
       full_epilogue_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ep);
       SF_CUDA(after_launch("full_epilogue", st));
     }

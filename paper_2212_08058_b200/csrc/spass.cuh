@@ -104,6 +104,7 @@ struct SpassParams {
                            //   pass that produced v)
   int vzero;               // > 0: the pass zeroes slot vzero - 1 for the next temporal pass (the slot of
                            //   the other iteration parity); 0: none
+  int eslot;               // tcgen05 pass: sc slot of the data exponent e (0: SC_VEXP)
   int pslot;               // tcgen05 pass (spass_tc6): > 0 records max |p_k| per volume into
                            //   sc[SC_VMAX + pslot - 1] (the next TP_FWD16 temporal pass's range); 0: none
   const float* ua;         // full operator, fused combination (spass_tc EPI_FULL): G*(S^p X), G*(F^2 S^p X)

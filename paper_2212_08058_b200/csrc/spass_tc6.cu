@@ -14,7 +14,7 @@ cudaError_t launch_tc6_epi(const SpassParams& P, int grid, cudaStream_t st) {
 }
 template <int R>
 cudaError_t launch_tc6_one(const SpassParams& P, int grid, cudaStream_t st) {
-  if (P.plain) return cudaErrorInvalidValue;  // forward epilogues only (v arrives as fp16 planes)
+  if (P.plain) return launch_tc6_epi<R, EPI_PLAIN>(P, grid, st);
   if (P.tape_u || P.pprev) return launch_tc6_epi<R, EPI_FWD_OPT>(P, grid, st);
   return launch_tc6_epi<R, EPI_FWD>(P, grid, st);
 }

@@ -183,8 +183,11 @@ __device__ __forceinline__ float t6_w(const float* gsm, int d, int R) {
   const int a = d < 0 ? -d : d;
   return a <= R ? gsm[a] : 0.f;
 }
-// the data exponent e of volume b (written by the temporal pass, TP_FWD16)
-__device__ __forceinline__ int t6_vexp(const double* sc, int b) { return (int)sc[b * kScal + SC_VEXP]; }
+// the data exponent e of volume b (written by the temporal pass: TP_FWD16 into SC_VEXP, the stacked
+// full-operator pass into the slot P.eslot names)
+__device__ __forceinline__ int t6_vexp(const SpassParams& P, int b) {
+  return (int)P.sc[b * kScal + (P.eslot > 0 ? P.eslot : (int)SC_VEXP)];
+}
 
 // Segment walker shared by the roles.  Units are (volume b, strip s, frame t, 64-row y-block),
 // in that order (volume-major: the finalize's per-volume CTA ranges; strip-major inside a
@@ -213,6 +216,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
   constexpr int TXMIN = t6_txmin(R), TYMIN = t6_tymin(R);
   constexpr uint32_t TXPL = 32u * t6_txrows(R), TYPL = 32u * t6_tyrows(R);
   constexpr bool OPT = EPI == EPI_FWD_OPT;
+  constexpr bool PLAIN = EPI == EPI_PLAIN;   // u = G_xy v only (no F, no norm): the full operator's passes
   constexpr float TSC = (float)(1 << kF16TapExp);
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       tma_load_3d(reinterpret_cast<unsigned char*>(fbuf) + fb * k6FBytes, &P.fmap, &b_ffull[fb], fs.s * k6M,
                   k6YN * (fs.yb0 + fj), fs.bt);
     };
-    if (fissuer) {
+    if (fissuer && !PLAIN) {
       f_issue(0);
       f_issue(1);
     }
@@ -514,9 +518,9 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
       const int vol = sg.bt / T;
       if (vol != cur_vol) {
-        if (cur_vol >= 0) flush(cur_vol);
+        if (cur_vol >= 0 && !PLAIN) flush(cur_vol);
         cur_vol = vol;
-        usc = pow2f(-t6_vexp(P.sc, vol) - kF16TapExp) * (P.lag ? (float)P.sc[vol * kScal + SC_S] : 1.f);
+        usc = pow2f(-t6_vexp(P, vol) - kF16TapExp) * (P.lag ? (float)P.sc[vol * kScal + SC_S] : 1.f);
       }
       const int x = sg.s * k6M + xl;
       const bool xin = x < Wp;
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         const long base = ((long)sg.bt * H + y0) * Wp + x;
         const unsigned buf = m & 1;
         const float* ft = fbuf + buf * (k6FBytes / 4) + xl;
-        T6W(8, &b_ffull[buf], (m >> 1) & 1);
+        if (!PLAIN) T6W(8, &b_ffull[buf], (m >> 1) & 1);
         T6W(9, &b_d2full[buf], (m >> 1) & 1);
         t6_fence_after();
         float s0 = 0.f, s1 = 0.f;
@@ -549,16 +553,30 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
           const int r0 = 16 * c;
           const float* fr = ft + r0 * k6M;
           float* op = P.out + base + (long)r0 * Wp;
-          if (r0 + 16 <= nrow && !OPT) {
+          if (PLAIN) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (r0 + i >= nrow) break;
+              *op = __uint_as_float(q[i]) * usc * cmask;
+              op += Wp;
+            }
+          } else if (r0 + 16 <= nrow && (!OPT || !P.pprev)) {
+            // full chunk: branch-free, running pointers (the training forward's tape u included)
+            float* tp = OPT ? P.tape_u + (base + (long)r0 * Wp) : nullptr;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float f = fr[i * k6M];
-              const float yv = f * (__uint_as_float(q[i]) * usc);
+              const float uu = __uint_as_float(q[i]) * usc;
+              const float yv = f * uu;
               s0 = fmaf(yv, yv, s0);
               const float pv = P.last ? yv : f * yv;
               pmax = fmaxf(pmax, fabsf(pv));
               *op = pv;
               op += Wp;
+              if (OPT && tp) {
+                *tp = uu * cmask;
+                tp += Wp;
+              }
             }
           } else {
 #pragma unroll
@@ -582,14 +600,16 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         t6_fence_before();
         __syncwarp();
         if (lane == 0) t6_arrive(&b_d2empty[buf]);
-        asm volatile("bar.sync 2, 128;" ::: "memory");   // the group is done reading F tile buf
-        if (fissuer) f_issue(buf);
+        if (!PLAIN) {
+          asm volatile("bar.sync 2, 128;" ::: "memory");   // the group is done reading F tile buf
+          if (fissuer) f_issue(buf);
+        }
         acc0 += (double)s0;
         acc1 += (double)s1;
       }
       u += sg.ny;
     }
-    if (cur_vol >= 0) flush(cur_vol);
+    if (cur_vol >= 0 && !PLAIN) flush(cur_vol);
   }
 #ifdef T6_PROFILE
   if (warp == 6 && lane == 0) printf("[t6cta] %d %lld\n", blockIdx.x, clock64() - prof_t0);
@@ -606,7 +626,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     __syncwarp();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(k6TmemCols));
   }
-  spass_finalize<SP_FWD, k6Threads>(P, red, flag);
+  if (!PLAIN) spass_finalize<SP_FWD, k6Threads>(P, red, flag);
 }
 
 }  // namespace sfseg

@@ -32,12 +32,15 @@ cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t s
 cudaError_t launch_tpass_fwdf(int RT, const TpassParams& P, int B, cudaStream_t st) {
   return launch_tpass_t<TP_FWDF>(RT, P, B, st);
 }
-cudaError_t launch_tpass3(int RT, const Tpass3Params& P, int B, cudaStream_t st) {
+cudaError_t launch_tpass3(int RT, const Tpass3Params& P, int B, cudaStream_t st, bool f16) {
   dim3 grid((unsigned)((P.frame2 + kTpThreads - 1) / kTpThreads), (unsigned)B);
   switch (RT) {
 #define TP3_CASE(r)                                             \
   case r:                                                       \
-    tpass3_kernel<r><<<grid, kTpThreads, 0, st>>>(P);           \
+    if (f16)                                                    \
+      tpass3_kernel<r, true><<<grid, kTpThreads, 0, st>>>(P);   \
+    else                                                        \
+      tpass3_kernel<r, false><<<grid, kTpThreads, 0, st>>>(P);  \
     return cudaGetLastError();
     TP3_CASE(0) TP3_CASE(1) TP3_CASE(2) TP3_CASE(3) TP3_CASE(4) TP3_CASE(5) TP3_CASE(6) TP3_CASE(8) TP3_CASE(9)
     TP3_CASE(12) TP3_CASE(16)

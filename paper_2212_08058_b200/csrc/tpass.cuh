@@ -254,6 +254,13 @@ struct Tpass3Params {
   float* out[3];
   unsigned* vmax[3];       // per-output max |out| slots (fp16 spatial pass) or null
   const double* sc;
+  // F16 (tcgen05 plain passes): outputs as two fp16 planes of out_c 2^e_c; e_c from the bounds
+  // |out_a| <= s gsum max|a|, |out_b| <= s gsum max|F|^2 max|a|, |out_c| <= s gsum max|F| max|a|
+  const unsigned* amax_in;   // max |a| (float bits, stride 2 kScal words)
+  const unsigned* fmax_in;   // max |F|
+  unsigned* amax_zero;       // slot zeroed for the next epilogue's max |a_k| (or null)
+  double* vexp_out;          // sc + first exponent slot (stride kScal): e_c at vexp_out[c]
+  float gsum;
   long frame2;             // H*Wp/2 float2 per frame
   int T;
   float g[2 * kMaxRT + 1];
@@ -263,7 +270,7 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
 
-template <int RT>
+template <int RT, bool F16 = false>
 __global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constant__ Tpass3Params P) {
   constexpr int NR = 2 * RT + 1;
   constexpr int NS = 8;
@@ -278,6 +285,21 @@ __global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constan
   const float2* A = reinterpret_cast<const float2*>(P.a) + b * vol2 + ec;
   const float2* Fp = reinterpret_cast<const float2*>(P.F) + b * vol2 + ec;
   const float scale = (float)P.sc[b * kScal + SC_S];
+  float m16[3] = {1.f, 1.f, 1.f};   // F16: s 2^e_c
+  if (F16) {
+    const float ma = __uint_as_float(P.amax_in[(long)b * 2 * kScal]);
+    const float mf = __uint_as_float(P.fmax_in[(long)b * 2 * kScal]);
+    const float bound[3] = {scale * ma * P.gsum, scale * mf * mf * ma * P.gsum, scale * mf * ma * P.gsum};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      int ex = 0;
+      if (bound[c] > 0.f && bound[c] <= 3.4e38f) frexpf(bound[c], &ex);
+      const int e = min(max(kF16DataExp - ex, -100), 100);
+      m16[c] = scale * __int_as_float((127 + e) << 23);
+      if (blockIdx.x == 0 && tid == 0) P.vexp_out[(long)b * kScal + c] = (double)e;
+    }
+    if (blockIdx.x == 0 && tid == 0 && P.amax_zero) P.amax_zero[(long)b * 2 * kScal] = 0u;
+  }
   const int jend = T + 2 * RT;
   auto issue = [&](int jp) {
     const int j = jp - RT;
@@ -322,7 +344,16 @@ __global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constan
       }
       const int slot0 = (((d - 2 * RT) % NR) + NR) % NR;
       const int t = jp - 2 * RT;
-      if (active && t >= 0 && t < T) {
+      if (F16 && active && t >= 0 && t < T) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {   // planes [bt][plane][H][Wp] halves: hi, then lo at + frame2
+          uint32_t h[2];
+          split_planes_f16<2>(acc[c][slot0].x * m16[c], acc[c][slot0].y * m16[c], h);
+          uint32_t* o32 = reinterpret_cast<uint32_t*>(P.out[c]) + ((long)b * T + t) * 2 * P.frame2 + ec;
+          __stcg(o32, h[0]);
+          __stcg(o32 + P.frame2, h[1]);
+        }
+      } else if (active && t >= 0 && t < T) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const float2 o = make_float2(acc[c][slot0].x * scale, acc[c][slot0].y * scale);
@@ -335,7 +366,7 @@ __global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constan
     }
   }
   cp_async_wait<0>();
-  if (P.vmax[0]) {
+  if (!F16 && P.vmax[0]) {
     __shared__ unsigned wm[3][kTpThreads / 32];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
