@@ -245,6 +245,8 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
 #ifdef T6_PROFILE
   long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const long long prof_t0 = clock64();
+  unsigned long long g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
 #endif
   const long u_begin = (long)blockIdx.x * P.U / P.G;
   const long u_end = (long)(blockIdx.x + 1) * P.U / P.G;
@@ -612,7 +614,11 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     if (cur_vol >= 0 && !PLAIN) flush(cur_vol);
   }
 #ifdef T6_PROFILE
-  if (warp == 6 && lane == 0) printf("[t6cta] %d %lld\n", blockIdx.x, clock64() - prof_t0);
+  if (warp == 6 && lane == 0) {
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    printf("[t6cta] %d %lld %llu %llu\n", blockIdx.x, clock64() - prof_t0, g0, g1);
+  }
   if (blockIdx.x == 0 && lane == 0 && (warp <= 2 || warp == 6))
     printf("[t6prof] warp %d total %lld waits: prod sempty %lld fempty %lld | iss sfull %lld d1empty %lld qfull %lld "
            "d2empty %lld | split d1full %lld sfree %lld | epi ffull %lld d2full %lld\n",

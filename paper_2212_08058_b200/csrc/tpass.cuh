@@ -55,6 +55,9 @@ __host__ __device__ constexpr int tpass_min_blocks(int RT) { return RT <= 6 ? 6 
 __host__ __device__ constexpr int tpass_stages(int MODE) {
   return (MODE == TP_FWD || MODE == TP_FWD16) ? 12 : (MODE == TP_FWDF ? 6 : 4);
 }
+#ifndef TPASS16_HINT
+#define TPASS16_HINT 1  // A/B: TP_FWD16 stores v's planes with an L2 evict-last policy (0: .cg stores)
+#endif
 constexpr int kF16DataExp = 14;  // TP_FWD16: |v 2^e| < 2^14 (fp16 max 65504)
 __device__ __forceinline__ void st_u2_hint(uint2* ptr, uint2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol)
@@ -215,8 +218,13 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
         split_planes_f16<2>(o.x, o.y, h0);
         split_planes_f16<2>(o.z, o.w, h1);
         uint2* dst = o16 + (long)(TPASS_REV ? T - 1 - t : t) * 2 * P.frame4;
-        st_u2_hint(dst, make_uint2(h0[0], h1[0]), pol);
-        st_u2_hint(dst + P.frame4, make_uint2(h0[1], h1[1]), pol);
+        if (TPASS16_HINT) {
+          st_u2_hint(dst, make_uint2(h0[0], h1[0]), pol);
+          st_u2_hint(dst + P.frame4, make_uint2(h0[1], h1[1]), pol);
+        } else {
+          __stcg(dst, make_uint2(h0[0], h1[0]));
+          __stcg(dst + P.frame4, make_uint2(h0[1], h1[1]));
+        }
       } else if (active && t >= 0 && t < T) {
         const float4 o = f4_scale(acc[slot0], scale);
         float4* dst = out + (long)(TPASS_REV ? T - 1 - t : t) * P.frame4;
