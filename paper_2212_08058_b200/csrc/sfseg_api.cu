@@ -490,7 +490,12 @@ void fill_tpass_common(TpassParams& tp, const Plan& P, void* ws) {
   tp.sc = at<double>(ws, P.off_sc);
   tp.frame4 = P.H * P.Wp / 4;
   tp.T = (int)P.T;
-  for (int i = 0; i < 2 * P.RT + 1; ++i) tp.g[i] = P.gt[i];
+  for (int i = 0; i < 2 * P.RT + 1; ++i) {
+    tp.g[i] = P.gt[i];
+    uint32_t b;
+    std::memcpy(&b, &P.gt[i], 4);
+    tp.g2[i] = (unsigned long long)b | ((unsigned long long)b << 32);
+  }
 }
 
 bool validate_act(int act) { return act == SFSEG_ACT_IDENTITY || act == SFSEG_ACT_SIGMOID; }

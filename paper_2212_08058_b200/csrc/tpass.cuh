@@ -41,6 +41,7 @@ struct TpassParams {
   int T;
   int fexp;              // FWDF: exponent of F multiplying the source (1 or 2)
   float g[2 * kMaxRT + 1];  // g[i] = weight of temporal offset i - RT
+  unsigned long long g2[2 * kMaxRT + 1];  // {g[i], g[i]} packed for fma.rn.f32x2 (set by fill_tpass_common)
 };
 
 constexpr int kTpThreads = 128;
@@ -53,12 +54,31 @@ constexpr int kTpThreads = 128;
 __host__ __device__ constexpr int tpass_min_blocks(int RT) { return RT <= 6 ? 6 : (RT <= 9 ? 4 : 2); }
 // cp.async stages per input stream (frames prefetched ahead of the ring).
 __host__ __device__ constexpr int tpass_stages(int MODE) {
-  return (MODE == TP_FWD || MODE == TP_FWD16) ? 12 : (MODE == TP_FWDF ? 6 : 4);
+  return (MODE == TP_FWD || MODE == TP_FWD16) ? 16 : (MODE == TP_FWDF ? 8 : 4);   // powers of two: no modulo code
 }
 #ifndef TPASS16_HINT
 #define TPASS16_HINT 1  // A/B: TP_FWD16 stores v's planes with an L2 evict-last policy (0: .cg stores)
 #endif
 constexpr int kF16DataExp = 14;  // TP_FWD16: |v 2^e| < 2^14 (fp16 max 65504)
+// register-pair (un)packing: mov.b64 lets ptxas allocate the pair instead of emitting shifts / ORs
+__device__ __forceinline__ unsigned long long pack_f2(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_f2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ float4 unpack_f4(unsigned long long xy, unsigned long long zw) {
+  const float2 a = unpack_f2(xy), b = unpack_f2(zw);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+// acc = w * v + acc on two packed fp32 lanes (sm_100 fma.rn.f32x2: the same rounding as two FFMA)
+__device__ __forceinline__ void ffma2(unsigned long long& acc, unsigned long long w, unsigned long long v) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(w), "l"(v));
+}
 __device__ __forceinline__ void st_u2_hint(uint2* ptr, uint2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol)
                : "memory");
@@ -186,9 +206,11 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   // forward: keep v in L2 for the spatial pass that reads it next (and its halo re-reads)
   const uint64_t pol = (MODE == TP_FWD || F16) ? l2_policy_evict_last() : 0ull;
   uint2* const o16 = F16 ? reinterpret_cast<uint2*>(P.out) + (long)b * T * 2 * P.frame4 + ec : nullptr;
-  float4 acc[NR];
+  // the ring of 2RT+1 partial outputs: float4 as two packed float2 (fma.rn.f32x2 = FFMA2: half
+  // the FMA instructions of a pass that is issue-bound, profiles/r02e/tpass_ncu.txt)
+  unsigned long long acc[NR][2];
 #pragma unroll
-  for (int i = 0; i < NR; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = 0; i < NR; ++i) acc[i][0] = acc[i][1] = 0ull;
   float vm = 0.f;  // max |out| of this thread (FWD with vmax)
 #pragma unroll
   for (int d = 0; d < NS; ++d) issue(d);
@@ -201,19 +223,20 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
       const float4 val = fetch(jp);
       issue(jp + NS);  // refill the slot just read
 #pragma unroll
+      const unsigned long long vxy = pack_f2(val.x, val.y), vzw = pack_f2(val.z, val.w);
+#pragma unroll
       for (int ee = 0; ee < NR; ++ee) {
         // input j feeds output t = j - RT + ee with weight g[(j - t) + RT] = g[2RT - ee]
         const int slot = (((d - 2 * RT + ee) % NR) + NR) % NR;
-        const float w = P.g[2 * RT - ee];
-        acc[slot].x = fmaf(w, val.x, acc[slot].x);
-        acc[slot].y = fmaf(w, val.y, acc[slot].y);
-        acc[slot].z = fmaf(w, val.z, acc[slot].z);
-        acc[slot].w = fmaf(w, val.w, acc[slot].w);
+        const unsigned long long w2 = P.g2[2 * RT - ee];
+        ffma2(acc[slot][0], w2, vxy);
+        ffma2(acc[slot][1], w2, vzw);
       }
       const int slot0 = (((d - 2 * RT) % NR) + NR) % NR;
       const int t = jp - 2 * RT;
+      const float4 a4 = unpack_f4(acc[slot0][0], acc[slot0][1]);
       if (F16 && active && t >= 0 && t < T) {
-        const float4 o = f4_scale(acc[slot0], m16);
+        const float4 o = f4_scale(a4, m16);
         uint32_t h0[2], h1[2];
         split_planes_f16<2>(o.x, o.y, h0);
         split_planes_f16<2>(o.z, o.w, h1);
@@ -226,13 +249,13 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
           __stcg(dst + P.frame4, make_uint2(h0[1], h1[1]));
         }
       } else if (active && t >= 0 && t < T) {
-        const float4 o = f4_scale(acc[slot0], scale);
+        const float4 o = f4_scale(a4, scale);
         float4* dst = out + (long)(TPASS_REV ? T - 1 - t : t) * P.frame4;
         if (MODE == TP_FWD) st_f4_hint(dst, o, pol);
         else __stcg(dst, o);
         vm = fmaxf(vm, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
       }
-      acc[slot0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[slot0][0] = acc[slot0][1] = 0ull;
     }
   }
   cp_async_wait<0>();
