@@ -1817,7 +1817,12 @@ sfseg_status sfseg_power_iterate_full(const float* s_ch, int32_t Cs, const float
   tp.sc = at<double>(ws, P.off_sc);
   tp.frame2 = P.H * P.Wp / 2;
   tp.T = (int)P.T;
-  for (int i = 0; i < 2 * P.RT + 1; ++i) tp.g[i] = P.gt[i];
+  for (int i = 0; i < 2 * P.RT + 1; ++i) {
+    tp.g[i] = P.gt[i];
+    uint32_t gb;
+    std::memcpy(&gb, &P.gt[i], 4);
+    tp.g2[i] = (unsigned long long)gb | ((unsigned long long)gb << 32);
+  }
   if (t6) {
     float gsum = 0.f;
     for (int i = 0; i < 2 * P.RT + 1; ++i) gsum += std::fabs(P.gt[i]);

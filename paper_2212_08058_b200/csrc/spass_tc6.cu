@@ -20,7 +20,7 @@ cudaError_t launch_tc6_one(const SpassParams& P, int grid, cudaStream_t st) {
 }
 }  // namespace
 
-#define T6_RADII(X) X(8) X(9) X(12) X(16) X(18) X(24)
+#define T6_RADII(X) X(8) X(9) X(12) X(16) X(18) X(24) X(32) X(36)
 
 bool spass_tc6_supported(int R) {
   switch (R) {

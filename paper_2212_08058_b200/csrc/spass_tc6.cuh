@@ -58,10 +58,8 @@ constexpr int k6Slots = 8;      // Q ring chunks (32 rows each)
 constexpr uint32_t k6ColQ = 0, k6ColD1 = 256, k6ColD2 = 384;  // D1, D2: two 64-column buffers each
 constexpr uint32_t k6TmemCols = 512;
 constexpr int k6BoxW = 64;      // TMA box columns: 128 B, SWIZZLE_128B
-constexpr int k6NBox = 3;
 constexpr uint32_t k6PlaneBox = k6XN * k6BoxW * 2;       // 8 KB: one plane of one box
 constexpr uint32_t k6BoxBytes = 2 * k6PlaneBox;          // both planes (one TMA)
-constexpr uint32_t k6StageBytes = k6NBox * k6BoxBytes;   // 48 KB
 constexpr int k6Stages = 2;
 constexpr uint32_t k6FBytes = k6YN * k6M * 4;            // 32 KB: the F tile of one y-block (fp32)
 
@@ -73,11 +71,21 @@ __host__ __device__ constexpr int t6_txmin(int R) { return -16 * (t6_nkx(R) - 1)
 __host__ __device__ constexpr int t6_txrows(int R) { return k6M - t6_txmin(R); }
 __host__ __device__ constexpr int t6_tymin(int R) { return -16 * (t6_jhi(R) - 1); }
 __host__ __device__ constexpr int t6_tyrows(int R) { return k6YN - 16 * t6_jlo(R) - t6_tymin(R); }
-// y-block j reads local chunks 2j .. 2j + 3 (R <= 32): x-blocks j and j + 1
-__host__ __device__ constexpr int t6_xneed(int j) { return j + 1; }
+// 64-column TMA boxes per stage (3 for r_s <= 32, 4 for r_s = 36) and the stage size
+__host__ __device__ constexpr int t6_nbox(int R) { return (16 * t6_nkx(R) + k6BoxW - 1) / k6BoxW; }
+__host__ __device__ constexpr uint32_t t6_stage_bytes(int R) { return (uint32_t)t6_nbox(R) * k6BoxBytes; }
+// chunk origin: local chunk c covers rows R0 - 32 OFF + 32 c (OFF = 1 for r_s <= 32, 2 above), so
+// the first y-block's window never starts before chunk 0; y-block j's k step kk reads chunk
+// 2j + (kk + 2 OFF) / 2 (half (kk + 2 OFF) & 1)
+__host__ __device__ constexpr int t6_off(int R) { return (R + 31) / 32; }
+__host__ __device__ constexpr int t6_cfirst(int R) { return (t6_jlo(R) + 2 * t6_off(R)) / 2; }    // + 2j
+__host__ __device__ constexpr int t6_clast(int R) { return (t6_jhi(R) - 1 + 2 * t6_off(R)) / 2; }  // + 2j
+// the x-block (two chunks) holding y-block j's last chunk, and x-blocks per segment of ny y-blocks
+__host__ __device__ constexpr int t6_xneed(int R, int j) { return (2 * j + t6_clast(R)) / 2; }
+__host__ __device__ constexpr int t6_nx(int R, int ny) { return t6_xneed(R, ny - 1) + 1; }
 __host__ __device__ constexpr size_t t6_smem_bytes(int R) {
-  return 1024 + (size_t)k6Stages * k6StageBytes + 2 * (size_t)k6FBytes + 2 * 32 * (size_t)t6_txrows(R) +
-         2 * 32 * (size_t)t6_tyrows(R) + 512;
+  return 1024 + (size_t)k6Stages * t6_stage_bytes(R) + 2 * (size_t)k6FBytes + 2 * 32 * (size_t)t6_txrows(R) +
+         2 * 32 * (size_t)t6_tyrows(R) + 512;   // 512: 30 mbarriers, the TMEM slot, 16 doubles, a flag
 }
 
 __device__ __forceinline__ uint64_t t6_desc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -210,8 +218,11 @@ __device__ __forceinline__ T6Seg t6_seg(long u, long u_end, int NBY, int S, int 
 
 template <int R, int EPI>
 __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_constant__ SpassParams P) {
-  static_assert(R <= 32 && t6_jlo(R) >= -2 && t6_jhi(R) <= 6, "tcgen05 spatial pass: radii <= 32");
-  static_assert(16 * t6_nkx(R) <= k6NBox * k6BoxW, "x window fits the three TMA boxes");
+  static_assert(R <= 40 && t6_jlo(R) >= -2 * t6_off(R), "tcgen05 spatial pass: radii <= 40");
+  // Q ring: x(n) overwrites chunks 2n - 8, 2n - 7; every y-block reading them needs x-blocks <= n - 1
+  static_assert(t6_clast(R) - t6_cfirst(R) + 1 <= 6, "a y window spans at most six ring chunks");
+  constexpr int NBOX = t6_nbox(R), OFF = t6_off(R), CF = t6_cfirst(R);
+  constexpr uint32_t SBYTES = t6_stage_bytes(R);
   constexpr int RA = t6_ra(R), NKX = t6_nkx(R), JLO = t6_jlo(R), JHI = t6_jhi(R);
   constexpr int TXMIN = t6_txmin(R), TYMIN = t6_tymin(R);
   constexpr uint32_t TXPL = 32u * t6_txrows(R), TYPL = 32u * t6_tyrows(R);
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* stage = smem;                                    // [2][3 boxes][2 planes][64 rows][128 B]
-  float* fbuf = reinterpret_cast<float*>(stage + k6Stages * k6StageBytes);  // [2][64 rows][128 cols]
+  float* fbuf = reinterpret_cast<float*>(stage + k6Stages * SBYTES);  // [2][64 rows][128 cols]
   unsigned char* txb = reinterpret_cast<unsigned char*>(fbuf) + 2 * k6FBytes;   // [2 planes][TXPL]
   unsigned char* tyb = txb + 2 * TXPL;                            // [2 planes][TYPL]
   uint64_t* bars = reinterpret_cast<uint64_t*>(tyb + 2 * TYPL);
@@ -230,15 +241,18 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
   uint64_t* b_sempty = bars + 2;   // [2] x-pass done reading the stage (commit)
   uint64_t* b_d1full = bars + 4;   // [2] x-pass done (commit)
   uint64_t* b_d1empty = bars + 6;  // [2] D1 split into Q (4 splitter warps)
-  uint64_t* b_qfull = bars + 8;    // [2] x-block's Q chunks written (4 splitter warps)
-  uint64_t* b_d2full = bars + 10;  // [2] y-pass done (commit)
-  uint64_t* b_d2empty = bars + 12; // [2] D2 drained (4 epilogue warps)
-  uint64_t* b_ffull = bars + 14;   // [2] F tile landed
-  uint64_t* b_sfree = bars + 18;   // [8] ring chunk dead (commit after its last y-pass)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
-  double* red = reinterpret_cast<double*>(bars + 28);   // 16 doubles
+  uint64_t* b_d2full = bars + 8;   // [2] y-pass done (commit)
+  uint64_t* b_d2empty = bars + 10; // [2] D2 drained (4 epilogue warps)
+  uint64_t* b_ffull = bars + 12;   // [2] F tile landed
+  uint64_t* b_sfree = bars + 14;   // [8] ring chunk dead (commit after its last y-pass)
+  // [8] x-block n's Q chunks written (4 splitter warps), barrier n & 7: the splitter can finish
+  // x-blocks up to 3 ahead of the issuer's wait (r_s > 32: a segment's y-blocks need the x-block
+  // two past their own), so two barriers by parity would alias phases
+  uint64_t* b_qfull = bars + 22;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
+  double* red = reinterpret_cast<double*>(bars + 32);   // 16 doubles
   int* flag = reinterpret_cast<int*>(red + 16);
-  __shared__ float gsm[kMaxRS + 1];
+  float* const gsm = reinterpret_cast<float*>(stage);   // the taps, only until the bands are built
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = P.H, W = P.W, Wp = P.Wp, S = P.S, T = P.T, NBY = P.NB;
@@ -258,12 +272,14 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       mbar_init(&b_sempty[i], 1);
       mbar_init(&b_d1full[i], 1);
       mbar_init(&b_d1empty[i], 4);
-      mbar_init(&b_qfull[i], 4);
       mbar_init(&b_d2full[i], 1);
       mbar_init(&b_d2empty[i], 4);
       mbar_init(&b_ffull[i], 1);
     }
-    for (int i = 0; i < k6Slots; ++i) mbar_init(&b_sfree[i], 1);
+    for (int i = 0; i < k6Slots; ++i) {
+      mbar_init(&b_sfree[i], 1);
+      mbar_init(&b_qfull[i], 4);
+    }
     fence_barrier_init();
     prefetch_tmap(&P.tmap);
     prefetch_tmap(&P.fmap);
@@ -305,14 +321,14 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       for (long u = u_begin; u < u_end;) {
         const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
         const int x0 = sg.s * k6M - RA;
-        for (int i = 0; i <= sg.ny; ++i, ++n) {
+        for (int i = 0; i < t6_nx(R, sg.ny); ++i, ++n) {
           const unsigned st = n & 1;
           T6W(0, &b_sempty[st], ((n >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&b_sfull[st], k6StageBytes);
-          const int row0 = k6YN * sg.yb0 - 32 + k6XN * i;
+          mbar_arrive_expect_tx(&b_sfull[st], SBYTES);
+          const int row0 = k6YN * sg.yb0 - 32 * OFF + k6XN * i;
 #pragma unroll
-          for (int bx = 0; bx < k6NBox; ++bx)
-            tma_load_3d(stage + st * k6StageBytes + bx * k6BoxBytes, &P.tmap, &b_sfull[st], x0 + k6BoxW * bx, row0,
+          for (int bx = 0; bx < NBOX; ++bx)
+            tma_load_3d(stage + st * SBYTES + bx * k6BoxBytes, &P.tmap, &b_sfull[st], x0 + k6BoxW * bx, row0,
                         2 * sg.bt);
         }
         u += sg.ny;
@@ -333,7 +349,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         if (yhave && ++yj < ys.ny) return true;
         if (yhave) {
           yu += ys.ny;
-          yg0 += (unsigned)ys.ny + 1;
+          yg0 += (unsigned)t6_nx(R, ys.ny);
         }
         if (yu >= u_end) return false;
         ys = t6_seg(yu, u_end, NBY, S, T);
@@ -348,7 +364,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         T6W(3, &b_d1empty[db], ((nx >> 1) & 1) ^ 1);
         t6_fence_after();
         const uint32_t d = tmem + k6ColD1 + k6XN * db;
-        const uint64_t bd0 = t6_desc_sw128(st0 + st * k6StageBytes);
+        const uint64_t bd0 = t6_desc_sw128(st0 + st * SBYTES);
         // products (data plane, tap plane): the two corrections first, the leading one last.
         // Descriptor start addresses advance by (byte offset >> 4) in the low field.
 #pragma unroll
@@ -366,9 +382,9 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         ++nx;
       };
       auto issue_y = [&]() {
-        const unsigned need = yg0 + (unsigned)t6_xneed(yj);
+        const unsigned need = yg0 + (unsigned)t6_xneed(R, yj);
         while (nq <= need) {
-          T6W(4, &b_qfull[nq & 1], (nq >> 1) & 1);
+          T6W(4, &b_qfull[nq & 7], (nq >> 3) & 1);
           ++nq;
         }
         const unsigned buf = ny & 1;
@@ -381,25 +397,25 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
           const int pa = pp == 0 ? 1 : 0, pg = pp == 1 ? 1 : 0;
 #pragma unroll
           for (int kk = JLO; kk < JHI; ++kk) {
-            const uint32_t slot = (c0 + (unsigned)((kk + 2) / 2)) % k6Slots;
-            const uint32_t a = tmem + k6ColQ + 32 * slot + 16 * pa + 8 * ((kk + 2) & 1);
+            const uint32_t slot = (c0 + (unsigned)((kk + 2 * OFF) / 2)) % k6Slots;
+            const uint32_t a = tmem + k6ColQ + 32 * slot + 16 * pa + 8 * ((kk + 2 * OFF) & 1);
             const uint64_t bd = yd0 + (uint64_t)((pg * TYPL + (uint32_t)(-16 * kk - TYMIN) * 32) >> 4);
             t6_mma_ts_e(d, a, bd, idy, (pp > 0 || kk > JLO) ? 1u : 0u);
           }
         }
         t6_commit_e(&b_d2full[buf]);
         // chunks no later y-block of the segment reads are dead
-        const int target = (yj + 1 < ys.ny) ? 2 * (yj + 1) : 2 * (ys.ny + 1);
+        const int target = (yj + 1 < ys.ny) ? 2 * (yj + 1) + CF : 2 * t6_nx(R, ys.ny);
         for (; yrel < target; ++yrel) t6_commit_e(&b_sfree[(2u * yg0 + (unsigned)yrel) % k6Slots]);
         ++ny;
       };
       bool ymore = y_next();
       for (long u = u_begin; u < u_end;) {
         const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
-        for (int i = 0; i <= sg.ny; ++i) {
+        for (int i = 0; i < t6_nx(R, sg.ny); ++i) {
           issue_x();
           // y-blocks whose x-blocks were all issued before this one (their split ran under it)
-          while (ymore && yg0 + (unsigned)t6_xneed(yj) + 2 <= nx) {
+          while (ymore && yg0 + (unsigned)t6_xneed(R, yj) + 2 <= nx) {
             issue_y();
             ymore = y_next();
           }
@@ -416,7 +432,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     unsigned total = 0;
     for (long u = u_begin; u < u_end;) {
       const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
-      total += (unsigned)sg.ny + 1;
+      total += (unsigned)t6_nx(R, sg.ny);
       u += sg.ny;
     }
     constexpr float QSC = 1.f / (float)(1 << kF16TapExp);
@@ -451,7 +467,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       __syncwarp();
       if (lane == 0) {
         t6_arrive(&b_d1empty[db]);
-        t6_arrive(&b_qfull[db]);
+        t6_arrive(&b_qfull[n & 7]);
       }
     }
   } else {

@@ -295,6 +295,7 @@ struct Tpass3Params {
   long frame2;             // H*Wp/2 float2 per frame
   int T;
   float g[2 * kMaxRT + 1];
+  unsigned long long g2[2 * kMaxRT + 1];  // {g[i], g[i]} for fma.rn.f32x2
 };
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
@@ -340,11 +341,11 @@ __global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constan
     }
     cp_async_commit();
   };
-  float2 acc[3][NR];
+  unsigned long long acc[3][NR];   // packed float2 rings, updated with FFMA2
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int i = 0; i < NR; ++i) acc[c][i] = make_float2(0.f, 0.f);
+    for (int i = 0; i < NR; ++i) acc[c][i] = 0ull;
   float vm[3] = {0.f, 0.f, 0.f};
 #pragma unroll
   for (int d = 0; d < NS; ++d) issue(d);
@@ -363,15 +364,14 @@ __global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constan
         in[1] = make_float2(f.x * in[2].x, f.y * in[2].y);  // F^2 a = F (F a)
       }
       issue(jp + NS);
+      const unsigned long long in2[3] = {pack_f2(in[0].x, in[0].y), pack_f2(in[1].x, in[1].y),
+                                         pack_f2(in[2].x, in[2].y)};
 #pragma unroll
       for (int ee = 0; ee < NR; ++ee) {
         const int slot = (((d - 2 * RT + ee) % NR) + NR) % NR;
-        const float w = P.g[2 * RT - ee];
+        const unsigned long long w2 = P.g2[2 * RT - ee];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          acc[c][slot].x = fmaf(w, in[c].x, acc[c][slot].x);
-          acc[c][slot].y = fmaf(w, in[c].y, acc[c][slot].y);
-        }
+        for (int c = 0; c < 3; ++c) ffma2(acc[c][slot], w2, in2[c]);
       }
       const int slot0 = (((d - 2 * RT) % NR) + NR) % NR;
       const int t = jp - 2 * RT;
@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constan
 #pragma unroll
         for (int c = 0; c < 3; ++c) {   // planes [bt][plane][H][Wp] halves: hi, then lo at + frame2
           uint32_t h[2];
-          split_planes_f16<2>(acc[c][slot0].x * m16[c], acc[c][slot0].y * m16[c], h);
+          const float2 a2 = unpack_f2(acc[c][slot0]);
+          split_planes_f16<2>(a2.x * m16[c], a2.y * m16[c], h);
           uint32_t* o32 = reinterpret_cast<uint32_t*>(P.out[c]) + ((long)b * T + t) * 2 * P.frame2 + ec;
           __stcg(o32, h[0]);
           __stcg(o32 + P.frame2, h[1]);
@@ -387,13 +388,14 @@ __global__ void __launch_bounds__(kTpThreads) tpass3_kernel(const __grid_constan
       } else if (active && t >= 0 && t < T) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const float2 o = make_float2(acc[c][slot0].x * scale, acc[c][slot0].y * scale);
+          const float2 a2 = unpack_f2(acc[c][slot0]);
+          const float2 o = make_float2(a2.x * scale, a2.y * scale);
           __stcg(reinterpret_cast<float2*>(P.out[c]) + b * vol2 + ec + (long)t * P.frame2, o);
           vm[c] = fmaxf(vm[c], fmaxf(fabsf(o.x), fabsf(o.y)));
         }
       }
 #pragma unroll
-      for (int c = 0; c < 3; ++c) acc[c][slot0] = make_float2(0.f, 0.f);
+      for (int c = 0; c < 3; ++c) acc[c][slot0] = 0ull;
     }
   }
   cp_async_wait<0>();

@@ -148,8 +148,9 @@ def test_forward_path_selection(lib):
     assert m.forward_path(shp, m.Gauss(0.5, 1.0, 1, 3), m.ALGO_TWO_PASS)[0] == m.PATH_TWO_PASS_FP32
     assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS)[0] == m.PATH_TWO_PASS_TCGEN05
     assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_TCGEN05)[0] == m.PATH_TWO_PASS_TCGEN05
-    # radii outside the tcgen05 kernel's set (c5's r_s = 36): the mma.sync fp16 pass
-    assert m.forward_path(shp, m.Gauss(3.0, 12.0, 9, 36))[0] == m.PATH_TWO_PASS_TC_F16
+    # c5's r_s = 36 is in the tcgen05 kernel's set; r_s = 48 is not: the mma.sync fp16 pass
+    assert m.forward_path(shp, m.Gauss(3.0, 12.0, 9, 36))[0] == m.PATH_TWO_PASS_TCGEN05
+    assert m.forward_path(shp, m.Gauss(3.0, 16.0, 9, 48))[0] == m.PATH_TWO_PASS_TC_F16
     assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_MMA_SYNC)[0] == m.PATH_TWO_PASS_TC
     assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_FP32)[0] == m.PATH_TWO_PASS_FP32
     assert m.forward_path(shp, m.Gauss(2.0, 8.0, 6, 24), m.ALGO_TWO_PASS_MMA_F16)[0] == m.PATH_TWO_PASS_TC_F16

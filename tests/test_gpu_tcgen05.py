@@ -53,6 +53,9 @@ def _solve(sf, ch, w, g, K, rayleigh=False):
     (24, (1, 2, 1, 300)),      # H = 1
     (24, (1, 1, 5, 5)),        # tiny: pure padding around one partial block
     (24, (1, 20, 480, 260)),   # 960 units > 148 CTAs: segments of several y-blocks, Q ring wraps
+    (32, (1, 3, 150, 300)),    # 12 x-pass k steps (three full boxes)
+    (36, (1, 3, 150, 300)),    # c5's radius: four TMA boxes, chunk origin 64 rows above the segment
+    (36, (2, 12, 300, 200)),   # r_s = 36 with many units per CTA (segments of several y-blocks)
 ])
 def test_tcgen05_spatial_radii(sf, r_s, shape):
     B, T, H, W = shape

@@ -1,6 +1,6 @@
 """Debug harness for the tcgen05 spatial pass (spass_tc6.cuh): each case in its own process
 (a trap kills the context), x_K of the tcgen05 path against the mma.sync fp16 path, with the
-rows / columns where they disagree.   python tools/t6_debug.py B,T,H,W,r,K ..."""
+rows / columns where they disagree.   python tools/t6_debug.py B,T,H,W,r,K[,rayleigh] ..."""
 import subprocess
 import sys
 
@@ -9,13 +9,14 @@ import sys, numpy as np, torch
 sys.path.insert(0, ".")
 import paper_2212_08058_b200 as sf
 B, T, H, W, r, K = map(int, sys.argv[1:7])
+ray = len(sys.argv) > 7 and sys.argv[7] == "1"
 rng = np.random.default_rng(0)
 ch = torch.from_numpy((rng.random((B, 1, T, H, W)) * 0.8 + 0.1).astype(np.float32)).cuda()
 g = sf.Gauss(1.0, r / 3.0, 2, r)
 xs = {}
-for name, algo in (("t6", sf.ALGO_TWO_PASS_TCGEN05), ("mma", sf.ALGO_AUTO)):
+for name, algo in (("t6", sf.ALGO_TWO_PASS_TCGEN05), ("mma", sf.ALGO_TWO_PASS_MMA_F16)):
     s = sf.Solver((B, T, H, W), 1, g, K, algo=algo)
-    xs[name] = s.forward(ch, [1.0]).cpu().numpy().astype(np.float64)
+    xs[name] = s.forward(ch, [1.0], want_rayleigh=ray).cpu().numpy().astype(np.float64)
     xs[name + "_st"] = s.stats.cpu().numpy()
 a, b = xs["t6"], xs["mma"]
 rel = np.linalg.norm(a - b) / np.linalg.norm(b)
