@@ -34,6 +34,7 @@ struct BwdEpiParams {
   const double* tape_bin;  // [B][K][2] (theta in x units, n_pos) of the binarised iterations
   float kappa_prev;        // steepness of iteration k-1 (0: not binarised)
   double* loc;             // time slabs: per-volume local sums [B][2] (finalized after the allreduce)
+  unsigned* xbmax;         // max |x_bar_{k-1}| per volume (the next tcgen05 backward step's range) or null
   int B, T, H, W, Wp, gx, K, k;
 };
 
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(kEwThreads) bwd_epi_kernel(const __grid_consta
   const bool bin = kap > 0.f;  // iteration k-1 >= 1 was soft-binarised (then u2 != null)
   const float theta = bin ? (float)P.tape_bin[((long)b * P.K + (P.k - 2)) * 2] : 0.f;
   double acc = 0.0, acc2 = 0.0;
+  float xm = 0.f;
   for (int y = blockIdx.x; y < P.H; y += P.gx) {
     for (long x4 = threadIdx.x; x4 < W4; x4 += kEwThreads) {
       const long po = (long)bt * HWp + (long)y * P.Wp + 4 * x4;
@@ -91,9 +93,14 @@ __global__ void __launch_bounds__(kEwThreads) bwd_epi_kernel(const __grid_consta
       }
       *reinterpret_cast<float4*>(P.Fbar + po) = make_float4(fo[0], fo[1], fo[2], fo[3]);
       *reinterpret_cast<float4*>(P.xbar + po) = make_float4(xo[0], xo[1], xo[2], xo[3]);
+      xm = fmaxf(xm, fmaxf(fmaxf(fabsf(xo[0]), fabsf(xo[1])), fmaxf(fabsf(xo[2]), fabsf(xo[3]))));
       acc += (double)s;
       acc2 += (double)s2;
     }
+  }
+  if (P.xbmax) {
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(xm));
+    if ((threadIdx.x & 31) == 0) atomicMax(P.xbmax + (long)b * 2 * kScal, m);
   }
   const double s = block_sum<kEwThreads>(acc, red);
   const double s2 = bin ? block_sum<kEwThreads>(acc2, red) : 0.0;

@@ -13,6 +13,7 @@ cudaError_t launch_spass_bwd(int R, const SpassParams& P, int grid, cudaStream_t
 cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t st);
 // TP_FWD16: v written as two fp16 planes for the tcgen05 spatial pass (spass_tc6.cuh)
 cudaError_t launch_tpass_fwd16(int RT, const TpassParams& P, int B, cudaStream_t st);
+cudaError_t launch_tpass_bwd16(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st);
 cudaError_t launch_tpass_fwdf(int RT, const TpassParams& P, int B, cudaStream_t st);
 // f16: the three outputs as two fp16 planes each (the tcgen05 plain passes; Tpass3Params F16 fields)

@@ -25,6 +25,7 @@ struct CombineParams {
   unsigned* err;
   double* loc;          // time-slab mode: per-volume local sum of x_0^2 -> loc[2b]
   unsigned* pmax;       // max |p_0| per volume (float bits, stride 2 kScal words; tcgen05 pass) or null
+  unsigned* fmax;       // max |F| per volume (the tcgen05 backward's range bound) or null
   int B, C, T, H, W, Wp, act, gx;
   int in_T, in_t0;      // ch / x0 buffers hold in_T frames; this call's frame t is buffer frame in_t0 + t
   float bias;
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
   const float* chf = P.ch + (long)b * P.C * vol_dense + (long)(P.in_t0 + t) * HW;  // frame base, channel 0
   const long dbase = (long)b * vol_dense + (long)(P.in_t0 + t) * HW;              // dense x0 / F_out frame base
   double acc = 0.0;
-  float pm = 0.f;
+  float pm = 0.f, fm = 0.f;
   for (int y0 = blockIdx.x * kRows; y0 < P.H; y0 += P.gx * kRows) {
     for (int c0 = 0; c0 < P.Wp; c0 += kEwThreads * kCols) {
       float z[kRows][kCols];
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
             xx = P.x0 ? xv[r][i] : f;
             pv = f * xx;
             pm = fmaxf(pm, fabsf(pv));
+            fm = fmaxf(fm, fabsf(f));
             if (P.F_out) P.F_out[dbase + (long)y * P.W + x] = f;
             acc += (double)xx * (double)xx;
           }
@@ -106,6 +108,10 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
   if (P.pmax) {   // order-free max: one atomic per warp
     const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(pm));
     if ((threadIdx.x & 31) == 0) atomicMax(P.pmax + (long)b * 2 * kScal, m);
+  }
+  if (P.fmax) {
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(fm));
+    if ((threadIdx.x & 31) == 0) atomicMax(P.fmax + (long)b * 2 * kScal, m);
   }
   if (P.partials == nullptr) return;  // plain combine (sfseg_combine_channels): no reduction
   const double s = block_sum<kEwThreads>(acc, red);
@@ -296,6 +302,7 @@ struct BwdInitParams {
   double* loc;             // time slabs: per-volume local sums [B][2] (finalized after the allreduce)
   int B, T, H, W, Wp, K, gx;
   int g_T, g_t0;           // dL/dx buffer frames per volume and this slab's first frame in it
+  unsigned* xbmax;         // max |x_bar_K| per volume (float bits, stride 2 kScal words) or null
 };
 
 // x_bar_K = dL/dx_K, c_K = <x_K, x_bar_K>.  When iteration K was soft-binarised the output is
@@ -312,6 +319,7 @@ __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_const
   const float inv_nuK = (float)(1.0 / P.tape_nu[(long)b * P.K + (P.K - 1)]);
   const float theta = bin ? (float)P.tape_bin[((long)b * P.K + (P.K - 1)) * 2] : 0.f;
   double acc = 0.0, acc2 = 0.0;
+  float xm = 0.f;
   // row-parallel (see combine_kernel): no per-element index division
   for (int y = blockIdx.x; y < P.H; y += P.gx) {
     for (int c0 = 0; c0 < P.Wp; c0 += kEwThreads * kCols) {
@@ -337,13 +345,19 @@ __global__ void __launch_bounds__(kEwThreads) bwd_init_kernel(const __grid_const
           acc += (double)xk * (double)gg;
           acc2 += (double)gg;
           P.xbar[po] = gg;
+          xm = fmaxf(xm, fabsf(gg));
         } else {
           acc += (double)gv[i] * (double)fv[i] * (double)uv[i];
           P.xbar[po] = gv[i];
+          xm = fmaxf(xm, fabsf(gv[i]));
         }
         P.Fbar[po] = 0.f;
       }
     }
+  }
+  if (P.xbmax) {
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(xm));
+    if ((threadIdx.x & 31) == 0) atomicMax(P.xbmax + (long)b * 2 * kScal, m);
   }
   const double s = block_sum<kEwThreads>(acc, red);
   const double s2 = bin ? block_sum<kEwThreads>(acc2, red) : 0.0;

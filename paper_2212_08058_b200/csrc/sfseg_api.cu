@@ -1536,11 +1536,20 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
                                           (size_t)i * align_up(sizeof(float) * (size_t)P.vol_elems));
   };
 
+  // tcgen05 plain passes (the forward's plan): the temporal pass writes fp16 planes with an exponent
+  // from the range bound of A26; slots SC_VMAX + (k & 1): max |x_bar_k|; + 3: max |F|; + 4: max |F x_0|
+  const bool t6 = P.tc6;
+  double* const scb = at<double>(ws, P.off_sc);
+  auto bslot = [&](int j) { return reinterpret_cast<unsigned*>(scb + SC_VMAX + j); };
   CombineParams cp;
   fill_combine(cp, P, ch, w_host, b, act, ws);
   cp.x0 = x0;
   cp.F = F;
   cp.x0p = x0p;
+  if (t6) {
+    cp.fmax = bslot(3);
+    cp.pmax = bslot(4);
+  }
   combine_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(cp);
   SF_CUDA(after_launch("combine", st));
 
@@ -1566,6 +1575,7 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   ip.g_T = (int)P.T;
   ip.g_t0 = 0;
   ip.gx = P.gx;
+  if (t6) ip.xbmax = bslot(K & 1);
   bwd_init_kernel<<<dim3(P.gx, (unsigned)P.BT), kEwThreads, 0, st>>>(ip);
   SF_CUDA(after_launch("bwd_init", st));
 
@@ -1574,8 +1584,9 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   // spatial part of a backward step: on the tensor-core plan, u = G_xy * v by the
   // tensor-core pass in plain mode into a scratch volume, then the streaming epilogue
   // (bwd_epi_kernel); otherwise the FP32 pass with the fused epilogue (SP_BWD)
-  if (!(P.tc ? make_spass_fwd_tmap(&sp.tmap, P, v)
-             : make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))))
+  if (!(t6     ? make_planes_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp)
+         : P.tc ? make_spass_fwd_tmap(&sp.tmap, P, v)
+                : make_volume_tmap(&sp.tmap, v, P.W, P.H, P.BT, P.Wp, spass_boxw(P.RS))))
     return SFSEG_ERR_CUDA;
   fill_spass_common(sp, P, ws);
   sp.tape_nu = const_cast<double*>(tape_nu);
@@ -1608,10 +1619,28 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
   tp.src = xbar;
   tp.F = F;
   tp.out = v;
+  if (t6) {
+    float gt = 0.f, gs = 0.f;
+    for (int i = 0; i < 2 * P.RT + 1; ++i) gt += std::fabs(P.gt[i]);
+    for (int i = 0; i < 2 * P.RS + 1; ++i) gs += std::fabs(P.gs[i]);
+    tp.gsum = gt * (1.f + 1e-4f);
+    tp.gs3 = gt * gs * gs * (1.f + 1e-4f);
+    tp.fmax_in = bslot(3);
+    tp.vexp_out = scb + SC_VEXP;
+  }
   for (int k = K; k >= 1; --k) {
     tp.u1 = tape_u(k - 1);
-    set_vslot(tp, &sp, P, ws, k);
-    {
+    if (t6) {
+      tp.vmax = nullptr;
+      tp.pmax_in = bslot(k & 1);          // max |x_bar_k|
+      tp.pmax_zero = bslot((k - 1) & 1);  // for bwd_epi's max |x_bar_{k-1}|
+      tp.umax_in = bslot(k == 1 ? 4 : 3); // |u_1| <= gs3 max|F x_0|, |u_k| <= gs3 max|F| (x_{k-1} unit norm)
+      be.xbmax = bslot((k - 1) & 1);
+      ProfScope ps(P.prof, st, PC_BWD);
+      SF_CUDA(launch_tpass_bwd16(P.RT, tp, (int)P.B, st));
+      SF_CUDA(after_launch("tpass_bwd16", st));
+    } else {
+      set_vslot(tp, &sp, P, ws, k);
       ProfScope ps(P.prof, st, PC_BWD);
       SF_CUDA(launch_tpass_bwd(P.RT, tp, (int)P.B, st));
       SF_CUDA(after_launch("tpass_bwd", st));
@@ -1625,7 +1654,16 @@ sfseg_status sfseg_power_iterate_backward_ex(const float* ch, int32_t C, const f
       SpassParams pl = sp;
       pl.plain = 1;
       pl.out = ubuf;
-      {
+      if (t6) {
+        pl.S = P.S6;
+        pl.NB = P.NB6;
+        pl.U = P.U6;
+        pl.G = P.G6;
+        pl.eslot = 0;
+        ProfScope ps(P.prof, st, PC_BWD);
+        SF_CUDA(launch_spass_tc6(P.RS, pl, P.G6, st));
+        SF_CUDA(after_launch("spass_tc6(plain, bwd)", st));
+      } else {
         ProfScope ps(P.prof, st, PC_BWD);
         SF_CUDA(launch_spass_forward(P, pl, st));
         SF_CUDA(after_launch("spass_tc(plain, bwd)", st));

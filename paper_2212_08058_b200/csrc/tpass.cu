@@ -26,6 +26,9 @@ cudaError_t launch_tpass_fwd(int RT, const TpassParams& P, int B, cudaStream_t s
 cudaError_t launch_tpass_fwd16(int RT, const TpassParams& P, int B, cudaStream_t st) {
   return launch_tpass_t<TP_FWD16>(RT, P, B, st);
 }
+cudaError_t launch_tpass_bwd16(int RT, const TpassParams& P, int B, cudaStream_t st) {
+  return launch_tpass_t<TP_BWD16>(RT, P, B, st);
+}
 cudaError_t launch_tpass_bwd(int RT, const TpassParams& P, int B, cudaStream_t st) {
   return launch_tpass_t<TP_BWD>(RT, P, B, st);
 }

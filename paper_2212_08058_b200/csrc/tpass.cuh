@@ -21,6 +21,8 @@ enum TpassMode : int {
   TP_FWDF = 2,  // full SFSeg operator (f1): src = F^fexp * a, out = s_{k-1} * G_t * src  (Eq.7's three inputs)
   TP_FWD16 = 3, // as TP_FWD, out = the two fp16 planes of v 2^e ([bt][plane][H][Wp] halves, 4 B/voxel) for the
                 //   tcgen05 spatial pass (spass_tc6.cuh); e from max |p_{k-1}| so that |v 2^e| < 2^14
+  TP_BWD16 = 4, // as TP_BWD, out as TP_FWD16; e from the bound |src| <= max|F| (max|x_bar_k| + |corr| +
+                //   max|F| max|u| |cn|) |1/nu_k| (A26)
 };
 
 struct TpassParams {
@@ -36,6 +38,9 @@ struct TpassParams {
   unsigned* pmax_zero;     // FWD16: slot zeroed for the next spatial pass's max |p_k| (or null)
   double* vexp_out;        // FWD16: sc + SC_VEXP (stride kScal): the exponent e written per volume
   float gsum;              // FWD16: sum of |g| (|v| <= s gsum max |src|)
+  const unsigned* fmax_in; // BWD16: max |F|; pmax_in is then max |x_bar_k|
+  const unsigned* umax_in; // BWD16: max |F| (u_k, k >= 2) or max |F x_0| (u_1): |u| <= gs3 * it
+  float gs3;               // BWD16: sum|g_t| (sum|g_s|)^2
   int lag;               // FWD: no scale (the spatial pass applies s_{k-1}: lagged normalisation, time slabs)
   long frame4;           // H*Wp/4 float4 per frame
   int T;
@@ -103,8 +108,9 @@ template <int RT, int MODE, bool HALO>
 __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel(const __grid_constant__ TpassParams P) {
   constexpr int NR = 2 * RT + 1;
   constexpr int NS = tpass_stages(MODE);
-  constexpr bool F16 = MODE == TP_FWD16;
-  constexpr int NIN = (MODE == TP_FWD || F16) ? 1 : (MODE == TP_FWDF ? 2 : 3);
+  constexpr bool F16 = MODE == TP_FWD16 || MODE == TP_BWD16;   // fp16-plane output
+  constexpr bool FWDM = MODE == TP_FWD || MODE == TP_FWD16;     // input p (one stream)
+  constexpr int NIN = FWDM ? 1 : (MODE == TP_FWDF ? 2 : 3);
   __shared__ float4 sq[NS][NIN][kTpThreads];
   const int b = blockIdx.y;
   const int tid = threadIdx.x;
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   const float4* U1 = nullptr;
   float cn = 0.f, inv_nu = 0.f, corr = 0.f, scale = 1.f;
   float m16 = 1.f;  // FWD16: s_{k-1} 2^e
-  if (MODE == TP_FWD || F16) {
+  if (FWDM) {
     scale = P.lag ? 1.f : (float)P.sc[b * kScal + SC_S];
     if (F16) {
       const float bound = scale * __uint_as_float(P.pmax_in[(long)b * 2 * kScal]) * P.gsum;
@@ -140,6 +146,21 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
     cn = (float)P.sc[b * kScal + SC_CN];
     inv_nu = (float)P.sc[b * kScal + SC_INV_NU];
     corr = (float)P.sc[b * kScal + SC_CORR];  // 0 unless iteration k was soft-binarised
+    if (F16) {
+      const float mf = __uint_as_float(P.fmax_in[(long)b * 2 * kScal]);
+      const float bound = mf *
+                          (__uint_as_float(P.pmax_in[(long)b * 2 * kScal]) + fabsf(corr) +
+                           mf * P.gs3 * __uint_as_float(P.umax_in[(long)b * 2 * kScal]) * fabsf(cn)) *
+                          fabsf(inv_nu) * P.gsum;
+      int ex = 0;
+      if (bound > 0.f && bound <= 3.4e38f) frexpf(bound, &ex);
+      const int e = min(max(kF16DataExp - ex, -100), 100);
+      m16 = __int_as_float((127 + e) << 23);
+      if (blockIdx.x == 0 && tid == 0) {
+        P.vexp_out[(long)b * kScal] = (double)e;
+        if (P.pmax_zero) P.pmax_zero[(long)b * 2 * kScal] = 0u;
+      }
+    }
   }
   const float4* hlo = P.halo_lo ? reinterpret_cast<const float4*>(P.halo_lo) + (long)b * RT * P.frame4 + ec : nullptr;
   const float4* hhi = P.halo_hi ? reinterpret_cast<const float4*>(P.halo_hi) + (long)b * RT * P.frame4 + ec : nullptr;
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
     const int j = jp - RT;
     const int sl = jp % NS;
     float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (MODE == TP_FWD || F16) {
+    if (FWDM) {
       if (frame_src(jp, 0)) val = sq[sl][0][tid];
     } else if (MODE == TP_FWDF) {
       if (j >= 0 && j < T) {
@@ -204,7 +225,7 @@ __global__ void __launch_bounds__(kTpThreads, tpass_min_blocks(RT)) tpass_kernel
   };
 
   // forward: keep v in L2 for the spatial pass that reads it next (and its halo re-reads)
-  const uint64_t pol = (MODE == TP_FWD || F16) ? l2_policy_evict_last() : 0ull;
+  const uint64_t pol = (FWDM || F16) ? l2_policy_evict_last() : 0ull;
   uint2* const o16 = F16 ? reinterpret_cast<uint2*>(P.out) + (long)b * T * 2 * P.frame4 + ec : nullptr;
   // the ring of 2RT+1 partial outputs: float4 as two packed float2 (fma.rn.f32x2 = FFMA2: half
   // the FMA instructions of a pass that is issue-bound, profiles/r02e/tpass_ncu.txt)
