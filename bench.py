@@ -588,12 +588,14 @@ def run_ours(args):
                  "(fp32-class; DESIGN.md A23)")
     else:
         arith = "fp32 FFMA throughout"
+    # the arithmetic types that run: fp32 everywhere, except the tensor-core spatial pass's split operands
+    dtype = ("f32+f16x2split" if (path_t6 or path_f16) else "f32+bf16x3split" if path_tc else "f32")
     if rank == 0:
         ck = clocks.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if (slab or vshard) else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if (slab or vshard) else "weak", "vs_baseline": None, "dtype": dtype,
             "data": "synthetic (workloads/ generator; DAVIS-2016-shaped blobs, seed 0)",
             "config": {"workload": f"{args.config}: {cfg.note}", "shape": [B, T, H, W], "C": Cn,
                        "sigma_t": cfg.sigma_t, "sigma_s": cfg.sigma_s, "radius_t": r_t, "radius_s": r_s,
