@@ -50,6 +50,17 @@
 
 namespace sfseg {
 
+#ifndef T6_LDALL
+#define T6_LDALL 0  // A/B: splitters / epilogue read a whole D1 / D2 buffer in one TMEM round trip and release it
+#endif              //      before their stores (0: 32- / 16-column loads, each waited, buffer released at the end)
+#ifndef T6_XSTACK
+#define T6_XSTACK 1 // x-pass: the data planes stacked along N (one M128 N128 MMA per k step gives a_hi g_hi and
+#endif              //   a_lo g_hi side by side, one N64 MMA a_hi g_lo): 14 KB of operand reads per k step instead
+                    //   of 18 KB; D1 single-buffered (128 columns)
+#ifndef T6_L2PF
+#define T6_L2PF 0   // A/B: x-blocks (v boxes + F tile) the producer prefetches into L2 ahead of its loads (0: none)
+#endif
+
 constexpr int k6M = 128;        // output columns per strip (TMEM lanes, MMA M)
 constexpr int k6XN = 64;        // rows per x-block (x-pass MMA N): two ring chunks
 constexpr int k6YN = 64;        // rows per y-block (y-pass MMA N)
@@ -317,11 +328,34 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
   if (warp == 0) {
     // ================================================================== TMA producer
     if (lane == 0) {
+#if T6_L2PF > 0
+      // L2 prefetch cursor T6_L2PF x-blocks ahead of the loads (and the F tile of the y-block
+      // with the same index): DRAM latency is covered beyond the two shared-memory stages
+      long pu = u_begin;
+      int pi = 0;
+      T6Seg ps = pu < u_end ? t6_seg(pu, u_end, NBY, S, T) : T6Seg{};
+      auto l2pf = [&]() {
+        if (pu >= u_end) return;
+        const int prow = k6YN * ps.yb0 - 32 * OFF + k6XN * pi;
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx) tma_prefetch_3d(&P.tmap, ps.s * k6M - RA + k6BoxW * bx, prow, 2 * ps.bt);
+        if (!PLAIN && pi < ps.ny) tma_prefetch_3d(&P.fmap, ps.s * k6M, k6YN * (ps.yb0 + pi), ps.bt);
+        if (++pi >= t6_nx(R, ps.ny)) {
+          pu += ps.ny;
+          pi = 0;
+          if (pu < u_end) ps = t6_seg(pu, u_end, NBY, S, T);
+        }
+      };
+      for (int k = 0; k < T6_L2PF; ++k) l2pf();
+#endif
       unsigned n = 0;
       for (long u = u_begin; u < u_end;) {
         const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
         const int x0 = sg.s * k6M - RA;
         for (int i = 0; i < t6_nx(R, sg.ny); ++i, ++n) {
+#if T6_L2PF > 0
+          l2pf();
+#endif
           const unsigned st = n & 1;
           T6W(0, &b_sempty[st], ((n >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&b_sfull[st], SBYTES);
@@ -358,6 +392,33 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         yhave = true;
         return true;
       };
+#if T6_XSTACK
+      const uint32_t idx2 = t6_idesc(2 * k6XN);
+      auto issue_x = [&]() {
+        const unsigned st = nx & 1;
+        T6W(2, &b_sfull[st], (nx >> 1) & 1);
+        T6W(3, &b_d1empty[0], (nx & 1) ^ 1);
+        t6_fence_after();
+        const uint32_t d = tmem + k6ColD1;
+        const uint64_t bd0 = t6_desc_sw128(st0 + st * SBYTES);
+        // A: tap plane pg at k step s; B: k step s of the box, from data plane 0 (N = 64: plane 0 only,
+        // N = 128: planes 0 and 1, contiguous 64-row halves of the box)
+        auto adesc = [&](int pg, int s) {
+          return ad0 + (uint64_t)((pg * TXPL + (uint32_t)(-16 * s - TXMIN) * 32) >> 4);
+        };
+        auto bdesc = [&](int s) { return bd0 + (uint64_t)(((s >> 2) * k6BoxBytes + (s & 3) * 32) >> 4); };
+        // k step 0 of the leading tap plane initialises both halves [a_hi g_hi | a_lo g_hi]; then the
+        // correction a_hi g_lo (hi half), then the remaining leading k steps
+        t6_mma_ss_e(d, adesc(0, 0), bdesc(0), idx2, 0u);
+#pragma unroll
+        for (int s = 0; s < NKX; ++s) t6_mma_ss_e(d, adesc(1, s), bdesc(s), idx, 1u);
+#pragma unroll
+        for (int s = 1; s < NKX; ++s) t6_mma_ss_e(d, adesc(0, s), bdesc(s), idx2, 1u);
+        t6_commit_e(&b_sempty[st]);
+        t6_commit_e(&b_d1full[0]);
+        ++nx;
+      };
+#else
       auto issue_x = [&]() {
         const unsigned st = nx & 1, db = nx & 1;
         T6W(2, &b_sfull[st], (nx >> 1) & 1);
@@ -381,6 +442,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         t6_commit_e(&b_d1full[db]);
         ++nx;
       };
+#endif
       auto issue_y = [&]() {
         const unsigned need = yg0 + (unsigned)t6_xneed(R, yj);
         while (nq <= need) {
@@ -438,9 +500,85 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     constexpr float QSC = 1.f / (float)(1 << kF16TapExp);
 #pragma unroll 1
     for (unsigned n = 0; n < total; ++n) {
+#if T6_XSTACK
+      // D1 (single buffer) = [hi half | lo half]: the two halves summed in fp32, D1 released as soon as
+      // both 32-row chunks are in registers
+      T6W(6, &b_d1full[0], n & 1);
+      t6_fence_after();
+      float sum[2][32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t a[32], b[32];
+        __syncwarp();
+        t6_ld32(lanebase + k6ColD1 + 32 * c, a);
+        t6_ld32(lanebase + k6ColD1 + k6XN + 32 * c, b);
+        t6_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sum[c][i] = __uint_as_float(a[i]) + __uint_as_float(b[i]);
+      }
+      t6_fence_before();
+      __syncwarp();
+      if (lane == 0) t6_arrive(&b_d1empty[0]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          uint32_t pl[2];
+          split_planes_f16<2>(sum[c][2 * i] * QSC, sum[c][2 * i + 1] * QSC, pl);
+          hi[i] = pl[0];
+          lo[i] = pl[1];
+        }
+        const unsigned gc = 2 * n + c, slot = gc % k6Slots;
+        T6W(7, &b_sfree[slot], ((gc / k6Slots) & 1) ^ 1);
+        t6_fence_after();
+        __syncwarp();
+        t6_st16(lanebase + k6ColQ + 32 * slot, hi);
+        t6_st16(lanebase + k6ColQ + 32 * slot + 16, lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      t6_fence_before();
+      __syncwarp();
+      if (lane == 0) t6_arrive(&b_qfull[n & 7]);
+#else
       const unsigned db = n & 1;
       T6W(6, &b_d1full[db], (n >> 1) & 1);
       t6_fence_after();
+#endif
+#if T6_XSTACK
+#elif T6_LDALL
+      // both 32-row halves of D1 in one round trip; D1 is released before the split (the
+      // issuer's next x-pass into this buffer no longer waits for the stores into the ring)
+      uint32_t d[2][32];
+      __syncwarp();
+      t6_ld32(lanebase + k6ColD1 + k6XN * db, d[0]);
+      t6_ld32(lanebase + k6ColD1 + k6XN * db + 32, d[1]);
+      t6_wait_ld();
+      t6_fence_before();
+      __syncwarp();
+      if (lane == 0) t6_arrive(&b_d1empty[db]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          uint32_t pl[2];
+          split_planes_f16<2>(__uint_as_float(d[c][2 * i]) * QSC, __uint_as_float(d[c][2 * i + 1]) * QSC, pl);
+          hi[i] = pl[0];
+          lo[i] = pl[1];
+        }
+        const unsigned gc = 2 * n + c, slot = gc % k6Slots;
+        T6W(7, &b_sfree[slot], ((gc / k6Slots) & 1) ^ 1);
+        t6_fence_after();
+        __syncwarp();
+        t6_st16(lanebase + k6ColQ + 32 * slot, hi);
+        t6_st16(lanebase + k6ColQ + 32 * slot + 16, lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      t6_fence_before();
+      __syncwarp();
+      if (lane == 0) t6_arrive(&b_qfull[n & 7]);
+#else
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t d[32];
@@ -469,6 +607,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         t6_arrive(&b_d1empty[db]);
         t6_arrive(&b_qfull[n & 7]);
       }
+#endif
     }
   } else {
     // ================================================================== epilogue (warps 6-9)
@@ -554,6 +693,21 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         T6W(9, &b_d2full[buf], (m >> 1) & 1);
         t6_fence_after();
         float s0 = 0.f, s1 = 0.f;
+#if T6_LDALL
+        // the whole 64-row D2 buffer in one round trip, released before the stores
+        uint32_t qa[2][32];
+        __syncwarp();
+        t6_ld32(lanebase + k6ColD2 + k6YN * buf, qa[0]);
+        t6_ld32(lanebase + k6ColD2 + k6YN * buf + 32, qa[1]);
+        t6_wait_ld();
+        t6_fence_before();
+        __syncwarp();
+        if (lane == 0) t6_arrive(&b_d2empty[buf]);
+#pragma unroll
+        for (int c = 0; c < k6YN / 16; ++c) {
+          const uint32_t* q = &qa[c >> 1][16 * (c & 1)];
+          if (!xin) break;
+#else
 #pragma unroll 1
         for (int c = 0; c < k6YN / 16; ++c) {
           uint32_t q[16];
@@ -566,6 +720,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
               : "memory");
           t6_wait_ld();
           if (!xin) continue;
+#endif
           // one element per row: F from the shared tile, p (and the options) stored through
           // running pointers; full 16-row chunks take the branch-free path
           const int r0 = 16 * c;
@@ -615,9 +770,11 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
             }
           }
         }
+#if !T6_LDALL
         t6_fence_before();
         __syncwarp();
         if (lane == 0) t6_arrive(&b_d2empty[buf]);
+#endif
         if (!PLAIN) {
           asm volatile("bar.sync 2, 128;" ::: "memory");   // the group is done reading F tile buf
           if (fissuer) f_issue(buf);
