@@ -82,9 +82,9 @@ def main(src, dst):
             if os.path.basename(f).startswith("plain"):
                 continue
             shutil.copy(f, dst)
-    lf = os.path.join(src, "launches.csv")
-    if os.path.exists(lf):
-        with open(os.path.join(dst, "launches_summary.txt"), "w") as f:
+    for lf in sorted(glob.glob(os.path.join(src, "launches*.csv"))):   # launches.csv, launches_<config>.csv
+        tag = os.path.basename(lf)[len("launches"):-4]
+        with open(os.path.join(dst, f"launches_summary{tag}.txt"), "w") as f:
             f.write(launches_table(lf))
     traffic = {}
     for rep in sorted(glob.glob(os.path.join(src, "*.ncu-rep"))):
