@@ -208,6 +208,36 @@ __global__ void __launch_bounds__(kEwThreads) final_scale_kernel(const float* __
 
 // ------------------------------------------------------------------ threshold
 // Per-frame maximum in two deterministic steps (max is order independent):
+// Time slabs on the tcgen05 path: the temporal pass TP_FWD16 picks its fp16 exponent from
+// max |p_{k-1}| over every frame it reads, and the r_t halo frames received from the neighbour
+// slabs are among them.  halo_absmax_kernel folds max |halo| of volume blockIdx.y (halo
+// blockIdx.z: 0 lower, 1 upper; [B][n4] float4 each, null = absent) into the volume's slot
+// (float bits, order-free atomicMax; stride 2 kScal words as the spatial pass's own maximum).
+__global__ void __launch_bounds__(kEwThreads) halo_absmax_kernel(const float4* __restrict__ lo,
+                                                                 const float4* __restrict__ hi, long n4,
+                                                                 unsigned* slot) {
+  const float4* h = blockIdx.z == 0 ? lo : hi;
+  if (h == nullptr) return;
+  h += (long)blockIdx.y * n4;
+  float m = 0.f;
+  const long step = (long)gridDim.x * kEwThreads;
+  long e = (long)blockIdx.x * kEwThreads + threadIdx.x;
+  for (; e + 3 * step < n4; e += 4 * step) {
+    float4 a[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = __ldg(h + e + i * step);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(a[i].x), fabsf(a[i].y)), fmaxf(fabsf(a[i].z), fabsf(a[i].w))));
+  }
+  for (; e < n4; e += step) {
+    const float4 a = __ldg(h + e);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+  }
+  const unsigned w = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+  if ((threadIdx.x & 31) == 0 && w != 0u) atomicMax(slot + (long)blockIdx.y * 2 * kScal, w);
+}
+
 // frame_max_kernel writes one partial per (frame, block) -> part[bt * gx + bx],
 // threshold_kernel folds the gx partials of its frame (or of the whole volume).
 constexpr int kThrGx = 16;

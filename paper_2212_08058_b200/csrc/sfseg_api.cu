@@ -289,6 +289,14 @@ bool valid_algo(int32_t algo) {
          algo == SFSEG_ALGO_TWO_PASS_MMA_F16;
 }
 
+// Grid of the tcgen05 spatial pass over U units of B volumes x S strips: one CTA per SM; a
+// multiple of B x S when that fits, so CTA ranges align with strips (spass_tc6.cuh).
+int tc6_grid(int64_t B, int64_t S, int64_t U) {
+  const int64_t bs = B * S, sms = num_sms();
+  const int64_t g = bs <= sms ? bs * (sms / bs) : sms;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, U));
+}
+
 sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan* P,
                        const sfseg_options* opt = nullptr) {
   const int algo = opt ? opt->algo : SFSEG_ALGO_AUTO;
@@ -342,11 +350,7 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->S6 = (int)((sh.W + k6M - 1) / k6M);
   P->NB6 = (int)((sh.H + k6YN - 1) / k6YN);
   P->U6 = P->BT * P->S6 * P->NB6;
-  {  // one CTA per SM; a multiple of B x S when that fits, so CTA ranges align with strips (spass_tc6.cuh)
-    const int64_t bs = P->B * P->S6, sms = num_sms();
-    const int64_t g = bs <= sms ? bs * (sms / bs) : sms;
-    P->G6 = (int)std::max<int64_t>(1, std::min<int64_t>(g, P->U6));
-  }
+  P->G6 = tc6_grid(P->B, P->S6, P->U6);
   P->Gcap_tc = num_sms() * spass_tc_occupancy(P->RS, P->f16 ? 1 : 0);
   P->Gtc = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)P->Gcap_tc, P->U / 4));
   P->f3d = algo == SFSEG_ALGO_AUTO && !P->bin && f3d_supported(P->RT, P->RS);
@@ -573,8 +577,16 @@ sfseg_status rank_setup(Rank& r, cudaStream_t st) {
   r.glob = at<double>(r.ws, r.so.off_glob);
   SF_CUDA(clear_header(r.ws, P.off_part, st));
   std::memset(&r.sp, 0, sizeof(r.sp));
-  if (!make_spass_fwd_tmap(&r.sp.tmap, P, r.v)) return SFSEG_ERR_CUDA;
+  // the slab runs the single-GPU plan's spatial pass: tcgen05 (v as fp16 planes, F by TMA) when the
+  // plan says so, else the mma.sync / FP32 pass
+  if (!(P.tc6 ? make_planes_tmap(&r.sp.tmap, r.v, P.W, P.H, P.BT, P.Wp) : make_spass_fwd_tmap(&r.sp.tmap, P, r.v)))
+    return SFSEG_ERR_CUDA;
+  if (P.tc6 && !make_volume_tmap(&r.sp.fmap, r.F, P.W, P.H, P.BT, P.Wp, k6M, k6YN)) return SFSEG_ERR_CUDA;
   fill_spass_common(r.sp, P, r.ws);
+  if (P.tc6) {
+    r.sp.S = P.S6;
+    r.sp.NB = P.NB6;
+  }
   r.sp.stats = r.stats;
   r.sp.loc = r.loc;
   r.sp.tape_nu = nullptr;   // nu_k is written by the post-allreduce finalize
@@ -586,6 +598,12 @@ sfseg_status rank_setup(Rank& r, cudaStream_t st) {
   r.tp.halo_hi = r.has_hi ? r.hhi : nullptr;
   r.tp.lag = 1;   // lagged normalisation (slab_iterations)
   r.sp.lag = 1;
+  if (P.tc6) {
+    float gsum = 0.f;
+    for (int i = 0; i < 2 * P.RT + 1; ++i) gsum += std::fabs(P.gt[i]);
+    r.tp.gsum = gsum * (1.f + 1e-5f);   // |v| <= gsum max |p| over the slab's frames and its halos
+    r.tp.vexp_out = at<double>(r.ws, P.off_sc) + SC_VEXP;
+  }
   return SFSEG_OK;
 }
 
@@ -598,6 +616,7 @@ sfseg_status ph_combine(Rank& r, const float* w_host, float b, int act, cudaStre
   cp.loc = r.loc;
   cp.in_T = r.in_T;
   cp.in_t0 = r.in_t0;
+  if (r.P.tc6) cp.pmax = reinterpret_cast<unsigned*>(at<double>(r.ws, r.P.off_sc) + SC_VMAX);   // max |p_0|
   combine_kernel<<<dim3(r.P.gx, (unsigned)r.P.BT), kEwThreads, 0, st>>>(cp);
   SF_CUDA(after_launch("combine(slab)", st));
   return SFSEG_OK;
@@ -620,9 +639,29 @@ sfseg_status ph_finalize(Rank& r, int k, cudaStream_t st) {
 }
 
 sfseg_status ph_T(Rank& r, int k, cudaStream_t st) {
-  set_vslot(r.tp, &r.sp, r.P, r.ws, k);
-  ProfScope ps(r.P.prof, st, PC_TPASS);
-  SF_CUDA(launch_tpass_fwd(r.P.RT, r.tp, (int)r.P.B, st));
+  const Plan& P = r.P;
+  if (P.tc6) {
+    // v as two fp16 planes of v 2^e: e from max |p_{k-1}| over the slab's own frames (slot (k-1) & 1,
+    // written by the combine / the spatial pass's range launches) and the received halo frames
+    double* const scv = at<double>(r.ws, P.off_sc);
+    unsigned* const pin = reinterpret_cast<unsigned*>(scv + SC_VMAX + ((k - 1) & 1));
+    if (r.tp.halo_lo || r.tp.halo_hi) {
+      const long n4 = (long)P.RT * P.H * P.Wp / 4;
+      const unsigned gx = (unsigned)std::max<long>(1, std::min<long>(64, n4 / (4 * kEwThreads)));
+      halo_absmax_kernel<<<dim3(gx, (unsigned)P.B, 2), kEwThreads, 0, st>>>(
+          reinterpret_cast<const float4*>(r.tp.halo_lo), reinterpret_cast<const float4*>(r.tp.halo_hi), n4, pin);
+      SF_CUDA(after_launch("halo_absmax(slab)", st));
+    }
+    r.tp.pmax_in = pin;
+    r.tp.pmax_zero = reinterpret_cast<unsigned*>(scv + SC_VMAX + (k & 1));
+    ProfScope ps(P.prof, st, PC_TPASS);
+    SF_CUDA(launch_tpass_fwd16(P.RT, r.tp, (int)P.B, st));
+    SF_CUDA(after_launch("tpass16(slab)", st));
+    return SFSEG_OK;
+  }
+  set_vslot(r.tp, &r.sp, P, r.ws, k);
+  ProfScope ps(P.prof, st, PC_TPASS);
+  SF_CUDA(launch_tpass_fwd(P.RT, r.tp, (int)P.B, st));
   SF_CUDA(after_launch("tpass(slab)", st));
   return SFSEG_OK;
 }
@@ -672,7 +711,14 @@ sfseg_status ph_S_range(Rank& r, int k, int t_lo, int t_cnt, int acc, cudaStream
   r.sp.t_cnt = t_cnt;
   r.sp.loc_acc = acc;
   ProfScope ps(r.P.prof, st, PC_SPASS);
-  SF_CUDA(launch_spass_forward(r.P, r.sp, st));
+  if (r.P.tc6) {
+    r.sp.pslot = r.sp.last ? 0 : (k & 1) + 1;   // max |p_k| of the range for the next temporal pass
+    r.sp.U = r.P.B * (int64_t)t_cnt * r.P.S6 * r.P.NB6;
+    r.sp.G = tc6_grid(r.P.B, r.P.S6, r.sp.U);
+    SF_CUDA(launch_spass_tc6(r.P.RS, r.sp, r.sp.G, st));
+  } else {
+    SF_CUDA(launch_spass_forward(r.P, r.sp, st));
+  }
   SF_CUDA(after_launch("spass(slab)", st));
   return SFSEG_OK;
 }
@@ -1124,7 +1170,6 @@ sfseg_status dist_power_iterate(const float* ch, int32_t C, const float* w_host,
   if (agreed != SFSEG_OK) return agreed;  // a peer failed its validation: nobody starts the solve
   Rank r;
   r.P = P;
-  r.P.tc6 = false;  // time slabs: frame-range launches and the lagged scale are in the mma.sync / FP32 passes
   r.ch = ch;
   r.x0 = x0;
   r.in_T = (int)P.T;
@@ -2394,7 +2439,6 @@ sfseg_status sfseg_power_iterate_slabs(const float* ch, int32_t C, const float* 
     sfseg_shape ls = sh;
     ls.T = t1 - t0;
     if ((s = make_plan(ls, C, gauss, K, &R[i].P, opt)) != SFSEG_OK) return s;
-    R[i].P.tc6 = false;  // as in dist_power_iterate
     if (tape) {
       R[i].tape = static_cast<char*>(tape) + toff;
       toff += align_up(R[i].P.tape_bytes);

@@ -217,14 +217,19 @@ __device__ __forceinline__ int t6_vexp(const SpassParams& P, int b) {
 struct T6Seg {
   int bt, s, yb0, ny;
 };
-__device__ __forceinline__ T6Seg t6_seg(long u, long u_end, int NBY, int S, int T) {
+// Frame-range launches (time-slab schedule, P.t_cnt > 0): the units cover frames
+// [t_lo, t_lo + t_cnt) of every volume only; T6Frames carries the range.
+struct T6Frames {
+  int T, t_lo, t_cnt;   // frames per volume, first frame and frame count of the launch
+};
+__device__ __forceinline__ T6Seg t6_seg(long u, long u_end, int NBY, int S, T6Frames fr) {
   const long col = u / NBY;                 // (b, s, t)
   const int yb0 = (int)(u - col * NBY);
-  const int t = (int)(col % T);
-  const long bs = col / T;
+  const int t = (int)(col % fr.t_cnt);
+  const long bs = col / fr.t_cnt;
   const int s = (int)(bs % S);
   const int b = (int)(bs / S);
-  return T6Seg{b * T + t, s, yb0, (int)min((long)NBY - yb0, u_end - u)};
+  return T6Seg{b * fr.T + fr.t_lo + t, s, yb0, (int)min((long)NBY - yb0, u_end - u)};
 }
 
 template <int R, int EPI>
@@ -267,6 +272,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = P.H, W = P.W, Wp = P.Wp, S = P.S, T = P.T, NBY = P.NB;
+  const T6Frames FR{T, P.t_cnt > 0 ? P.t_lo : 0, P.t_cnt > 0 ? P.t_cnt : T};
 #ifdef T6_PROFILE
   long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const long long prof_t0 = clock64();
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       // with the same index): DRAM latency is covered beyond the two shared-memory stages
       long pu = u_begin;
       int pi = 0;
-      T6Seg ps = pu < u_end ? t6_seg(pu, u_end, NBY, S, T) : T6Seg{};
+      T6Seg ps = pu < u_end ? t6_seg(pu, u_end, NBY, S, FR) : T6Seg{};
       auto l2pf = [&]() {
         if (pu >= u_end) return;
         const int prow = k6YN * ps.yb0 - 32 * OFF + k6XN * pi;
@@ -343,14 +349,14 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
         if (++pi >= t6_nx(R, ps.ny)) {
           pu += ps.ny;
           pi = 0;
-          if (pu < u_end) ps = t6_seg(pu, u_end, NBY, S, T);
+          if (pu < u_end) ps = t6_seg(pu, u_end, NBY, S, FR);
         }
       };
       for (int k = 0; k < T6_L2PF; ++k) l2pf();
 #endif
       unsigned n = 0;
       for (long u = u_begin; u < u_end;) {
-        const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
+        const T6Seg sg = t6_seg(u, u_end, NBY, S, FR);
         const int x0 = sg.s * k6M - RA;
         for (int i = 0; i < t6_nx(R, sg.ny); ++i, ++n) {
 #if T6_L2PF > 0
@@ -386,7 +392,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
           yg0 += (unsigned)t6_nx(R, ys.ny);
         }
         if (yu >= u_end) return false;
-        ys = t6_seg(yu, u_end, NBY, S, T);
+        ys = t6_seg(yu, u_end, NBY, S, FR);
         yj = 0;
         yrel = 0;
         yhave = true;
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       };
       bool ymore = y_next();
       for (long u = u_begin; u < u_end;) {
-        const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
+        const T6Seg sg = t6_seg(u, u_end, NBY, S, FR);
         for (int i = 0; i < t6_nx(R, sg.ny); ++i) {
           issue_x();
           // y-blocks whose x-blocks were all issued before this one (their split ran under it)
@@ -493,7 +499,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     // ================================================================== splitters (warps 2-5)
     unsigned total = 0;
     for (long u = u_begin; u < u_end;) {
-      const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
+      const T6Seg sg = t6_seg(u, u_end, NBY, S, FR);
       total += (unsigned)t6_nx(R, sg.ny);
       u += sg.ny;
     }
@@ -658,7 +664,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
       }
       if (!fhave) {
         if (fu >= u_end) return;
-        fs = t6_seg(fu, u_end, NBY, S, T);
+        fs = t6_seg(fu, u_end, NBY, S, FR);
         fj = 0;
         fhave = true;
       }
@@ -672,7 +678,7 @@ __global__ void __launch_bounds__(k6Threads, 1) spass_tc6_kernel(const __grid_co
     }
     unsigned m = 0;
     for (long u = u_begin; u < u_end;) {
-      const T6Seg sg = t6_seg(u, u_end, NBY, S, T);
+      const T6Seg sg = t6_seg(u, u_end, NBY, S, FR);
       const int vol = sg.bt / T;
       if (vol != cur_vol) {
         if (cur_vol >= 0 && !PLAIN) flush(cur_vol);

@@ -52,6 +52,33 @@ def test_slabs_match_single_gpu_and_oracle(sf, name, shape, nslabs, K):
     np.testing.assert_allclose(sts.cpu().numpy()[..., 1], sto["gain"], rtol=1e-5)
 
 
+def test_slab_fp16_range_covers_halo_frames(sf):
+    """tcgen05 path in slabs: the temporal pass writes v as fp16 planes scaled by 2^e, e from
+    max |p_{k-1}| over the frames it READS -- the neighbour's halo frames included.  A dim slab
+    (1e-4 x the brightness of its neighbour) would overflow fp16 on its boundary frames if only
+    its own maximum set the range."""
+    cfg = WL.get_config("c2", T=28, H=70, W=150)
+    wl = WL.generate("c2", cfg=cfg)
+    chn = wl.ch.copy()
+    chn[:, :, :14] *= 1e-4          # slab 0 of 2 is dim, slab 1 bright
+    g = sf.Gauss(cfg.sigma_t, cfg.sigma_s, cfg.radius_t, cfg.radius_s)
+    B, C, T, H, W = chn.shape
+    assert sf.forward_path((B, T // 2, H, W), g, sf.ALGO_AUTO)[0] == sf.PATH_TWO_PASS_TCGEN05
+    ch = torch.from_numpy(chn).cuda()
+    K = 4
+    xs, sts = sf.power_iterate_slabs(ch, wl.w, g, K, 2, want_rayleigh=True)
+    xs = xs.cpu().numpy()
+    assert np.isfinite(xs).all()
+    F, _ = O.combine(chn, wl.w)
+    xo, sto = O.power_iterate(F, O.gaussian_taps(cfg.sigma_t, cfg.radius_t),
+                              O.gaussian_taps(cfg.sigma_s, cfg.radius_s), K)
+    assert _rel(xs[0], xo[0]) <= 1e-4
+    # the dim slab's frames next to the bright one are where an overflow would show
+    fr = slice(14 - cfg.radius_t, 14)
+    assert _rel(xs[0][fr], xo[0][fr]) <= 1e-4
+    np.testing.assert_allclose(sts.cpu().numpy()[..., 1], sto["gain"], rtol=1e-5)
+
+
 def test_slab_too_thin_rejected(sf):
     ch = torch.rand((1, 1, 8, 20, 20), device="cuda")
     with pytest.raises(sf.SfsegError) as e:
