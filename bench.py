@@ -572,6 +572,40 @@ def run_ours(args):
         e2e["unpipelined_value"] = units_per_step * 2 / (time.perf_counter() - t0)
         del x_hosts, m_hosts, d_ch
 
+    # ---------------------------------------------------------------- the same step on FP32 FMA arithmetic only
+    fp32_arm = None
+    if path_tc and world == 1 and not slab and not full and not train and not args.no_fp32_arm:
+        # north_star asks for fp32 arithmetic; the default spatial pass runs on the tensor pipe in split
+        # fp16 operands (fp32-class, see "arithmetic").  Time the SAME step (combine, K iterations, final
+        # scale, threshold) with every pass on FP32 FFMA (SFSEG_ALGO_TWO_PASS_FP32) in the same run, and
+        # report how far the two x_K are apart.
+        x_def = x.clone()
+        s32 = sf.Solver((B, T, H, W), Cn, gauss, K, device=dev, algo=sf.ALGO_TWO_PASS_FP32)
+
+        def step32():
+            s32.forward(ch, wl.w, wl.b, cfg.act, x_out=x, check=False)
+            thr_solver.threshold(x, cfg.tau, sf.THR_PER_FRAME_MAX, mask=mask)
+
+        n32 = max(2, min(args.steps, 10))
+        for _ in range(max(args.warmup, 3)):
+            step32()
+        s32.sync()
+        torch.cuda.synchronize(dev)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(n32):
+            step32()
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        s32.sync()
+        ms32 = a0.elapsed_time(a1) / n32
+        diff = float(torch.linalg.vector_norm((x.double() - x_def.double())) / torch.linalg.vector_norm(x.double()))
+        fp32_arm = {"value": units_per_step / (ms32 * 1e-3), "unit": UNIT, "ms_per_step": ms32, "steps": n32,
+                    "dtype": "f32", "algo": "SFSEG_ALGO_TWO_PASS_FP32 (temporal pass + FP32-FMA spatial pass, "
+                                            "stream launches)",
+                    "x_K_rel_l2_vs_default_path": diff}
+        del s32, x_def
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(args.config)
@@ -611,7 +645,7 @@ def run_ours(args):
                         "max": float(max(step_ms)), "rank": rank},
             "once_per_solve_ms_per_step": prof["once"][0] / args.steps,   # combine + final scale (events)
             "path_hbm_frac_12B_nameplate_8TBs": 12.0 * value / world / 1e9 / 8000.0,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "fp32_ffma_arm": fp32_arm,
             "gpu_launches": n_launch + (int(prof["backward"][1]) + 2 * args.steps if train else 0),
             "clocks": {k: ck[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
             "clock_samples": ck["samples"],
@@ -641,6 +675,8 @@ def main():
     ap.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4", "c5", "probe", "c2f"],
                     help="default: c2 at N=1, c5 (time slabs) at N>1, c4 with --shard volume")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-fp32-arm", action="store_true",
+                    help="skip the FP32-FMA-only arm of the same step (reported as fp32_ffma_arm)")
     ap.add_argument("--algo", default="auto", choices=["auto", "tcgen05", "mma", "fp32", "f16"],
                     help="forward path (sfseg_options.algo): auto, the tcgen05/TMEM spatial pass, the mma.sync "
                          "one, or the FP32-FMA one")

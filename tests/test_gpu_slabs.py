@@ -29,6 +29,7 @@ def _rel(a, b):
     ("c2", dict(T=26, H=70, W=150), 2, 6),
     ("c2", dict(T=26, H=70, W=150), 4, 6),      # uneven: 6,7,6,7 frames, r_t = 6
     ("c5", dict(T=40, H=64, W=140), 3, 5),      # r_t = 9, r_s = 36
+    ("c5", dict(T=40, H=200, W=300), 2, 4),     # several y-blocks and strips per frame-range launch (tcgen05 pass)
     ("c4", dict(B=2, T=23, H=48, W=70), 2, 5),  # B > 1
 ])
 def test_slabs_match_single_gpu_and_oracle(sf, name, shape, nslabs, K):
