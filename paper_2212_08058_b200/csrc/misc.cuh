@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
           xv[r][i] = 0.f;
           if (P.x0 && y < P.H && x < P.W) xv[r][i] = __ldcs(P.x0 + dbase + (long)y * P.W + x);
         }
+      float ps = 0.f;  // ||x_0||^2 of this thread's kRows x kCols values in fp32, then into the fp64 sum
+                       // (as the spatial pass's norm partials: one fp64 add per 16 values, not per value)
 #pragma unroll
       for (int r = 0; r < kRows; ++r)
 #pragma unroll
@@ -97,12 +99,13 @@ __global__ void __launch_bounds__(kEwThreads) combine_kernel(const __grid_consta
             pm = fmaxf(pm, fabsf(pv));
             fm = fmaxf(fm, fabsf(f));
             if (P.F_out) P.F_out[dbase + (long)y * P.W + x] = f;
-            acc += (double)xx * (double)xx;
+            ps = fmaf(xx, xx, ps);
           }
           P.F[po] = f;  // pad columns x >= W hold zeros
           if (P.p0) P.p0[po] = pv;
           if (P.x0p) P.x0p[po] = xx;
         }
+      acc += (double)ps;
     }
   }
   if (P.pmax) {   // order-free max: one atomic per warp
@@ -200,14 +203,13 @@ __global__ void __launch_bounds__(kEwThreads) final_scale_kernel(const float* __
 #pragma unroll
         for (int i = 0; i < kCols; ++i) {
           const int yy = y0 + r, xx = c0 + i * kEwThreads + threadIdx.x;
-          if (yy < H && xx < W) __stcs(xo + (long)yy * W + xx, v[r][i] * s);
+          if (yy < H && xx < W) xo[(long)yy * W + xx] = v[r][i] * s;   // plain store: the threshold's frame max reads x next
         }
     }
   }
 }
 
-// ------------------------------------------------------------------ threshold
-// Per-frame maximum in two deterministic steps (max is order independent):
+// ------------------------------------------------------------------ time-slab fp16 range
 // Time slabs on the tcgen05 path: the temporal pass TP_FWD16 picks its fp16 exponent from
 // max |p_{k-1}| over every frame it reads, and the r_t halo frames received from the neighbour
 // slabs are among them.  halo_absmax_kernel folds max |halo| of volume blockIdx.y (halo
@@ -238,13 +240,18 @@ __global__ void __launch_bounds__(kEwThreads) halo_absmax_kernel(const float4* _
   if ((threadIdx.x & 31) == 0 && w != 0u) atomicMax(slot + (long)blockIdx.y * 2 * kScal, w);
 }
 
+// ------------------------------------------------------------------ threshold
+// Per-frame maximum in two deterministic steps (max is order independent):
 // frame_max_kernel writes one partial per (frame, block) -> part[bt * gx + bx],
 // threshold_kernel folds the gx partials of its frame (or of the whole volume).
 constexpr int kThrGx = 16;
 
 __global__ void __launch_bounds__(kEwThreads) frame_max_kernel(const float* __restrict__ x, float* part, long HW) {
   __shared__ float red[kEwThreads / 32];
-  const float* xf = x + (long)blockIdx.y * HW;
+  // frames last to first: x was just written first to last (final scale), so the frames still in
+  // L2 are read first; the threshold kernel then walks first to last over what this pass read last
+  const long bt = (long)gridDim.y - 1 - blockIdx.y;
+  const float* xf = x + bt * HW;
   float m = -INFINITY;
   const bool vec = ((HW & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   if (vec) {
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(kEwThreads) frame_max_kernel(const float* __re
   if (threadIdx.x == 0) {
     float r = red[0];
     for (int i = 1; i < kEwThreads / 32; ++i) r = fmaxf(r, red[i]);
-    part[(long)blockIdx.y * gridDim.x + blockIdx.x] = r;
+    part[bt * gridDim.x + blockIdx.x] = r;
   }
 }
 
