@@ -341,7 +341,7 @@ sfseg_status make_plan(sfseg_shape sh, int32_t C, sfseg_gauss g, int32_t K, Plan
   P->Gcap = (int)cap;
   P->gx = ew_gx(P->H, P->BT);
   P->tc = algo != SFSEG_ALGO_TWO_PASS_FP32 && spass_tc_supported(P->RS);
-  // the hot forward's default spatial pass (r_s in 8..24, no soft-binarisation): tcgen05 / TMEM
+  // the hot forward's default spatial pass (r_s in 8..36, no soft-binarisation; single GPU and time slabs): tcgen05 / TMEM
   P->tc6 = P->tc && spass_tc6_supported(P->RS) && !P->bin &&
            (algo == SFSEG_ALGO_AUTO || algo == SFSEG_ALGO_TWO_PASS || algo == SFSEG_ALGO_TWO_PASS_TCGEN05);
   // the forward's default tensor-core format is two fp16 planes (A25); SFSEG_ALGO_TWO_PASS_MMA_SYNC
